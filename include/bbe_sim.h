@@ -1,0 +1,157 @@
+/*
+ * bbe_sim.h -- C-ABI of the B200-native batched Monte Carlo race simulator.
+ *
+ * This is the drop-in boundary for the Bristol Betting Exchange dry-run hot path.  The reference
+ * (racemarket, pure Python) has no FFI layer; each entry point below replaces a group of reference
+ * functions, cited as /root/reference/pkg/src/racemarket/<file>:<line>:
+ *
+ *   bbe_simulate          race.py:393-406  simulate_from(state, config, seed)      (batched over sims)
+ *                         race.py:373-390  run_race(config, seed, record=False)    (from_start = 1)
+ *                         agents.py:153-166 rp_predict(state, config, d, rng)      (wins -> (w+1)/(d+n))
+ *                         batch.py:110-124 run_batch(BatchConfig)                  (per-sim outputs)
+ *                         batch.py:149-170 estimate_pmf / pmf_from_results         (perms tally, n <= 6)
+ *   bbe_simulate_async    the same, device-resident: tallies accumulate into a device buffer on a
+ *                         caller stream (used by the multi-GPU path before one NCCL all-reduce).
+ *   bbe_derive_seeds      seeding.py:50-59 derive_seed(master, "run", i) for a range of i.
+ *   bbe_last_error        -- (error text for the Python exceptions of race.py:27-32, batch.py:30-38)
+ *
+ * All types are plain C; no torch or CUDA types appear.  Host pointers are caller-owned and only
+ * touched during the call.  Calls on one device are serialised by the library.
+ *
+ * Return codes: BBE_OK, BBE_EINVAL (-> RaceConfigError), BBE_EDIVERGED (-> RaceDivergedError /
+ * BatchRunError(first_diverged)), BBE_EDRAWS (inject stream under/over-consumed), BBE_ECUDA,
+ * BBE_ENODEV.
+ */
+#ifndef BBE_SIM_H
+#define BBE_SIM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BBE_ABI_VERSION 1
+#define BBE_MAX_COMPETITORS 128
+#define BBE_MAX_PERM_COMPETITORS 6 /* batch.py:27 MAX_FULL_OUTCOME_COMPETITORS */
+
+enum {
+    BBE_OK = 0,
+    BBE_EINVAL = 1,
+    BBE_EDIVERGED = 2,
+    BBE_EDRAWS = 3,
+    BBE_ECUDA = 4,
+    BBE_ENODEV = 5
+};
+
+/* Random-draw source. */
+enum {
+    BBE_MODE_NATIVE = 0, /* in-register Philox4x32-10, FP32 race state: statistically equivalent */
+    BBE_MODE_INJECT = 1, /* recorded reference draws (CSR), FP64 state: bit-exact to the reference */
+    BBE_MODE_MT = 2      /* CPython MT19937 from per-sim seeds, FP64 state: bit-exact from seeds */
+};
+
+enum { BBE_FAMILY_UNIFORM = 0, BBE_FAMILY_LOGNORMAL = 1 };
+
+/* race.py:158-189 (RaceConfig); dt, conditions and betting_close do not enter a step. */
+typedef struct {
+    double track_length;
+    int64_t tick_limit; /* race.py:165; run_race checks it absolutely, simulate_from relatively */
+    int32_t n;          /* competitors, 1..BBE_MAX_COMPETITORS */
+    int32_t _pad;
+} bbe_race;
+
+/* race.py:35-116 (UniformSteps / LogNormalSteps / Responsiveness / Competitor), with the two
+ * per-competitor constants the reference recomputes every step hoisted by the host in double:
+ *   pref_factor = preference_factor(conditions, preference, pref_sensitivity)   race.py:192-199
+ *   bp_abs      = breakpoint * track_length                                      race.py:94      */
+typedef struct {
+    int32_t family; /* BBE_FAMILY_* */
+    int32_t _pad;
+    double lo, hi;            /* uniform */
+    double mu, sigma, scale;  /* lognormal: scale * exp(N(mu, sigma)) */
+    double pref_factor;
+    double theta;             /* blocking threshold */
+    double early_mult, late_mult, bp_abs;
+} bbe_competitor;
+
+/* race.py:207-230 (RaceState).  Ignored when from_start != 0 (run_race: positions 0, previous
+ * steps primed by one free draw each, race.py:233-241). */
+typedef struct {
+    int64_t tick;
+    const double* positions;     /* [n] */
+    const double* prev_steps;    /* [n] */
+    const int64_t* finish_ticks; /* [n], -1 = still racing (None) */
+    int32_t from_start;
+    int32_t _pad;
+} bbe_state;
+
+typedef struct {
+    int64_t n_sims;
+    int64_t sim_offset;   /* global index of this call's first sim (multi-GPU sharding) */
+    uint64_t seed;        /* NATIVE: Philox key */
+    int32_t mode;         /* BBE_MODE_* */
+    int32_t lanes_per_slot_hint; /* 0 = auto; else competitors per lane K (tuning) */
+    /* INJECT: draws of sim s are draws[draw_offsets[s] .. draw_offsets[s+1]) in consumption order */
+    const double* draws;
+    const int64_t* draw_offsets; /* [n_sims + 1] */
+    /* MT: per-sim CPython seeds (e.g. rp_predict's getrandbits(64) stream); NULL -> derive_seed(
+     * seed_master, "run", sim_offset + s) as run_batch does */
+    const uint64_t* seeds;
+    uint64_t seed_master;
+} bbe_request;
+
+/* Outputs.  Tally pointers (host for bbe_simulate) may be NULL except wins. */
+typedef struct {
+    uint64_t* wins;          /* [n]   winner counts (rp_predict tally) */
+    uint64_t* ranks;         /* [n*n] ranks[c*n + r] = sims where competitor c finished at rank r */
+    uint64_t* perms;         /* [n!]  full finish-order histogram by Lehmer index (n <= 6) */
+    int32_t* winner;         /* [n_sims] */
+    int32_t* order;          /* [n_sims*n] finish order (competitor indices) */
+    int64_t* finish_ticks;   /* [n_sims*n] */
+    double* final_positions; /* [n_sims*n] (FP32 state widened in NATIVE mode) */
+    int64_t* blocked;        /* [n_sims] blocked steps per sim */
+    int64_t* draws_used;     /* [n_sims] (INJECT / MT) */
+    uint64_t competitor_steps; /* total racing competitor-timesteps (ct) */
+    uint64_t blocked_steps;
+    int64_t first_diverged;  /* global sim index of the first diverged sim, -1 none */
+    int64_t first_bad_draws; /* INJECT: first sim whose draw stream mismatched, -1 none */
+    float kernel_ms;         /* device time of the race kernel(s) */
+    int32_t lanes_per_slot;  /* K actually used */
+} bbe_result;
+
+int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_state* state,
+                 const bbe_request* req, bbe_result* out);
+
+/* Device-resident variant.  All pointers in req/state are HOST except draws/draw_offsets/seeds,
+ * which must be DEVICE pointers; per-sim output pointers in `dev_out` are DEVICE pointers or NULL.
+ * Tallies are ADDED into d_tally (device, bbe_tally_len(n) u64, layout below) on `stream`
+ * (a cudaStream_t, NULL = legacy default).  Asynchronous: read d_tally after the stream syncs. */
+int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const bbe_state* state,
+                       const bbe_request* req, const bbe_result* dev_out, uint64_t* d_tally, void* stream);
+
+/* d_tally layout: [wins n][ranks n*n][perms n! or 0][ct][blocked][diverged count][bad-draw count]
+ *                 [~(first_diverged + 1) or 0 = none][~(first_bad_draws + 1) or 0 = none]
+ * Every field but the last two is SUM-reduced across shards; the last two are MAX-reduced (the bit
+ * complement turns "smallest sim index" into "largest value"). */
+int64_t bbe_tally_len(int32_t n);
+int64_t bbe_tally_offset(int32_t n, int32_t field); /* field: 0 wins 1 ranks 2 perms 3 ct 4 blocked
+                                                       5 n_diverged 6 n_bad 7 first_div 8 first_bad */
+
+int bbe_derive_seeds(uint64_t master, int64_t first, int64_t count, uint64_t* out_host);
+
+/* Device time (ms) of the race kernel of the most recent call on the current device; synchronises
+ * on that kernel's completion event. */
+float bbe_last_kernel_ms(void);
+
+const char* bbe_last_error(void);
+int bbe_version(void);
+int bbe_device_count(void);
+/* Fills name (NUL-terminated, up to 63 chars), SM count and max SM clock (kHz). */
+int bbe_device_info(int device, char* name64, int32_t* sm_count, int32_t* clock_khz);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BBE_SIM_H */

@@ -1,0 +1,502 @@
+// bbe_sim.cu -- C-ABI (include/bbe_sim.h) over the sm_100a race kernels.
+//
+// Host responsibilities: validate (race.py:175-189 errors), pack the race into a small SoA parameter
+// block (one H2D copy), size a persistent grid to residency on this GPU, launch, and bring tallies
+// (and optional per-sim records) back.  One context per device: cached device buffers, a private
+// stream, and a mutex serialising calls on that device.  No CPU fallback exists: every entry point
+// that needs a GPU returns BBE_ENODEV / BBE_ECUDA when there is none.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/bbe_sim.h"
+#include "race_kernel.cuh"
+
+using namespace bbe;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define BBE_CK(x)                                                                                \
+    do {                                                                                         \
+        cudaError_t e_ = (x);                                                                    \
+        if (e_ != cudaSuccess) return fail(BBE_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max(bytes, (size_t)4096);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+};
+
+struct HostBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max(bytes, (size_t)4096);
+        cudaError_t e = cudaMallocHost(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+};
+
+struct DevCtx {
+    std::mutex mu;
+    int dev = -1;
+    bool ready = false;
+    int sm_count = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    HostBuf h_params, h_tally;
+    DevBuf d_params, d_tally, d_draws, d_offsets, d_winner, d_order, d_fin, d_fpos, d_blocked, d_dused;
+};
+
+std::mutex g_ctx_mu;
+std::vector<DevCtx*> g_ctx;
+
+int get_ctx(DevCtx** out) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(BBE_ENODEV, "no CUDA device visible (the simulator has no CPU fallback)");
+    }
+    int dev = 0;
+    BBE_CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> g(g_ctx_mu);
+    if ((int)g_ctx.size() < ndev) g_ctx.resize(ndev, nullptr);
+    if (!g_ctx[dev]) g_ctx[dev] = new DevCtx();
+    DevCtx* c = g_ctx[dev];
+    if (!c->ready) {
+        c->dev = dev;
+        BBE_CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, dev));
+        BBE_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        BBE_CK(cudaEventCreate(&c->ev0));
+        BBE_CK(cudaEventCreate(&c->ev1));
+        c->ready = true;
+    }
+    *out = c;
+    return BBE_OK;
+}
+
+int64_t factorial(int n) {
+    int64_t f = 1;
+    for (int i = 2; i <= n; ++i) f *= i;
+    return f;
+}
+
+int nperm_for(int n) { return n <= BBE_MAX_PERM_COMPETITORS ? (int)factorial(n) : 0; }
+
+// race.py:175-189 / :42-44 / :62-66 / :87-91 / :108-116 (ids are checked by the Python host)
+int validate(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, const bbe_request* rq) {
+    if (!race || !comps || !st || !rq) return fail(BBE_EINVAL, "null argument");
+    const int n = race->n;
+    if (n < 1 || n > BBE_MAX_COMPETITORS)
+        return fail(BBE_EINVAL, "n must be in [1, " + std::to_string(BBE_MAX_COMPETITORS) + "], got " + std::to_string(n));
+    if (!(race->track_length > 0.0)) return fail(BBE_EINVAL, "track_length must be > 0");
+    if (race->tick_limit < 1) return fail(BBE_EINVAL, "tick_limit must be >= 1");
+    for (int c = 0; c < n; ++c) {
+        const bbe_competitor& p = comps[c];
+        if (p.family == BBE_FAMILY_UNIFORM) {
+            if (!(0.0 < p.lo && p.lo <= p.hi)) return fail(BBE_EINVAL, "uniform steps need 0 < lo <= hi");
+        } else if (p.family == BBE_FAMILY_LOGNORMAL) {
+            if (p.sigma < 0.0) return fail(BBE_EINVAL, "lognormal sigma must be >= 0");
+            if (!(p.scale > 0.0)) return fail(BBE_EINVAL, "lognormal scale must be > 0");
+        } else {
+            return fail(BBE_EINVAL, "unknown step family");
+        }
+        if (p.theta < 0.0) return fail(BBE_EINVAL, "theta must be >= 0");
+        if (!(p.early_mult > 0.0) || !(p.late_mult > 0.0)) return fail(BBE_EINVAL, "responsiveness multipliers must be > 0");
+        if (!(p.pref_factor > 0.0)) return fail(BBE_EINVAL, "pref_factor must be > 0");
+    }
+    if (!st->from_start && (!st->positions || !st->prev_steps || !st->finish_ticks))
+        return fail(BBE_EINVAL, "continuation state needs positions, prev_steps and finish_ticks");
+    if (rq->n_sims < 0 || rq->sim_offset < 0) return fail(BBE_EINVAL, "n_sims and sim_offset must be >= 0");
+    if (rq->mode == BBE_MODE_INJECT) {
+        if (!rq->draws || !rq->draw_offsets) return fail(BBE_EINVAL, "inject mode needs draws and draw_offsets");
+    } else if (rq->mode == BBE_MODE_MT) {
+        return fail(BBE_EINVAL, "mode MT is not available in this build");
+    } else if (rq->mode != BBE_MODE_NATIVE) {
+        return fail(BBE_EINVAL, "unknown mode");
+    }
+    return BBE_OK;
+}
+
+// Choose competitors-per-lane K: maximise occupied slots (n * sims-per-warp) / (32 * K); ties -> smaller K.
+int choose_k(int n, int hint) {
+    static const int ks[] = {1, 2, 3, 4};
+    if (hint > 0) {
+        for (int k : ks)
+            if (k == hint && (n + k - 1) / k <= kWarp) return k;
+    }
+    int best = -1;
+    double best_u = -1;
+    for (int k : ks) {
+        const int w = (n + k - 1) / k;
+        if (w > kWarp) continue;
+        const int s = kWarp / w;
+        const double u = (double)n * s / (kWarp * k);
+        if (u > best_u + 1e-9) { best_u = u; best = k; }
+    }
+    return best;
+}
+
+void pack_params(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, double* P) {
+    const int n = race->n;
+    for (int c = 0; c < n; ++c) {
+        const bbe_competitor& p = comps[c];
+        P[F_LO * n + c] = p.lo;
+        P[F_SPAN * n + c] = p.hi - p.lo;  // uniform(a, b) = a + (b - a) * random()
+        P[F_LMU * n + c] = p.mu + std::log(p.family == BBE_FAMILY_LOGNORMAL ? p.scale : 1.0);
+        P[F_SIGMA * n + c] = p.sigma;
+        P[F_SCALE * n + c] = p.scale;
+        P[F_MU * n + c] = p.mu;
+        P[F_RP_EARLY * n + c] = p.early_mult * p.pref_factor;  // (resp * pref), race.py:273
+        P[F_RP_LATE * n + c] = p.late_mult * p.pref_factor;
+        P[F_EARLY * n + c] = p.early_mult;
+        P[F_LATE * n + c] = p.late_mult;
+        P[F_BP * n + c] = p.bp_abs;
+        P[F_THETA * n + c] = p.theta;
+        if (st->from_start) {
+            P[F_POS0 * n + c] = 0.0;
+            P[F_PREV0 * n + c] = 0.0;
+            P[F_FIN0 * n + c] = -1.0;
+        } else {
+            P[F_POS0 * n + c] = st->positions[c];
+            P[F_PREV0 * n + c] = st->prev_steps[c];
+            P[F_FIN0 * n + c] = (double)(st->finish_ticks[c] < 0 ? -1 : st->finish_ticks[c]);
+        }
+        P[F_FAMILY * n + c] = (double)p.family;
+    }
+}
+
+typedef void (*KernelFn)(LaunchArgs);
+
+KernelFn pick_kernel(int mode, int k) {
+    if (mode == BBE_MODE_INJECT) {
+        switch (k) {
+            case 1: return race_kernel<double, 1, INJECT>;
+            case 2: return race_kernel<double, 2, INJECT>;
+            case 3: return race_kernel<double, 3, INJECT>;
+            case 4: return race_kernel<double, 4, INJECT>;
+        }
+    } else {
+        switch (k) {
+            case 1: return race_kernel<float, 1, NATIVE>;
+            case 2: return race_kernel<float, 2, NATIVE>;
+            case 3: return race_kernel<float, 3, NATIVE>;
+            case 4: return race_kernel<float, 4, NATIVE>;
+        }
+    }
+    return nullptr;
+}
+
+struct Plan {
+    int n, K, W, S, nperm, tally_len;
+    size_t smem;
+    KernelFn fn;
+    int grid;
+};
+
+int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_request* rq, int want_perms, Plan* pl) {
+    const int n = race->n;
+    pl->n = n;
+    pl->K = choose_k(n, rq->lanes_per_slot_hint);
+    if (pl->K < 0) return fail(BBE_EINVAL, "field too large for one warp");
+    pl->W = (n + pl->K - 1) / pl->K;
+    pl->S = kWarp / pl->W;
+    pl->nperm = want_perms ? nperm_for(n) : 0;
+    TallyLayout TL{n, pl->nperm};
+    pl->tally_len = TL.len();
+    pl->smem = (size_t)TL.smem_len() * sizeof(unsigned long long);
+    pl->fn = pick_kernel(rq->mode, pl->K);
+    if (!pl->fn) return fail(BBE_EINVAL, "no kernel for this configuration");
+    if (pl->smem > 48 * 1024) {
+        BBE_CK(cudaFuncSetAttribute((const void*)pl->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->smem));
+    }
+    int per_sm = 0;
+    BBE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl->fn, kBlockThreads, pl->smem));
+    if (per_sm < 1) per_sm = 1;
+    const int64_t sims_per_block = (int64_t)(kBlockThreads / kWarp) * pl->S;
+    const int64_t need = (rq->n_sims + sims_per_block - 1) / sims_per_block;
+    const int64_t cap = (int64_t)per_sm * ctx->sm_count;
+    pl->grid = (int)std::max<int64_t>(1, std::min(need, cap));
+    return BBE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bbe_version(void) { return BBE_ABI_VERSION; }
+
+float bbe_last_kernel_ms(void) {
+    DevCtx* ctx = nullptr;
+    if (get_ctx(&ctx)) return -1.f;
+    std::lock_guard<std::mutex> guard(ctx->mu);
+    if (cudaEventSynchronize(ctx->ev1) != cudaSuccess) return -1.f;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) != cudaSuccess) {
+        cudaGetLastError();
+        return -1.f;
+    }
+    return ms;
+}
+
+const char* bbe_last_error(void) { return g_err.c_str(); }
+
+int bbe_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int bbe_device_info(int device, char* name64, int32_t* sm_count, int32_t* clock_khz) {
+    cudaDeviceProp p;
+    BBE_CK(cudaGetDeviceProperties(&p, device));
+    if (name64) {
+        std::strncpy(name64, p.name, 63);
+        name64[63] = 0;
+    }
+    if (sm_count) *sm_count = p.multiProcessorCount;
+    int clk = 0;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, device);
+    if (clock_khz) *clock_khz = clk;
+    return BBE_OK;
+}
+
+int64_t bbe_tally_len(int32_t n) {
+    if (n < 1 || n > BBE_MAX_COMPETITORS) return -1;
+    return TallyLayout{n, nperm_for(n)}.len();
+}
+
+int64_t bbe_tally_offset(int32_t n, int32_t field) {
+    if (n < 1 || n > BBE_MAX_COMPETITORS) return -1;
+    TallyLayout T{n, nperm_for(n)};
+    switch (field) {
+        case 0: return T.wins();
+        case 1: return T.ranks();
+        case 2: return T.perms();
+        case 3: return T.ct();
+        case 4: return T.blocked();
+        case 5: return T.n_div();
+        case 6: return T.n_bad();
+        case 7: return T.first_div();
+        case 8: return T.first_bad();
+    }
+    return -1;
+}
+
+// seeding.py:24-59, the per-run seeds of batch.py:117-119
+static uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+static uint64_t fnv1a(const unsigned char* b, int len) {
+    uint64_t h = 0xCBF29CE484222325ull;
+    for (int i = 0; i < len; ++i) h = (h ^ b[i]) * 0x100000001B3ull;
+    return h;
+}
+
+int bbe_derive_seeds(uint64_t master, int64_t first, int64_t count, uint64_t* out) {
+    if (!out || count < 0) return fail(BBE_EINVAL, "bad arguments");
+    const unsigned char run[5] = {'s', ':', 'r', 'u', 'n'};
+    const uint64_t h0 = splitmix64(splitmix64(master) ^ fnv1a(run, 5));
+    for (int64_t j = 0; j < count; ++j) {
+        const uint64_t i = (uint64_t)(first + j);
+        unsigned char b[10] = {'i', ':'};
+        for (int k = 0; k < 8; ++k) b[2 + k] = (unsigned char)(i >> (56 - 8 * k));
+        out[j] = splitmix64(h0 ^ fnv1a(b, 10));
+    }
+    return BBE_OK;
+}
+
+static int launch_go(const Plan& pl, LaunchArgs& a, const bbe_competitor* comps, cudaStream_t stream) {
+    a.scan = 0;
+    for (int c = 0; c < a.n; ++c)
+        if (comps[c].theta > 0.0) a.scan = 1;
+    if (a.n_sims == 0) return BBE_OK;
+    pl.fn<<<pl.grid, kBlockThreads, pl.smem, stream>>>(a);
+    BBE_CK(cudaGetLastError());
+    return BBE_OK;
+}
+
+static int build_args(const Plan& pl, const bbe_race* race, const bbe_state* st, const bbe_request* rq,
+                      const double* d_params, const double* d_draws, const int64_t* d_offsets, uint64_t* d_tally,
+                      const bbe_result* dev_out, LaunchArgs* out) {
+    LaunchArgs& a = *out;
+    a = LaunchArgs{};
+    a.P = d_params;
+    a.n = race->n;
+    a.W = pl.W;
+    a.S = pl.S;
+    a.from_start = st->from_start ? 1 : 0;
+    a.perms = pl.nperm;
+    a.L = race->track_length;
+    a.tick0 = st->from_start ? 0 : st->tick;
+    a.tick_limit = race->tick_limit;
+    a.n_sims = rq->n_sims;
+    a.sim_offset = rq->sim_offset;
+    a.seed = rq->seed;
+    a.draws = d_draws;
+    a.draw_offsets = d_offsets;
+    a.tally = d_tally;
+    if (dev_out) {
+        a.winner = dev_out->winner;
+        a.order = dev_out->order;
+        a.finish_ticks = dev_out->finish_ticks;
+        a.final_pos = dev_out->final_positions;
+        a.blocked = dev_out->blocked;
+        a.draws_used = dev_out->draws_used;
+    }
+    return BBE_OK;
+}
+
+int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, const bbe_request* rq,
+                 bbe_result* out) {
+    int rc = validate(race, comps, st, rq);
+    if (rc) return rc;
+    if (!out || !out->wins) return fail(BBE_EINVAL, "result needs a wins buffer");
+    DevCtx* ctx = nullptr;
+    if ((rc = get_ctx(&ctx))) return rc;
+    std::lock_guard<std::mutex> guard(ctx->mu);
+    const int n = race->n;
+    const int64_t ns = rq->n_sims;
+    Plan pl;
+    if ((rc = make_plan(ctx, race, rq, out->perms != nullptr, &pl))) return rc;
+    cudaStream_t s = ctx->stream;
+
+    // parameters: one pinned staging block, one H2D copy
+    const size_t pbytes = (size_t)F_COUNT * n * sizeof(double);
+    BBE_CK(ctx->h_params.ensure(pbytes));
+    BBE_CK(ctx->d_params.ensure(pbytes));
+    pack_params(race, comps, st, (double*)ctx->h_params.p);
+    BBE_CK(cudaMemcpyAsync(ctx->d_params.p, ctx->h_params.p, pbytes, cudaMemcpyHostToDevice, s));
+
+    const double* d_draws = nullptr;
+    const int64_t* d_offsets = nullptr;
+    if (rq->mode == BBE_MODE_INJECT) {
+        const int64_t nd = rq->draw_offsets[ns];
+        if (rq->draw_offsets[0] != 0 || nd < 0) return fail(BBE_EINVAL, "draw_offsets must start at 0 and be non-decreasing");
+        BBE_CK(ctx->d_draws.ensure((size_t)std::max<int64_t>(nd, 1) * sizeof(double)));
+        BBE_CK(ctx->d_offsets.ensure((size_t)(ns + 1) * sizeof(int64_t)));
+        if (nd) BBE_CK(cudaMemcpyAsync(ctx->d_draws.p, rq->draws, (size_t)nd * sizeof(double), cudaMemcpyHostToDevice, s));
+        BBE_CK(cudaMemcpyAsync(ctx->d_offsets.p, rq->draw_offsets, (size_t)(ns + 1) * sizeof(int64_t),
+                               cudaMemcpyHostToDevice, s));
+        d_draws = (const double*)ctx->d_draws.p;
+        d_offsets = (const int64_t*)ctx->d_offsets.p;
+    }
+
+    const size_t tbytes = (size_t)pl.tally_len * sizeof(uint64_t);
+    BBE_CK(ctx->d_tally.ensure(tbytes));
+    BBE_CK(ctx->h_tally.ensure(tbytes));
+    BBE_CK(cudaMemsetAsync(ctx->d_tally.p, 0, tbytes, s));
+
+    bbe_result dev{};
+    const size_t nsn = (size_t)ns * n;
+    if (out->winner) { BBE_CK(ctx->d_winner.ensure(ns * sizeof(int32_t))); dev.winner = (int32_t*)ctx->d_winner.p; }
+    if (out->order) { BBE_CK(ctx->d_order.ensure(nsn * sizeof(int32_t))); dev.order = (int32_t*)ctx->d_order.p; }
+    if (out->finish_ticks) { BBE_CK(ctx->d_fin.ensure(nsn * sizeof(int64_t))); dev.finish_ticks = (int64_t*)ctx->d_fin.p; }
+    if (out->final_positions) { BBE_CK(ctx->d_fpos.ensure(nsn * sizeof(double))); dev.final_positions = (double*)ctx->d_fpos.p; }
+    if (out->blocked) { BBE_CK(ctx->d_blocked.ensure(ns * sizeof(int64_t))); dev.blocked = (int64_t*)ctx->d_blocked.p; }
+    if (out->draws_used && rq->mode == BBE_MODE_INJECT) {
+        BBE_CK(ctx->d_dused.ensure(ns * sizeof(int64_t)));
+        dev.draws_used = (int64_t*)ctx->d_dused.p;
+    }
+
+    LaunchArgs a;
+    build_args(pl, race, st, rq, (const double*)ctx->d_params.p, d_draws, d_offsets, (uint64_t*)ctx->d_tally.p, &dev, &a);
+    BBE_CK(cudaEventRecord(ctx->ev0, s));
+    if ((rc = launch_go(pl, a, comps, s))) return rc;
+    BBE_CK(cudaEventRecord(ctx->ev1, s));
+
+    BBE_CK(cudaMemcpyAsync(ctx->h_tally.p, ctx->d_tally.p, tbytes, cudaMemcpyDeviceToHost, s));
+    if (out->winner && ns) BBE_CK(cudaMemcpyAsync(out->winner, dev.winner, ns * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    if (out->order && ns) BBE_CK(cudaMemcpyAsync(out->order, dev.order, nsn * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    if (out->finish_ticks && ns)
+        BBE_CK(cudaMemcpyAsync(out->finish_ticks, dev.finish_ticks, nsn * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    if (out->final_positions && ns)
+        BBE_CK(cudaMemcpyAsync(out->final_positions, dev.final_positions, nsn * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (out->blocked && ns) BBE_CK(cudaMemcpyAsync(out->blocked, dev.blocked, ns * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    if (dev.draws_used && ns)
+        BBE_CK(cudaMemcpyAsync(out->draws_used, dev.draws_used, ns * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    BBE_CK(cudaStreamSynchronize(s));
+
+    const uint64_t* T = (const uint64_t*)ctx->h_tally.p;
+    TallyLayout TL{n, pl.nperm};
+    std::memcpy(out->wins, T + TL.wins(), n * sizeof(uint64_t));
+    if (out->ranks) std::memcpy(out->ranks, T + TL.ranks(), (size_t)n * n * sizeof(uint64_t));
+    if (out->perms && pl.nperm) std::memcpy(out->perms, T + TL.perms(), (size_t)pl.nperm * sizeof(uint64_t));
+    out->competitor_steps = T[TL.ct()];
+    out->blocked_steps = T[TL.blocked()];
+    out->first_diverged = T[TL.first_div()] ? (int64_t)(~T[TL.first_div()]) - 1 : -1;
+    out->first_bad_draws = T[TL.first_bad()] ? (int64_t)(~T[TL.first_bad()]) - 1 : -1;
+    float ms = 0.f;
+    if (ns) cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    out->kernel_ms = ms;
+    out->lanes_per_slot = pl.K;
+    if (T[TL.n_div()]) return fail(BBE_EDIVERGED, "race exceeded tick_limit=" + std::to_string(race->tick_limit) +
+                                                      " in sim " + std::to_string(out->first_diverged));
+    if (T[TL.n_bad()]) return fail(BBE_EDRAWS, "injected draw stream under/over-consumed in sim " +
+                                                   std::to_string(out->first_bad_draws));
+    return BBE_OK;
+}
+
+int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, const bbe_request* rq,
+                       const bbe_result* dev_out, uint64_t* d_tally, void* stream) {
+    int rc = validate(race, comps, st, rq);
+    if (rc) return rc;
+    if (!d_tally) return fail(BBE_EINVAL, "d_tally is required");
+    DevCtx* ctx = nullptr;
+    if ((rc = get_ctx(&ctx))) return rc;
+    std::lock_guard<std::mutex> guard(ctx->mu);
+    Plan pl;
+    const bool perms = nperm_for(race->n) > 0;
+    if ((rc = make_plan(ctx, race, rq, perms, &pl))) return rc;
+    cudaStream_t s = stream ? (cudaStream_t)stream : ctx->stream;
+    // parameters: staged through pinned memory; the copy is ordered on `s` before the kernel, and
+    // the staging block is not reused until that copy has been consumed (sync on an event).
+    const size_t pbytes = (size_t)F_COUNT * race->n * sizeof(double);
+    BBE_CK(ctx->h_params.ensure(pbytes));
+    BBE_CK(ctx->d_params.ensure(pbytes));
+    BBE_CK(cudaEventSynchronize(ctx->ev1));  // previous async launch on this ctx has read its params
+    pack_params(race, comps, st, (double*)ctx->h_params.p);
+    BBE_CK(cudaMemcpyAsync(ctx->d_params.p, ctx->h_params.p, pbytes, cudaMemcpyHostToDevice, s));
+    LaunchArgs a;
+    build_args(pl, race, st, rq, (const double*)ctx->d_params.p, rq->draws, rq->draw_offsets, d_tally, dev_out, &a);
+    BBE_CK(cudaEventRecord(ctx->ev0, s));
+    if ((rc = launch_go(pl, a, comps, s))) return rc;
+    BBE_CK(cudaEventRecord(ctx->ev1, s));
+    return BBE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,378 @@
+"""ctypes binding of the C-ABI (include/bbe_sim.h) and the batched simulation API.
+
+``simulate_batch`` is the one call everything else goes through: it packs a race (reference
+``RaceConfig`` / ``RaceState`` or this package's mirrors, duck-typed) into the POD structs of the
+header, hoists the two per-competitor constants the reference recomputes every step
+(``preference_factor``, race.py:192-199, and ``breakpoint * track_length``, race.py:94) in Python
+double exactly as the reference evaluates them, and calls ``bbe_simulate``.
+
+There is no CPU path: if ``_lib/libbbe_sim.so`` is missing or no GPU is visible, calls raise
+``BackendUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from .race import (
+    RaceConfigError,
+    RaceDivergedError,
+    Trajectory,
+    preference_factor,
+    validate_config,
+)
+
+_LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
+LIB_PATH = os.path.join(_LIB_DIR, "libbbe_sim.so")
+
+BBE_OK, BBE_EINVAL, BBE_EDIVERGED, BBE_EDRAWS, BBE_ECUDA, BBE_ENODEV = range(6)
+MODES = {"native": 0, "inject": 1, "mt": 2}
+MAX_COMPETITORS = 128
+MAX_PERM_COMPETITORS = 6
+M64 = (1 << 64) - 1
+
+EXPORTED_SYMBOLS = (
+    "bbe_simulate",
+    "bbe_simulate_async",
+    "bbe_tally_len",
+    "bbe_tally_offset",
+    "bbe_derive_seeds",
+    "bbe_last_error",
+    "bbe_version",
+    "bbe_device_count",
+    "bbe_device_info",
+    "bbe_last_kernel_ms",
+)
+
+
+class BackendUnavailable(RuntimeError):
+    """The CUDA library is not built or no GPU is visible (there is deliberately no CPU fallback)."""
+
+
+class DrawStreamError(RuntimeError):
+    """Inject mode: a sim consumed fewer or more recorded draws than it was given."""
+
+    def __init__(self, sim_index: int, message: str):
+        super().__init__(message)
+        self.sim_index = sim_index
+
+
+class SimDivergedError(RaceDivergedError):
+    def __init__(self, sim_index: int, message: str):
+        super().__init__(message)
+        self.sim_index = sim_index
+
+
+# -- ctypes mirrors of the header structs -------------------------------------------------------
+
+
+class BbeRace(ctypes.Structure):
+    _fields_ = [("track_length", ctypes.c_double), ("tick_limit", ctypes.c_int64), ("n", ctypes.c_int32),
+                ("_pad", ctypes.c_int32)]
+
+
+class BbeCompetitor(ctypes.Structure):
+    _fields_ = [("family", ctypes.c_int32), ("_pad", ctypes.c_int32), ("lo", ctypes.c_double),
+                ("hi", ctypes.c_double), ("mu", ctypes.c_double), ("sigma", ctypes.c_double),
+                ("scale", ctypes.c_double), ("pref_factor", ctypes.c_double), ("theta", ctypes.c_double),
+                ("early_mult", ctypes.c_double), ("late_mult", ctypes.c_double), ("bp_abs", ctypes.c_double)]
+
+
+_P = ctypes.POINTER
+
+
+class BbeState(ctypes.Structure):
+    _fields_ = [("tick", ctypes.c_int64), ("positions", _P(ctypes.c_double)), ("prev_steps", _P(ctypes.c_double)),
+                ("finish_ticks", _P(ctypes.c_int64)), ("from_start", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+
+
+class BbeRequest(ctypes.Structure):
+    _fields_ = [("n_sims", ctypes.c_int64), ("sim_offset", ctypes.c_int64), ("seed", ctypes.c_uint64),
+                ("mode", ctypes.c_int32), ("lanes_per_slot_hint", ctypes.c_int32),
+                ("draws", _P(ctypes.c_double)), ("draw_offsets", _P(ctypes.c_int64)),
+                ("seeds", _P(ctypes.c_uint64)), ("seed_master", ctypes.c_uint64)]
+
+
+class BbeResult(ctypes.Structure):
+    _fields_ = [("wins", _P(ctypes.c_uint64)), ("ranks", _P(ctypes.c_uint64)), ("perms", _P(ctypes.c_uint64)),
+                ("winner", _P(ctypes.c_int32)), ("order", _P(ctypes.c_int32)),
+                ("finish_ticks", _P(ctypes.c_int64)), ("final_positions", _P(ctypes.c_double)),
+                ("blocked", _P(ctypes.c_int64)), ("draws_used", _P(ctypes.c_int64)),
+                ("competitor_steps", ctypes.c_uint64), ("blocked_steps", ctypes.c_uint64),
+                ("first_diverged", ctypes.c_int64), ("first_bad_draws", ctypes.c_int64),
+                ("kernel_ms", ctypes.c_float), ("lanes_per_slot", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load the sm_100a library (built in-tree by ``__graft_entry__.build()`` / ``make``)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise BackendUnavailable(f"{LIB_PATH} is not built; run `make` or __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        L.bbe_simulate.argtypes = [_P(BbeRace), _P(BbeCompetitor), _P(BbeState), _P(BbeRequest), _P(BbeResult)]
+        L.bbe_simulate.restype = ctypes.c_int
+        L.bbe_simulate_async.argtypes = [_P(BbeRace), _P(BbeCompetitor), _P(BbeState), _P(BbeRequest),
+                                         _P(BbeResult), ctypes.c_void_p, ctypes.c_void_p]
+        L.bbe_simulate_async.restype = ctypes.c_int
+        L.bbe_tally_len.argtypes = [ctypes.c_int32]
+        L.bbe_tally_len.restype = ctypes.c_int64
+        L.bbe_tally_offset.argtypes = [ctypes.c_int32, ctypes.c_int32]
+        L.bbe_tally_offset.restype = ctypes.c_int64
+        L.bbe_derive_seeds.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, _P(ctypes.c_uint64)]
+        L.bbe_derive_seeds.restype = ctypes.c_int
+        L.bbe_last_kernel_ms.restype = ctypes.c_float
+        L.bbe_last_error.restype = ctypes.c_char_p
+        L.bbe_version.restype = ctypes.c_int
+        L.bbe_device_count.restype = ctypes.c_int
+        L.bbe_device_info.argtypes = [ctypes.c_int, ctypes.c_char_p, _P(ctypes.c_int32), _P(ctypes.c_int32)]
+        L.bbe_device_info.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    return lib().bbe_last_error().decode(errors="replace")
+
+
+def device_count() -> int:
+    return int(lib().bbe_device_count())
+
+
+# -- packing ------------------------------------------------------------------------------------
+
+
+@dataclass
+class Packed:
+    race: BbeRace
+    comps: ctypes.Array
+    n: int
+    ids: tuple
+
+
+def pack_config(config) -> Packed:
+    """RaceConfig -> (bbe_race, bbe_competitor[n]).  Validates like RaceConfig.validate."""
+    validate_config(config)
+    n = len(config.competitors)
+    if n > MAX_COMPETITORS:
+        raise RaceConfigError(f"at most {MAX_COMPETITORS} competitors are supported, got {n}")
+    L = float(config.track_length)
+    race = BbeRace(L, int(config.tick_limit), n, 0)
+    comps = (BbeCompetitor * n)()
+    for k, c in enumerate(config.competitors):
+        o = comps[k]
+        s = c.steps
+        if hasattr(s, "lo"):
+            o.family, o.lo, o.hi = 0, float(s.lo), float(s.hi)
+            o.scale = 1.0
+        else:
+            o.family, o.mu, o.sigma, o.scale = 1, float(s.mu), float(s.sigma), float(s.scale)
+        o.pref_factor = preference_factor(config.conditions, c.preference, c.pref_sensitivity)
+        o.theta = float(c.theta)
+        r = c.responsiveness
+        o.early_mult, o.late_mult = float(r.early_mult), float(r.late_mult)
+        o.bp_abs = r.breakpoint * L  # race.py:94 evaluates breakpoint * track_length in double
+    return Packed(race, comps, n, tuple(c.cid for c in config.competitors))
+
+
+def _ptr(a, ct):
+    return None if a is None else a.ctypes.data_as(_P(ct))
+
+
+def pack_state(state, n: int):
+    if state is None:
+        return BbeState(0, None, None, None, 1, 0), ()
+    if len(state.positions) != n or len(state.prev_steps) != n or len(state.finish_ticks) != n:
+        raise RaceConfigError("state vectors must have one entry per competitor")
+    pos = np.ascontiguousarray(state.positions, np.float64)
+    prev = np.ascontiguousarray(state.prev_steps, np.float64)
+    fin = np.array([-1 if t is None else int(t) for t in state.finish_ticks], np.int64)
+    st = BbeState(int(state.tick), _ptr(pos, ctypes.c_double), _ptr(prev, ctypes.c_double),
+                  _ptr(fin, ctypes.c_int64), 0, 0)
+    return st, (pos, prev, fin)  # keep arrays alive
+
+
+# -- results ------------------------------------------------------------------------------------
+
+
+@dataclass
+class SimResult:
+    """Tallies (always) and optional per-sim records of one batched call."""
+
+    ids: tuple
+    n_sims: int
+    wins: np.ndarray
+    ranks: np.ndarray | None
+    perms: np.ndarray | None
+    winner: np.ndarray | None
+    order: np.ndarray | None
+    finish_ticks: np.ndarray | None
+    final_positions: np.ndarray | None
+    blocked: np.ndarray | None
+    draws_used: np.ndarray | None
+    competitor_steps: int
+    blocked_steps: int
+    kernel_ms: float
+    lanes_per_slot: int
+
+    def win_probabilities(self, laplace: bool = True) -> tuple[float, ...]:
+        """(w + 1) / (d + n) as agents.py:166, or plain frequencies."""
+        n, d = len(self.ids), self.n_sims
+        if laplace:
+            return tuple((int(w) + 1) / (d + n) for w in self.wins)
+        return tuple(int(w) / d for w in self.wins)
+
+
+def _raise(rc: int, res: BbeResult):
+    msg = last_error()
+    if rc == BBE_EINVAL:
+        raise RaceConfigError(msg)
+    if rc == BBE_EDIVERGED:
+        raise SimDivergedError(int(res.first_diverged), msg)
+    if rc == BBE_EDRAWS:
+        raise DrawStreamError(int(res.first_bad_draws), msg)
+    if rc == BBE_ENODEV:
+        raise BackendUnavailable(msg)
+    raise RuntimeError(f"bbe_simulate failed ({rc}): {msg}")
+
+
+def simulate_batch(
+    state,
+    config,
+    n_sims: int,
+    seed: int = 0,
+    *,
+    mode: str = "native",
+    draws=None,
+    draw_offsets=None,
+    seeds=None,
+    seed_master: int = 0,
+    sim_offset: int = 0,
+    ranks: bool = True,
+    perms: bool = False,
+    records: bool = False,
+    lanes_per_slot: int = 0,
+) -> SimResult:
+    """Run ``n_sims`` independent continuations of ``state`` (or races from the start line when
+    ``state is None``) and return tallies.
+
+    mode="native": Philox stream keyed by ``seed``; sim i uses counter (tick block, competitor,
+    sim_offset + i), so any sharding of the index range reproduces the same per-sim outcomes.
+    mode="inject": replay recorded reference draws (``draws`` / CSR ``draw_offsets``) -- bit-exact.
+    records=True also returns per-sim winner, order, finish ticks, final positions, blocked counts.
+    """
+    if mode not in MODES:
+        raise ValueError(f"unknown mode {mode!r}")
+    pk = pack_config(config)
+    n = pk.n
+    st, keep = pack_state(state, n)
+    n_sims = int(n_sims)
+    req = BbeRequest(n_sims, int(sim_offset), int(seed) & M64, MODES[mode], int(lanes_per_slot), None, None, None,
+                     int(seed_master) & M64)
+    if mode == "inject":
+        draws = np.ascontiguousarray(draws, np.float64)
+        draw_offsets = np.ascontiguousarray(draw_offsets, np.int64)
+        if len(draw_offsets) != n_sims + 1:
+            raise ValueError("draw_offsets needs n_sims + 1 entries")
+        if draw_offsets[-1] > len(draws):
+            raise ValueError("draw_offsets point past the end of draws")
+        req.draws = _ptr(draws, ctypes.c_double)
+        req.draw_offsets = _ptr(draw_offsets, ctypes.c_int64)
+    if seeds is not None:
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+        req.seeds = _ptr(seeds, ctypes.c_uint64)
+    wins = np.zeros(n, np.uint64)
+    rk = np.zeros((n, n), np.uint64) if ranks else None
+    pm = np.zeros(math.factorial(n), np.uint64) if (perms and n <= MAX_PERM_COMPETITORS) else None
+    winner = order = fin = fpos = blk = used = None
+    if records:
+        winner = np.zeros(n_sims, np.int32)
+        order = np.zeros((n_sims, n), np.int32)
+        fin = np.zeros((n_sims, n), np.int64)
+        fpos = np.zeros((n_sims, n), np.float64)
+        blk = np.zeros(n_sims, np.int64)
+        used = np.zeros(n_sims, np.int64) if mode == "inject" else None
+    res = BbeResult(_ptr(wins, ctypes.c_uint64), _ptr(rk, ctypes.c_uint64), _ptr(pm, ctypes.c_uint64),
+                    _ptr(winner, ctypes.c_int32), _ptr(order, ctypes.c_int32), _ptr(fin, ctypes.c_int64),
+                    _ptr(fpos, ctypes.c_double), _ptr(blk, ctypes.c_int64), _ptr(used, ctypes.c_int64),
+                    0, 0, -1, -1, 0.0, 0)
+    rc = lib().bbe_simulate(ctypes.byref(pk.race), pk.comps, ctypes.byref(st), ctypes.byref(req), ctypes.byref(res))
+    del keep
+    if rc != BBE_OK:
+        _raise(rc, res)
+    return SimResult(pk.ids, n_sims, wins, rk, pm, winner, order, fin, fpos, blk, used,
+                     int(res.competitor_steps), int(res.blocked_steps), float(res.kernel_ms),
+                     int(res.lanes_per_slot))
+
+
+# -- reference-shaped single-race entry points ---------------------------------------------------
+
+
+def simulate_from(state, config, seed: int, *, mode: str = "native") -> tuple[str, ...]:
+    """One continuation (race.py:393-406) on the GPU; returns the finish order as ids."""
+    r = simulate_batch(state, config, 1, seed, mode=mode, records=True, ranks=False,
+                       seeds=np.array([seed & M64], np.uint64) if mode == "mt" else None)
+    return tuple(r.ids[c] for c in r.order[0])
+
+
+def run_race(config, seed: int, record: bool = True, *, mode: str = "native") -> Trajectory:
+    """One race from the start line (race.py:373-390) on the GPU.
+
+    record=True (snapshots of every tick) is not produced by the batched kernel; it raises.
+    """
+    if record:
+        raise NotImplementedError("per-tick trajectory recording is not implemented on the GPU path; "
+                                  "use record=False")
+    r = simulate_batch(None, config, 1, seed, mode=mode, records=True, ranks=False,
+                       seeds=np.array([seed & M64], np.uint64) if mode == "mt" else None)
+    return Trajectory(
+        competitor_ids=r.ids,
+        dt=config.dt,
+        ticks=None,
+        finish_ticks=tuple(int(t) for t in r.finish_ticks[0]),
+        finish_order=tuple(r.ids[c] for c in r.order[0]),
+        final_positions=tuple(float(p) for p in r.final_positions[0]),
+        blocked_steps=int(r.blocked[0]),
+    )
+
+
+# -- device-resident path (bench `value`, multi-GPU shards) --------------------------------------
+
+
+class DeviceLauncher:
+    """Pre-packed race for repeated device-resident launches (``bbe_simulate_async``).
+
+    Tallies are added into a caller-owned device buffer (e.g. a torch int64 CUDA tensor, passed by
+    ``data_ptr()``) on a caller stream (``torch.cuda.current_stream().cuda_stream``).
+    """
+
+    def __init__(self, state, config, *, lanes_per_slot: int = 0):
+        self.pk = pack_config(config)
+        self.st, self._keep = pack_state(state, self.pk.n)
+        self.lanes_per_slot = int(lanes_per_slot)
+        self.tally_len = int(lib().bbe_tally_len(self.pk.n))
+        off = lambda f: int(lib().bbe_tally_offset(self.pk.n, f))  # noqa: E731
+        self.off = {name: off(i) for i, name in enumerate(
+            ["wins", "ranks", "perms", "ct", "blocked", "n_div", "n_bad", "first_div", "first_bad"])}
+
+    def launch(self, d_tally_ptr: int, n_sims: int, seed: int, *, sim_offset: int = 0, stream: int = 0,
+               mode: str = "native") -> None:
+        req = BbeRequest(int(n_sims), int(sim_offset), int(seed) & M64, MODES[mode], self.lanes_per_slot, None,
+                         None, None, 0)
+        rc = lib().bbe_simulate_async(ctypes.byref(self.pk.race), self.pk.comps, ctypes.byref(self.st),
+                                      ctypes.byref(req), None, ctypes.c_void_p(d_tally_ptr),
+                                      ctypes.c_void_p(stream))
+        if rc != BBE_OK:
+            _raise(rc, BbeResult())
+
+    @staticmethod
+    def last_kernel_ms() -> float:
+        return float(lib().bbe_last_kernel_ms())

@@ -1,0 +1,81 @@
+"""CPU-side checks of the boundary: the C-ABI library loads, exports every symbol the header declares,
+its host-only functions agree with the reference, and the product path refuses to run without a GPU
+(no CPU fallback)."""
+
+import os
+import random
+import re
+
+import numpy as np
+import pytest
+
+from paper_2108_02419_b200 import sim
+from paper_2108_02419_b200.agents import dry_run_seeds
+from paper_2108_02419_b200.race import Competitor, RaceConfig, RaceConfigError, UniformSteps
+from golden_io import rng_vectors
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "bbe_sim.h")).read()
+    return sorted(set(re.findall(r"^(?:int|int64_t|float|const char\*)\s+(bbe_\w+)\(", src, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    L = sim.lib()
+    declared = header_symbols()
+    assert declared and set(declared) == set(sim.EXPORTED_SYMBOLS)
+    for name in declared:
+        assert hasattr(L, name), name
+    assert L.bbe_version() == 1
+
+
+def test_tally_layout():
+    L = sim.lib()
+    for n in (1, 2, 5, 6, 7, 10, 20, 40, 128):
+        nperm = 1
+        for i in range(2, n + 1):
+            nperm *= i
+        nperm = nperm if n <= 6 else 0
+        assert L.bbe_tally_len(n) == n + n * n + nperm + 6
+        assert L.bbe_tally_offset(n, 0) == 0
+        assert L.bbe_tally_offset(n, 1) == n
+        assert L.bbe_tally_offset(n, 3) == n + n * n + nperm
+    assert L.bbe_tally_len(0) == -1 and L.bbe_tally_len(129) == -1
+
+
+def test_derive_seeds_matches_reference():
+    L = sim.lib()
+    for d in rng_vectors()["derive_seed_run"]:
+        out = np.zeros(1, np.uint64)
+        assert L.bbe_derive_seeds(int(d["master"]), d["i"], 1, out.ctypes.data_as(sim._P(sim.ctypes.c_uint64))) == 0
+        assert int(out[0]) == int(d["seed"])
+
+
+def test_dry_run_seeds_match_sequential_getrandbits():
+    a, b = random.Random(11), random.Random(11)
+    seeds = dry_run_seeds(a, 257)
+    assert [int(s) for s in seeds] == [b.getrandbits(64) for _ in range(257)]
+    assert a.random() == b.random()  # stream position identical afterwards
+
+
+def test_validation_mirrors_reference_errors():
+    bad = [
+        RaceConfig(0.0, (Competitor("a", UniformSteps(1, 2)),)),
+        RaceConfig(10.0, ()),
+        RaceConfig(10.0, (Competitor("a", UniformSteps(1, 2)), Competitor("a", UniformSteps(1, 2)))),
+        RaceConfig(10.0, (Competitor("a", UniformSteps(3, 2)),)),
+        RaceConfig(10.0, (Competitor("a", UniformSteps(1, 2), theta=-1.0),)),
+        RaceConfig(10.0, (Competitor("a", UniformSteps(1, 2)),), tick_limit=0),
+    ]
+    for cfg in bad:
+        with pytest.raises(RaceConfigError):
+            sim.pack_config(cfg)
+
+
+@pytest.mark.skipif(os.path.exists("/dev/nvidia0"), reason="checks the no-GPU behaviour")
+def test_no_cpu_fallback_without_gpu():
+    cfg = RaceConfig(100.0, (Competitor("a", UniformSteps(1, 2)), Competitor("b", UniformSteps(1, 2))))
+    with pytest.raises(sim.BackendUnavailable):
+        sim.simulate_batch(None, cfg, 10, 1)
