@@ -17,6 +17,7 @@
 
 #include "../../include/bbe_sim.h"
 #include "race_kernel.cuh"
+#include "native_kernel.cuh"
 
 using namespace bbe;
 
@@ -192,31 +193,69 @@ void pack_params(const bbe_race* race, const bbe_competitor* comps, const bbe_st
         }
         P[F_FAMILY * n + c] = (double)p.family;
     }
+    // Pre-finished competitors: their finish ticks only ever compare with each other and with later
+    // (new) finishes, so an order-preserving compression to -m..-1 keeps _finish_order exact while
+    // letting the kernel hold ticks as int32 relative to the state's tick.
+    // (A finish tick after the state's own tick -- an inconsistent state -- keeps its plain offset.)
+    for (int c = 0; c < n; ++c) {
+        double rel = 0.0;
+        if (!st->from_start && st->finish_ticks[c] > st->tick) {
+            rel = (double)std::min<int64_t>(st->finish_ticks[c] - st->tick, INT32_MAX - 2);
+        } else if (!st->from_start && st->finish_ticks[c] >= 0) {
+            int greater_distinct = 0;
+            for (int d = 0; d < n; ++d) {
+                if (st->finish_ticks[d] < 0 || st->finish_ticks[d] > st->tick ||
+                    st->finish_ticks[d] <= st->finish_ticks[c])
+                    continue;
+                bool seen = false;
+                for (int e = 0; e < d; ++e)
+                    if (st->finish_ticks[e] == st->finish_ticks[d]) seen = true;
+                if (!seen) ++greater_distinct;
+            }
+            rel = -1.0 - greater_distinct;
+        }
+        P[F_FINREL * n + c] = rel;
+    }
 }
 
 typedef void (*KernelFn)(LaunchArgs);
 
-KernelFn pick_kernel(int mode, int k) {
+template <int K>
+KernelFn native_for_ch(int ch) {
+    switch (ch) {
+        case 1: return native_kernel<K, 1>;
+        case 2: return native_kernel<K, 2>;
+        case 3: return native_kernel<K, 3>;
+        case 4: return native_kernel<K, 4>;
+        case 5: return native_kernel<K, 5>;
+        case 6: return native_kernel<K, 6>;
+        case 7: return native_kernel<K, 7>;
+        case 8: return native_kernel<K, 8>;
+    }
+    return nullptr;
+}
+
+KernelFn pick_kernel(int mode, int k, int ch) {
     if (mode == BBE_MODE_INJECT) {
         switch (k) {
-            case 1: return race_kernel<double, 1, INJECT>;
-            case 2: return race_kernel<double, 2, INJECT>;
-            case 3: return race_kernel<double, 3, INJECT>;
-            case 4: return race_kernel<double, 4, INJECT>;
+            case 1: return race_kernel<double, 1, INJECT, 1>;
+            case 2: return race_kernel<double, 2, INJECT, 1>;
+            case 3: return race_kernel<double, 3, INJECT, 1>;
+            case 4: return race_kernel<double, 4, INJECT, 1>;
         }
     } else {
         switch (k) {
-            case 1: return race_kernel<float, 1, NATIVE>;
-            case 2: return race_kernel<float, 2, NATIVE>;
-            case 3: return race_kernel<float, 3, NATIVE>;
-            case 4: return race_kernel<float, 4, NATIVE>;
+            case 1: return native_for_ch<1>(ch);
+            case 2: return native_for_ch<2>(ch);
+            case 3: return native_for_ch<3>(ch);
+            case 4: return native_for_ch<4>(ch);
         }
     }
     return nullptr;
 }
 
 struct Plan {
-    int n, K, W, S, nperm, tally_len;
+    int n, K, W, S, CH, WP, nperm, tally_len;
     size_t smem;
     KernelFn fn;
     int grid;
@@ -229,11 +268,13 @@ int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_request* rq, int want
     if (pl->K < 0) return fail(BBE_EINVAL, "field too large for one warp");
     pl->W = (n + pl->K - 1) / pl->K;
     pl->S = kWarp / pl->W;
+    pl->CH = (pl->W + 3) / 4;
+    pl->WP = 4 * pl->CH;
     pl->nperm = want_perms ? nperm_for(n) : 0;
     TallyLayout TL{n, pl->nperm};
     pl->tally_len = TL.len();
-    pl->smem = (size_t)TL.smem_len() * sizeof(unsigned long long);
-    pl->fn = pick_kernel(rq->mode, pl->K);
+    pl->smem = smem_bytes(rq->mode == BBE_MODE_NATIVE, (TL.hist_len() + 1) & ~1, pl->K, pl->S, pl->WP);
+    pl->fn = pick_kernel(rq->mode, pl->K, pl->CH);
     if (!pl->fn) return fail(BBE_EINVAL, "no kernel for this configuration");
     if (pl->smem > 48 * 1024) {
         BBE_CK(cudaFuncSetAttribute((const void*)pl->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->smem));
@@ -359,11 +400,12 @@ static int build_args(const Plan& pl, const bbe_race* race, const bbe_state* st,
     a.n = race->n;
     a.W = pl.W;
     a.S = pl.S;
+    a.WP = pl.WP;
     a.from_start = st->from_start ? 1 : 0;
     a.perms = pl.nperm;
     a.L = race->track_length;
     a.tick0 = st->from_start ? 0 : st->tick;
-    a.tick_limit = race->tick_limit;
+    a.limit = (int32_t)std::min<int64_t>(race->tick_limit, INT32_MAX);
     a.n_sims = rq->n_sims;
     a.sim_offset = rq->sim_offset;
     a.seed = rq->seed;
@@ -482,7 +524,7 @@ int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const 
     Plan pl;
     const bool perms = nperm_for(race->n) > 0;
     if ((rc = make_plan(ctx, race, rq, perms, &pl))) return rc;
-    cudaStream_t s = stream ? (cudaStream_t)stream : ctx->stream;
+    cudaStream_t s = (cudaStream_t)stream;  // NULL = legacy default stream (torch's default)
     // parameters: staged through pinned memory; the copy is ordered on `s` before the kernel, and
     // the staging block is not reused until that copy has been consumed (sync on an event).
     const size_t pbytes = (size_t)F_COUNT * race->n * sizeof(double);

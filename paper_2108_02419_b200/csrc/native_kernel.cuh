@@ -1,0 +1,384 @@
+// native_kernel.cuh -- the throughput kernel: Philox draws, FP32 race state (BBE_MODE_NATIVE).
+//
+// Same model as race_kernel.cuh (race.py:233-332 semantics, listed there); the arithmetic is FP32
+// and the random stream is Philox4x32-10, so outcomes are statistically -- not bitwise -- equal to
+// the reference's.  Everything else is the reference's rule set: synchronous ticks from
+// start-of-tick positions, nearest still-racing rival strictly ahead with the lowest-index tie rule,
+// gap > theta => free draw scaled by (resp * pref), else resp * min(prev_c, prev_front) with no draw,
+// nextafter on a zero-progress step, finish at p >= L, order by (finish tick, L - pos, index).
+//
+// Per tick and lane the work is: publish one u32 key, one __syncwarp, CH 128-bit shared loads and
+// one VIADDMNMX per rival (two independent min chains for ILP), one compare against theta, the step
+// and the position update.  Bookkeeping that the generic kernel did per tick (segment ballots,
+// 64-bit tick arithmetic, bool byte-packing) is moved to the 4-tick block boundary or removed:
+//   * rt (ticks advanced in this sim) is segment-uniform and simply incremented every tick; it only
+//     matters while a lane races, and a finished segment is re-filled at the next boundary;
+//   * racing <=> fin == kRacing (int32 finish tick relative to the state's tick);
+//   * the tick-limit check marks racing lanes "diverged" (fin = kDiverged); the segment is reported
+//     at finalize if any of its lanes did.
+#pragma once
+
+#include "race_kernel.cuh"
+
+namespace bbe {
+
+constexpr int32_t kRacing = 0x7fffffff;
+constexpr int32_t kDiverged = 0x7ffffffe;
+
+template <int K, int CH>
+__global__ void __launch_bounds__(kBlockThreads, K == 1 ? 8 : (K == 2 ? 5 : 3))
+native_kernel(const LaunchArgs a) {
+    extern __shared__ __align__(16) unsigned long long s_dyn[];
+    const TallyLayout TL{a.n, a.perms};
+    const int hist_len = TL.hist_len();
+    unsigned long long* s_hist = s_dyn;
+    for (int i = threadIdx.x; i < hist_len; i += blockDim.x) s_hist[i] = 0ull;
+
+    constexpr int WP = 4 * CH;
+    const int n = a.n, W = a.W, S = a.S;
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int warp = threadIdx.x >> 5;
+    const int seg = lane / W;
+    const bool lane_on = seg < S;
+    const int base = lane_on ? seg * W : 0;
+    const int l = lane - seg * W;
+    const unsigned segmask = lane_on ? ((W == 32 ? 0xffffffffu : ((1u << W) - 1u)) << base) : 0u;
+
+    // key rows: [warp][parity][slot][segment * WP + lane-in-segment]; pads and idle lanes hold 0
+    const int slot_words = S * WP;
+    const int row_words = K * slot_words;
+    uint32_t* rows = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) + warp * 2 * row_words;
+    for (int i = lane; i < 2 * row_words; i += kWarp) rows[i] = 0u;
+    uint32_t* const wr = rows + (lane_on ? seg * WP + l : 0);  // + parity*row_words + k*slot_words
+    const uint32_t* const rd = rows + (lane_on ? seg * WP : 0);
+    __syncthreads();
+
+    // ---- per-slot constants, FP32 ----
+    int cidx[K];
+    bool has[K], lognorm[K];
+    float lo[K], span[K], lmu[K], sg[K], rpE[K], rpL[K], eE[K], eL[K], bp[K], th[K];
+    const double* P = a.P;
+    bool any_lognorm = false;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int c = k * W + l;
+        cidx[k] = c;
+        has[k] = lane_on && c < n;
+        const int cc = has[k] ? c : 0;
+        lo[k] = (float)P[F_LO * n + cc];
+        span[k] = (float)P[F_SPAN * n + cc];
+        lmu[k] = (float)P[F_LMU * n + cc];
+        sg[k] = (float)P[F_SIGMA * n + cc];
+        rpE[k] = (float)P[F_RP_EARLY * n + cc];
+        rpL[k] = (float)P[F_RP_LATE * n + cc];
+        eE[k] = (float)P[F_EARLY * n + cc];
+        eL[k] = (float)P[F_LATE * n + cc];
+        bp[k] = (float)P[F_BP * n + cc];
+        th[k] = (float)P[F_THETA * n + cc];
+        lognorm[k] = has[k] && P[F_FAMILY * n + cc] != 0.0;
+        any_lognorm |= lognorm[k];
+    }
+    any_lognorm = __any_sync(0xffffffffu, any_lognorm);
+    const float L = (float)a.L;
+    const bool scan = a.scan != 0;
+
+    // ---- segment bookkeeping ----
+    const int64_t segs_total = (int64_t)gridDim.x * kWarpsPerBlock * S;
+    int64_t s = lane_on ? ((int64_t)blockIdx.x * kWarpsPerBlock + warp) * S + seg : a.n_sims;
+    int32_t rt = 0;
+    bool running = false;
+    const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
+
+    float pos[K], prev[K];
+    int32_t fin[K];
+    float rawd[K][kTicksPerBlock];
+    uint32_t ct_sim = 0, blk_sim = 0;
+    unsigned long long ct_tot = 0, blk_tot = 0, n_div = 0;
+    int64_t first_div = INT64_MAX;
+
+    auto load_sim = [&](bool do_it) {
+        if (!do_it) return;
+        running = lane_on && s < a.n_sims;
+        rt = 0;
+        ct_sim = blk_sim = 0;
+        const uint64_t gs = (uint64_t)(a.sim_offset + s);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int cc = has[k] ? cidx[k] : 0;
+            pos[k] = (float)P[F_POS0 * n + cc];
+            prev[k] = (float)P[F_PREV0 * n + cc];
+            const bool pre_finished = P[F_FIN0 * n + cc] >= 0.0;
+            fin[k] = !(running && has[k]) ? kDiverged - 1 : (pre_finished ? (int32_t)P[F_FINREL * n + cc] : kRacing);
+            if (a.from_start && running && has[k]) {
+                // race.py:233-241: one free draw per competitor, resp at position 0
+                const U4 w = philox4x32_10(U4{0xFFFFFFFFu, (uint32_t)cidx[k], (uint32_t)gs, (uint32_t)(gs >> 32)},
+                                           k0, k1);
+                float d;
+                if (lognorm[k]) {
+                    const float r = sqrtf(-2.0f * __logf(u01_open0(w.x)));
+                    d = __expf(fmaf(sg[k], r * __cosf(6.283185307f * u01_23(w.y)), lmu[k]));
+                } else {
+                    d = fmaf(span[k], u01_23(w.x), lo[k]);
+                }
+                prev[k] = __fmul_rn((0.0f < bp[k]) ? rpE[k] : rpL[k], d);
+            }
+        }
+    };
+    // fin sentinel for idle slots: neither racing nor diverged, sorts last
+    load_sim(true);
+
+    while (true) {
+        // ---------------- block boundary ----------------
+        bool live = false, dv = false;
+#pragma unroll
+        for (int k = 0; k < K; ++k) { live |= fin[k] == kRacing; dv |= fin[k] == kDiverged; }
+        const unsigned live_mask = __ballot_sync(0xffffffffu, live);
+        const bool seg_done = running && ((live_mask & segmask) == 0u);
+        if (__any_sync(0xffffffffu, seg_done)) {
+            const bool diverged = (__ballot_sync(0xffffffffu, dv) & segmask) != 0u;
+            float lp[K];
+            int rank[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) { lp[k] = __fsub_rn(L, pos[k]); rank[k] = 0; }
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) {
+                for (int j = 0; j < W; ++j) {
+                    const int32_t fr = shfl(fin[kk], base + j);
+                    const float dr = shfl(lp[kk], base + j);
+                    const int i = kk * W + j;
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const bool less = fr < fin[k] || (fr == fin[k] && (dr < lp[k] || (dr == lp[k] && i < cidx[k])));
+                        rank[k] += (i < n && less) ? 1 : 0;
+                    }
+                }
+            }
+            uint32_t seg_blk = 0;
+            for (int j = 0; j < W; ++j) seg_blk += shfl(blk_sim, base + j);
+            int64_t lehmer = 0;
+            if (a.perms) {
+                int cnt[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) cnt[k] = 0;
+#pragma unroll
+                for (int kk = 0; kk < K; ++kk)
+                    for (int j = 0; j < W; ++j) {
+                        const int rr = shfl(rank[kk], base + j);
+                        const int i = kk * W + j;
+#pragma unroll
+                        for (int k = 0; k < K; ++k) cnt[k] += (i < n && i < cidx[k] && rr > rank[k]) ? 1 : 0;
+                    }
+                int64_t term = 0;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    if (!has[k]) continue;
+                    int64_t f = 1;
+                    for (int q = 2; q <= n - 1 - rank[k]; ++q) f *= q;
+                    term += cnt[k] * f;
+                }
+                for (int j = 0; j < W; ++j) lehmer += shfl(term, base + j);
+            }
+            if (seg_done) {
+                const int64_t gs = a.sim_offset + s;
+                if (diverged) {
+                    if (l == 0) { n_div++; first_div = min(first_div, gs); }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        if (!has[k]) continue;
+                        if (rank[k] == 0) atomicAdd(&s_hist[TL.wins() + cidx[k]], 1ull);
+                        atomicAdd(&s_hist[TL.ranks() + cidx[k] * n + rank[k]], 1ull);
+                    }
+                    if (a.perms && l == 0) atomicAdd(&s_hist[TL.perms() + lehmer], 1ull);
+                }
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    if (!has[k]) continue;
+                    const int64_t o = s * n + cidx[k];
+                    if (a.winner && rank[k] == 0) a.winner[s] = diverged ? -1 : cidx[k];
+                    if (a.order) a.order[s * n + rank[k]] = cidx[k];
+                    if (a.finish_ticks) {
+                        const double f0 = P[F_FIN0 * n + cidx[k]];
+                        a.finish_ticks[o] = f0 >= 0.0 ? (int64_t)f0
+                                                      : (fin[k] >= kDiverged ? -1 : a.tick0 + (int64_t)fin[k]);
+                    }
+                    if (a.final_pos) a.final_pos[o] = (double)pos[k];
+                }
+                if (l == 0 && a.blocked) a.blocked[s] = seg_blk;
+                ct_tot += ct_sim;
+                blk_tot += blk_sim;
+                s += segs_total;
+            }
+            load_sim(seg_done);
+        }
+        if (!__any_sync(0xffffffffu, running)) break;
+
+        // ---------------- Philox: 4 draws per slot for this block of ticks ----------------
+        __syncwarp();  // key rows: the previous block's reads precede this block's writes
+        {
+            const uint64_t gs = (uint64_t)(a.sim_offset + s);
+            const uint32_t blk = (uint32_t)rt >> 2;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const U4 w = philox4x32_10(U4{blk, (uint32_t)cidx[k], (uint32_t)gs, (uint32_t)(gs >> 32)}, k0, k1);
+                if (any_lognorm && lognorm[k]) {
+                    const float r0 = sqrtf(-2.0f * __logf(u01_open0(w.x)));
+                    const float r1 = sqrtf(-2.0f * __logf(u01_open0(w.z)));
+                    float s0, c0, s1, c1;
+                    __sincosf(6.283185307f * u01_23(w.y), &s0, &c0);
+                    __sincosf(6.283185307f * u01_23(w.w), &s1, &c1);
+                    rawd[k][0] = __expf(fmaf(sg[k], r0 * c0, lmu[k]));
+                    rawd[k][1] = __expf(fmaf(sg[k], r0 * s0, lmu[k]));
+                    rawd[k][2] = __expf(fmaf(sg[k], r1 * c1, lmu[k]));
+                    rawd[k][3] = __expf(fmaf(sg[k], r1 * s1, lmu[k]));
+                } else {
+                    rawd[k][0] = fmaf(span[k], u01_23(w.x), lo[k]);
+                    rawd[k][1] = fmaf(span[k], u01_23(w.y), lo[k]);
+                    rawd[k][2] = fmaf(span[k], u01_23(w.z), lo[k]);
+                    rawd[k][3] = fmaf(span[k], u01_23(w.w), lo[k]);
+                }
+            }
+        }
+
+        // ---------------- 4 synchronous ticks ----------------
+#pragma unroll
+        for (int tj = 0; tj < kTicksPerBlock; ++tj) {
+            bool racing[K];
+            const bool over = rt >= a.limit;  // race.py:381-386 / 402-404, before the advance
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                racing[k] = fin[k] == kRacing;
+                if (racing[k] && over) { fin[k] = kDiverged; racing[k] = false; }
+            }
+
+            // ---- front runner: nearest key strictly ahead (race.py:244-264) ----
+            float gap[K];
+            uint32_t fkey[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) { gap[k] = CUDART_INF_F; fkey[k] = 0u; }
+            if (scan) {
+                uint32_t kp[K], nk[K];
+                uint32_t* w0 = wr + (tj & 1) * row_words;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    kp[k] = key_of(pos[k]);
+                    nk[k] = ~kp[k];
+                    if (lane_on) w0[k * slot_words] = racing[k] ? kp[k] : 0u;
+                }
+                __syncwarp();
+                uint32_t b0[K], b1[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) { b0[k] = 0xffffffffu; b1[k] = 0xffffffffu; }
+                const uint32_t* r0 = rd + (tj & 1) * row_words;
+#pragma unroll
+                for (int kk = 0; kk < K; ++kk) {
+                    const uint4* r4 = reinterpret_cast<const uint4*>(r0 + kk * slot_words);
+#pragma unroll
+                    for (int c = 0; c < CH; ++c) {
+                        const uint4 v = r4[c];
+#pragma unroll
+                        for (int k = 0; k < K; ++k) {
+                            b0[k] = min(b0[k], v.x + nk[k]);
+                            b1[k] = min(b1[k], v.y + nk[k]);
+                            b0[k] = min(b0[k], v.z + nk[k]);
+                            b1[k] = min(b1[k], v.w + nk[k]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const uint32_t fk = min(b0[k], b1[k]) - nk[k];  // = best + key_c + 1 (mod 2^32)
+                    const bool ahead = fk > kp[k];                    // no wrap <=> someone strictly ahead
+                    fkey[k] = ahead ? fk : 0u;
+                    gap[k] = ahead ? __fsub_rn(float_of_key(fk), pos[k]) : CUDART_INF_F;
+                }
+            }
+
+            // ---- step resolution (race.py:267-274) ----
+            bool fr[K], bl[K], any_bl = false;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                fr[k] = gap[k] > th[k];
+                bl[k] = racing[k] && !fr[k];
+                any_bl |= bl[k];
+            }
+            float pf[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) pf[k] = 0.0f;
+            if (__any_sync(0xffffffffu, any_bl)) {
+                // front index: lowest competitor index holding the front key (slot-major, then lane)
+                int bi[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) bi[k] = 0;
+                const uint32_t* r0 = rd + (tj & 1) * row_words;
+#pragma unroll
+                for (int kk = K - 1; kk >= 0; --kk) {
+                    const uint4* r4 = reinterpret_cast<const uint4*>(r0 + kk * slot_words);
+#pragma unroll
+                    for (int c = CH - 1; c >= 0; --c) {
+                        const uint4 v = r4[c];
+#pragma unroll
+                        for (int k = 0; k < K; ++k) {
+                            bi[k] = (v.w == fkey[k]) ? (kk << 5) | (4 * c + 3) : bi[k];
+                            bi[k] = (v.z == fkey[k]) ? (kk << 5) | (4 * c + 2) : bi[k];
+                            bi[k] = (v.y == fkey[k]) ? (kk << 5) | (4 * c + 1) : bi[k];
+                            bi[k] = (v.x == fkey[k]) ? (kk << 5) | (4 * c + 0) : bi[k];
+                        }
+                    }
+                }
+#pragma unroll
+                for (int kk = 0; kk < K; ++kk) {
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const float v = shfl(prev[kk], base + (bi[k] & 31));
+                        pf[k] = ((bi[k] >> 5) == kk) ? v : pf[k];
+                    }
+                }
+            }
+
+            // ---- synchronous update (race.py:299-320) ----
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const bool early = pos[k] < bp[k];
+                const float m = (pf[k] < prev[k]) ? pf[k] : prev[k];  // Python min(prev_c, prev_front)
+                const float step = fr[k] ? __fmul_rn(early ? rpE[k] : rpL[k], rawd[k][tj])
+                                         : __fmul_rn(early ? eE[k] : eL[k], m);
+                if (racing[k]) {
+                    float p = __fadd_rn(pos[k], step);
+                    if (p == pos[k]) p = nextafterf(p, CUDART_INF_F);
+                    pos[k] = p;
+                    prev[k] = step;
+                    ct_sim += 1;
+                    blk_sim += bl[k] ? 1u : 0u;
+                    if (p >= L) fin[k] = rt + 1;
+                }
+            }
+            rt += 1;
+        }
+    }
+
+    // ---------------- flush ----------------
+    unsigned long long v_ct = ct_tot, v_blk = blk_tot, v_div = n_div;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        v_ct += __shfl_xor_sync(0xffffffffu, v_ct, off);
+        v_blk += __shfl_xor_sync(0xffffffffu, v_blk, off);
+        v_div += __shfl_xor_sync(0xffffffffu, v_div, off);
+        first_div = min(first_div, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)first_div, off));
+    }
+    const int ct_at = TL.ct();
+    if (lane == 0) {
+        if (v_ct) atomicAdd((unsigned long long*)&a.tally[ct_at + 0], v_ct);
+        if (v_blk) atomicAdd((unsigned long long*)&a.tally[ct_at + 1], v_blk);
+        if (v_div) atomicAdd((unsigned long long*)&a.tally[ct_at + 2], v_div);
+        if (first_div != INT64_MAX)
+            atomicMax((unsigned long long*)&a.tally[ct_at + 4], ~(unsigned long long)(first_div + 1));
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < hist_len; i += blockDim.x) {
+        const unsigned long long v = s_hist[i];
+        if (v) atomicAdd((unsigned long long*)&a.tally[i], v);
+    }
+}
+
+}  // namespace bbe

@@ -15,8 +15,15 @@
 //   * One race ("sim") occupies a SEGMENT of W consecutive lanes of a warp; each lane holds K
 //     competitors ("slots"): competitor c = k*W + l lives in lane l, slot k.  S = 32/W segments
 //     (independent sims) share a warp, so a 10-runner field packs 3 sims per warp.
-//   * Front runner: each lane scans the segment's rival positions with __shfl_sync (index order,
-//     strict compare => lowest-index tie rule); finished rivals carry -inf and never qualify.
+//   * Front runner, NATIVE: every lane publishes an order-preserving u32 key of its start-of-tick
+//     position to a per-warp shared-memory row (double-buffered by tick parity, one __syncwarp);
+//     each lane then reads its segment's keys with 128-bit broadcast loads and keeps
+//     min((key_r - key_c - 1) mod 2^32) -- one IADD + one IMNMX per rival: the wrap sends every
+//     rival at or behind c (and every finished rival, key 0) above every rival ahead, so the
+//     minimum is the nearest position strictly ahead.  The front's index (needed only for a
+//     blocked step) is recovered by a second pass that runs only when some lane is blocked.
+//   * Front runner, INJECT (FP64, bit-exact): the reference's own arithmetic -- gap = p_i - p_c
+//     in double, strict compares in index order -- over __shfl_sync'd rival positions.
 //   * Finish/termination: __ballot_sync over "still racing" masks; a finished segment is
 //     re-filled with its next sim at a 4-tick block boundary (persistent grid, sims strided).
 //   * Draws: NATIVE = Philox4x32-10 keyed by the request seed, counter = (tick block, competitor,
@@ -24,7 +31,6 @@
 //     INJECT = recorded reference draws read from a CSR stream, per-lane offset = popc of free
 //     slots before it in competitor-index order (exactly the reference's consumption order).
 //   * Tallies: per-block shared-memory histograms (wins, ranks, perms), one atomic flush per block.
-//   * Real = float (NATIVE) or double with FMA contraction disabled (INJECT, bit-exact).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -35,12 +41,15 @@ namespace bbe {
 
 constexpr int kWarp = 32;
 constexpr int kBlockThreads = 128;
+constexpr int kWarpsPerBlock = kBlockThreads / kWarp;
 constexpr int kTicksPerBlock = 4;  // Philox4x32 yields 4 words per call: one per tick
 
 // Parameter block fields (SoA, stride n), host-packed in double (see bbe_sim.cu: pack_params).
 enum Field {
     F_LO = 0, F_SPAN, F_LMU, F_SIGMA, F_SCALE, F_MU, F_RP_EARLY, F_RP_LATE, F_EARLY, F_LATE, F_BP,
-    F_THETA, F_POS0, F_PREV0, F_FIN0, F_FAMILY, F_COUNT
+    F_THETA, F_POS0, F_PREV0, F_FIN0, F_FAMILY,
+    F_FINREL,  // finish tick relative to the state's tick, order-compressed to int32 (racing: unused)
+    F_COUNT
 };
 
 // Tally layout in u64 (see bbe_tally_offset in bbe_sim.h).
@@ -56,14 +65,15 @@ struct TallyLayout {
     __host__ __device__ int first_div() const { return ct() + 4; }
     __host__ __device__ int first_bad() const { return ct() + 5; }
     __host__ __device__ int len() const { return ct() + 6; }
-    __host__ __device__ int smem_len() const { return n + n * n + nperm; }  // histograms only
+    __host__ __device__ int hist_len() const { return n + n * n + nperm; }  // shared-memory histograms
 };
 
 struct LaunchArgs {
     const double* P;  // [F_COUNT][n] parameter block
-    int n, W, S, from_start, scan, perms;
+    int n, W, S, WP, from_start, scan, perms;
     double L;
-    int64_t tick0, tick_limit;
+    int64_t tick0;
+    int32_t limit;  // tick_limit clamped to int32 (ticks run per sim)
     int64_t n_sims, sim_offset;
     uint64_t seed;
     const double* draws;          // INJECT
@@ -76,6 +86,14 @@ struct LaunchArgs {
     int64_t* blocked;
     int64_t* draws_used;
 };
+
+// Dynamic shared memory of one block: histograms, then (NATIVE) the key rows.
+__host__ __device__ inline int key_row_words(int K, int S, int WP) { return K * S * WP; }
+__host__ __device__ inline size_t smem_bytes(int mode_native, int hist_len, int K, int S, int WP) {
+    size_t b = (size_t)hist_len * 8;
+    if (mode_native) b += (size_t)kWarpsPerBlock * 2 * key_row_words(K, S, WP) * 4;
+    return b;
+}
 
 // ------------------------------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al., SC'11), in registers.
@@ -95,12 +113,17 @@ __device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
 }
 
 // [0,1) with 23 random bits, via the exponent trick (no I2F on the hot path).
-__device__ __forceinline__ float u01_23(uint32_t w) {
-    return __uint_as_float(0x3f800000u | (w >> 9)) - 1.0f;
-}
+__device__ __forceinline__ float u01_23(uint32_t w) { return __uint_as_float(0x3f800000u | (w >> 9)) - 1.0f; }
 // (0,1] for the Box-Muller log.
-__device__ __forceinline__ float u01_open0(uint32_t w) {
-    return 1.0f - u01_23(w);
+__device__ __forceinline__ float u01_open0(uint32_t w) { return 1.0f - u01_23(w); }
+
+// Order-preserving float <-> u32 key (total order of non-NaN floats; key 0 is never a real position).
+__device__ __forceinline__ uint32_t key_of(float x) {
+    const uint32_t b = __float_as_uint(x);
+    return b ^ ((uint32_t)((int32_t)b >> 31) | 0x80000000u);
+}
+__device__ __forceinline__ float float_of_key(uint32_t k) {
+    return __uint_as_float(k ^ (((int32_t)k < 0) ? 0x80000000u : 0xffffffffu));
 }
 
 template <typename Real> struct RealOps;
@@ -125,26 +148,38 @@ __device__ __forceinline__ T shfl(T v, int src) { return __shfl_sync(0xffffffffu
 enum Mode { NATIVE = 0, INJECT = 1 };
 
 // ------------------------------------------------------------------------------------------------
-// The race kernel.  K = competitors per lane (slots).  Persistent: grid sized to residency.
+// The race kernel.  K = competitors per lane (slots); CH = 128-bit key chunks per segment row
+// (NATIVE; W <= 4*CH).  Persistent: grid sized to residency, sims strided over segments.
 // ------------------------------------------------------------------------------------------------
-template <typename Real, int K, int MODE>
-__global__ void __launch_bounds__(kBlockThreads)
+template <typename Real, int K, int MODE, int CH>
+__global__ void __launch_bounds__(kBlockThreads, MODE == NATIVE ? (K == 1 ? 8 : (K == 2 ? 5 : 3)) : 1)
 race_kernel(const LaunchArgs a) {
     using R = RealOps<Real>;
-    extern __shared__ unsigned long long s_hist[];
+    extern __shared__ __align__(16) unsigned long long s_dyn[];
     const TallyLayout TL{a.n, a.perms};
-    const int hist_len = a.n + a.n * a.n + (a.perms ? a.perms : 0);
+    const int hist_len = TL.hist_len();
+    unsigned long long* s_hist = s_dyn;
     for (int i = threadIdx.x; i < hist_len; i += blockDim.x) s_hist[i] = 0ull;
-    __syncthreads();
 
     const int n = a.n, W = a.W, S = a.S;
     const int lane = threadIdx.x & (kWarp - 1);
+    const int warp = threadIdx.x >> 5;
     const int seg = lane / W;
     const bool lane_on = seg < S;
     const int base = lane_on ? seg * W : 0;
     const int l = lane - seg * W;
     const unsigned segmask = lane_on ? ((W == 32 ? 0xffffffffu : ((1u << W) - 1u)) << base) : 0u;
     const unsigned lt_mask = (1u << lane) - 1u;
+
+    // NATIVE key rows: [warp][parity][slot][segment * WP + lane-in-segment]
+    const int row_words = key_row_words(K, S, a.WP);
+    uint32_t* s_keys = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1));  // 16-B aligned
+    uint32_t* my_rows = s_keys + warp * 2 * row_words;
+    const int seg_off = lane_on ? seg * a.WP : 0;
+    if (MODE == NATIVE) {
+        for (int i = lane; i < 2 * row_words; i += kWarp) my_rows[i] = 0u;  // pads stay "behind"
+    }
+    __syncthreads();
 
     // ---- per-slot constants (loaded once: the lane->competitor map is fixed for the kernel) ----
     int cidx[K];
@@ -177,13 +212,18 @@ race_kernel(const LaunchArgs a) {
     }
     const Real L = (Real)a.L;
     const Real NEG_INF = -R::inf();
+    bool any_lognorm = false;
+#pragma unroll
+    for (int k = 0; k < K; ++k) any_lognorm |= has[k] && lognorm[k];
+    any_lognorm = __any_sync(0xffffffffu, any_lognorm);
 
     // ---- segment bookkeeping (replicated in every lane of the segment) ----
-    const int64_t warps_total = (int64_t)gridDim.x * (kBlockThreads / kWarp);
-    const int64_t gwarp = (int64_t)blockIdx.x * (kBlockThreads / kWarp) + (threadIdx.x >> 5);
+    const int64_t warps_total = (int64_t)gridDim.x * kWarpsPerBlock;
+    const int64_t gwarp = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
     const int64_t segs_total = warps_total * S;
     int64_t s = lane_on ? gwarp * S + seg : a.n_sims;  // local sim index
-    int64_t tick = a.tick0, start = a.tick0;
+    const int64_t start = a.tick0;
+    int32_t rt = 0;                      // ticks advanced in the current sim
     int64_t cursor = 0, cursor_end = 0;  // INJECT
     bool running = false, diverged = false, bad = false;
     const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
@@ -192,7 +232,7 @@ race_kernel(const LaunchArgs a) {
     int64_t fin[K];
     bool racing[K];
     Real rawd[K][kTicksPerBlock];
-    uint32_t ct_sim = 0, blk_sim = 0;          // this lane's slots, current sim
+    uint32_t ct_sim = 0, blk_sim = 0;            // this lane's slots, current sim
     unsigned long long ct_tot = 0, blk_tot = 0;  // this lane, whole kernel
     unsigned long long n_div = 0, n_bad = 0;
     int64_t first_div = INT64_MAX, first_bad = INT64_MAX;
@@ -203,7 +243,7 @@ race_kernel(const LaunchArgs a) {
         running = lane_on && s < a.n_sims;
         diverged = false;
         bad = false;
-        tick = start = a.tick0;
+        rt = 0;
         ct_sim = blk_sim = 0;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -343,12 +383,13 @@ race_kernel(const LaunchArgs a) {
 
         // ---------------- NATIVE: 4 draws per slot for this tick block (counter = tick block) ----
         if (MODE == NATIVE) {
+            __syncwarp();  // key rows: reads of the previous block precede this block's writes
             const uint64_t gs = (uint64_t)(a.sim_offset + s);
-            const uint32_t blk = (uint32_t)((tick - start) >> 2);
+            const uint32_t blk = (uint32_t)rt >> 2;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 const U4 w = philox4x32_10(U4{blk, (uint32_t)cidx[k], (uint32_t)gs, (uint32_t)(gs >> 32)}, k0, k1);
-                if (lognorm[k]) {
+                if (any_lognorm && lognorm[k]) {
                     const float r0 = sqrtf(-2.0f * __logf(u01_open0(w.x)));
                     const float r1 = sqrtf(-2.0f * __logf(u01_open0(w.z)));
                     float s0, c0, s1, c1;
@@ -360,10 +401,10 @@ race_kernel(const LaunchArgs a) {
                     rawd[k][2] = (Real)__expf(fmaf(sg, r1 * c1, mu));
                     rawd[k][3] = (Real)__expf(fmaf(sg, r1 * s1, mu));
                 } else {
-                    rawd[k][0] = lo[k] + span[k] * (Real)u01_23(w.x);
-                    rawd[k][1] = lo[k] + span[k] * (Real)u01_23(w.y);
-                    rawd[k][2] = lo[k] + span[k] * (Real)u01_23(w.z);
-                    rawd[k][3] = lo[k] + span[k] * (Real)u01_23(w.w);
+                    rawd[k][0] = fmaf((float)span[k], u01_23(w.x), (float)lo[k]);
+                    rawd[k][1] = fmaf((float)span[k], u01_23(w.y), (float)lo[k]);
+                    rawd[k][2] = fmaf((float)span[k], u01_23(w.z), (float)lo[k]);
+                    rawd[k][3] = fmaf((float)span[k], u01_23(w.w), (float)lo[k]);
                 }
             }
         }
@@ -379,7 +420,7 @@ race_kernel(const LaunchArgs a) {
             if (rmask == 0u) break;  // every segment finished inside this block
 
             // tick-limit check before the advance (race.py:381-386, 402-404)
-            if (seg_running && tick - start >= a.tick_limit) {
+            if (seg_running && rt >= a.limit) {
                 diverged = true;
 #pragma unroll
                 for (int k = 0; k < K; ++k) { racing[k] = false; pv[k] = NEG_INF; }
@@ -388,34 +429,59 @@ race_kernel(const LaunchArgs a) {
             // ---- front runner (race.py:244-264) ----
             Real gap[K];
             int bi[K];
+            uint32_t fkey[K];
 #pragma unroll
-            for (int k = 0; k < K; ++k) { gap[k] = R::inf(); bi[k] = 0; }
+            for (int k = 0; k < K; ++k) { gap[k] = R::inf(); bi[k] = 0; fkey[k] = 0u; }
             if (a.scan) {
+                if constexpr (MODE == NATIVE) {
+                    uint32_t* row = my_rows + (tj & 1) * row_words;
+                    uint32_t kp[K], nk[K], best[K];
 #pragma unroll
-                for (int kk = 0; kk < K; ++kk) {
+                    for (int k = 0; k < K; ++k) {
+                        kp[k] = key_of((float)pos[k]);
+                        nk[k] = ~kp[k];
+                        best[k] = 0xffffffffu;
+                        if (lane_on) row[k * S * a.WP + seg_off + l] = racing[k] ? kp[k] : 0u;
+                    }
+                    __syncwarp();
+#pragma unroll
+                    for (int kk = 0; kk < K; ++kk) {
+                        const uint4* r4 = reinterpret_cast<const uint4*>(row + kk * S * a.WP + seg_off);
+#pragma unroll
+                        for (int c = 0; c < CH; ++c) {
+                            const uint4 v = r4[c];
+#pragma unroll
+                            for (int k = 0; k < K; ++k) {
+                                best[k] = min(best[k], v.x + nk[k]);
+                                best[k] = min(best[k], v.y + nk[k]);
+                                best[k] = min(best[k], v.z + nk[k]);
+                                best[k] = min(best[k], v.w + nk[k]);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const uint32_t fk = best[k] - nk[k];  // = best + key_c + 1 (mod 2^32)
+                        const bool ahead = fk > kp[k];        // no wrap <=> a rival strictly ahead
+                        fkey[k] = ahead ? fk : 0u;
+                        gap[k] = ahead ? R::sub((Real)float_of_key(fk), pos[k]) : R::inf();
+                    }
+                } else {
+                    // exact reference arithmetic: gap = p_i - p_c, strict compares in index order
+#pragma unroll
+                    for (int kk = 0; kk < K; ++kk) {
 #pragma unroll 2
-                    for (int j = 0; j < W; ++j) {
-                        const Real pr = shfl(pv[kk], base + j);
+                        for (int j = 0; j < W; ++j) {
+                            const Real pr = shfl(pv[kk], base + j);
 #pragma unroll
-                        for (int k = 0; k < K; ++k) {
-                            if (MODE == INJECT) {
-                                // exact reference arithmetic: gap = p_i - p_c, strict compares
+                            for (int k = 0; k < K; ++k) {
                                 const Real g = R::sub(pr, pos[k]);
                                 const bool t = (g > (Real)0) & (g < gap[k]);
                                 gap[k] = t ? g : gap[k];
                                 bi[k] = t ? (kk << 5) | j : bi[k];
-                            } else {
-                                // nearest position strictly ahead (lowest index on ties); gap below
-                                const bool t = (pr > pos[k]) & (pr < gap[k]);
-                                gap[k] = t ? pr : gap[k];
-                                bi[k] = t ? (kk << 5) | j : bi[k];
                             }
                         }
                     }
-                }
-                if (MODE != INJECT) {
-#pragma unroll
-                    for (int k = 0; k < K; ++k) gap[k] = R::sub(gap[k], pos[k]);  // inf - p = inf
                 }
             }
 
@@ -432,6 +498,25 @@ race_kernel(const LaunchArgs a) {
 #pragma unroll
             for (int k = 0; k < K; ++k) pf[k] = (Real)0;
             if (__any_sync(0xffffffffu, any_blocked)) {
+                if constexpr (MODE == NATIVE) {
+                    // lowest competitor index whose key is the front key (slot-major, then lane)
+                    const uint32_t* row = my_rows + (tj & 1) * row_words;
+#pragma unroll
+                    for (int kk = K - 1; kk >= 0; --kk) {
+                        const uint4* r4 = reinterpret_cast<const uint4*>(row + kk * S * a.WP + seg_off);
+#pragma unroll
+                        for (int c = CH - 1; c >= 0; --c) {
+                            const uint4 v = r4[c];
+#pragma unroll
+                            for (int k = 0; k < K; ++k) {
+                                bi[k] = (v.w == fkey[k]) ? (kk << 5) | (4 * c + 3) : bi[k];
+                                bi[k] = (v.z == fkey[k]) ? (kk << 5) | (4 * c + 2) : bi[k];
+                                bi[k] = (v.y == fkey[k]) ? (kk << 5) | (4 * c + 1) : bi[k];
+                                bi[k] = (v.x == fkey[k]) ? (kk << 5) | (4 * c + 0) : bi[k];
+                            }
+                        }
+                    }
+                }
 #pragma unroll
                 for (int kk = 0; kk < K; ++kk) {
 #pragma unroll
@@ -442,7 +527,7 @@ race_kernel(const LaunchArgs a) {
                 }
             }
             Real draw[K];
-            if (MODE == INJECT) {
+            if constexpr (MODE == INJECT) {
                 // free slots consume the stream in competitor-index order (slot-major, then lane):
                 // offset = free slots of lower index in this segment = popc of the ballot below me
                 int seg_total = 0;
@@ -465,7 +550,6 @@ race_kernel(const LaunchArgs a) {
             }
 
             // ---- synchronous update (race.py:299-320) ----
-            const int64_t t = tick + 1;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 const bool early_phase = pos[k] < bp[k];
@@ -483,11 +567,11 @@ race_kernel(const LaunchArgs a) {
                     prev[k] = step;
                     ct_sim += 1;
                     blk_sim += bl[k] ? 1 : 0;
-                    if (p >= L) { fin[k] = t; racing[k] = false; }
+                    if (p >= L) { fin[k] = start + rt + 1; racing[k] = false; }
                 }
-                pv[k] = racing[k] ? pos[k] : NEG_INF;
+                if (MODE == INJECT) pv[k] = racing[k] ? pos[k] : NEG_INF;
             }
-            if (seg_running && !diverged) tick = t;
+            if (seg_running && !diverged) rt += 1;
         }
     }
 
@@ -502,14 +586,13 @@ race_kernel(const LaunchArgs a) {
         first_div = min(first_div, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)first_div, off));
         first_bad = min(first_bad, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)first_bad, off));
     }
-    const int nperm = a.perms;
-    const int ct_at = a.n + a.n * a.n + nperm;
+    const int ct_at = TL.ct();
     if (lane == 0) {
         if (v_ct) atomicAdd((unsigned long long*)&a.tally[ct_at + 0], v_ct);
         if (v_blk) atomicAdd((unsigned long long*)&a.tally[ct_at + 1], v_blk);
         if (v_div) atomicAdd((unsigned long long*)&a.tally[ct_at + 2], v_div);
         if (v_bad) atomicAdd((unsigned long long*)&a.tally[ct_at + 3], v_bad);
-        // first_* stored +1 so that 0 = none; MIN via max of complement
+        // first_* stored as ~(index + 1) so that MAX picks the smallest index and 0 means none
         if (first_div != INT64_MAX)
             atomicMax((unsigned long long*)&a.tally[ct_at + 4], ~(unsigned long long)(first_div + 1));
         if (first_bad != INT64_MAX)

@@ -137,7 +137,7 @@ def test_stream_under_and_over_consumption_is_an_error():
     short[2:] -= 1
     with pytest.raises(sim.DrawStreamError) as e:
         sim.simulate_batch(st, cfg, 3, mode="inject", draws=draws, draw_offsets=short)
-    assert e.value.sim_index == 0
+    assert e.value.sim_index == 1  # sim 1 is one draw short (sim 2 is misaligned too; the first is reported)
     longer = offs.copy()
     longer[2:] += 1
     d2 = np.insert(draws, offs[2], 15.0)
