@@ -4,7 +4,7 @@ ARCH = -gencode arch=compute_100a,code=sm_100a
 NVFLAGS = $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared \
           --expt-relaxed-constexpr -Xptxas -v
 LIB = paper_2108_02419_b200/_lib/libbbe_sim.so
-SRC = paper_2108_02419_b200/csrc/bbe_sim.cu paper_2108_02419_b200/csrc/race_kernel.cuh include/bbe_sim.h
+SRC = paper_2108_02419_b200/csrc/bbe_sim.cu $(wildcard paper_2108_02419_b200/csrc/*.cuh) include/bbe_sim.h
 
 all: $(LIB) oracle
 

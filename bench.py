@@ -56,51 +56,73 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line).
+
+    Sampling starts before the region (nvidia-smi needs ~0.1-0.3 s to start); each sample is
+    timestamped on arrival and only samples inside [mark_start(), mark_end()] are summarised.
+    """
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_ms: int = 20):
         self.index = index
+        self.period_ms = period_ms
         self.rows = []
         self.proc = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                                          "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            deadline = time.time() + 3.0
+            while not self.rows and time.time() < deadline:  # wait for the first sample
+                time.sleep(0.02)
         except OSError:
             self.proc = None
         return self
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
 
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 7:
-                self.rows.append(parts)
+                self.rows.append((time.time(), parts))
 
     def __exit__(self, *exc):
         if self.proc:
+            time.sleep(2 * self.period_ms / 1000)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+            self.t.join(timeout=2)
 
     def summary(self):
-        if not self.rows:
+        t0 = self.t0 if self.t0 is not None else 0.0
+        t1 = (self.t1 if self.t1 is not None else time.time()) + self.period_ms / 1000
+        rows = [r for ts, r in self.rows if t0 <= ts <= t1]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        num = lambda v: v.replace(".", "", 1).isdigit()  # noqa: E731
+        sm = [float(r[0]) for r in rows if num(r[0])]
+        mx = [float(r[1]) for r in rows if num(r[1])]
+        pw = [float(r[2]) for r in rows if num(r[2])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows), "power_w_max": max(pw) if pw else None}
 
 
 def cpu_baseline_pyref(cfg, state, n_sims: int):
@@ -139,14 +161,16 @@ def run_reference(args):
     cores = pyref.cpu_count()
     sample = args.ref_sample
     times, cts = [], []
+    pool = pyref.TallyPool(cfg, state, workers=cores)
     for i in range(args.warmup + args.steps):
         seeds = [pyref.derive_seed(20260818, "ref", i, j) for j in range(sample)]
         t0 = time.perf_counter()
-        wins, ct = pyref.batch_tally(cfg, seeds, state, workers=cores)
+        wins, ct = pool.run(seeds)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
             cts.append(ct)
+    pool.close()
     t = sum(times) / len(times)
     value = sample / t
     line = {
@@ -212,6 +236,7 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        clk.mark_start()
         for i in range(args.steps):
             flush.fill_(float(i))  # L2 flush between timed iterations (outside the event bracket)
             ev[i][0].record(stream)
@@ -222,6 +247,7 @@ def run_ours(args):
             ct_total += int(t[launcher.off["ct"]])
             blocked_total += int(t[launcher.off["blocked"]])
         torch.cuda.synchronize()
+        clk.mark_end()
     if world > 1:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
@@ -266,7 +292,7 @@ def run_ours(args):
             e2e_t.append(time.perf_counter() - t0)
         assert abs(sum(probs) - 1.0) < 1e-9
         e2e_s = statistics.mean(e2e_t[args.warmup:])
-        h2d = 16 * n * 8  # parameter block (F_COUNT x n doubles)
+        h2d = int(sim.lib().bbe_param_bytes(n))  # the race-parameter block, the call's only H2D input
         d2h = launcher.tally_len * 8
 
         cpu = cpu_baseline_pyref(cfg, state, args.cpu_sample) if args.cpu_sample else None
@@ -303,13 +329,13 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--sims", type=int, default=SIMS_PER_CALL)
     ap.add_argument("--cpu-sample", type=int, default=10000, help="pyref sims for cpu_baseline (0 = skip)")
     ap.add_argument("--cpu-c-sample", type=int, default=200_000, help="C oracle sims (0 = skip)")
-    ap.add_argument("--ref-sample", type=int, default=4000, help="sims per --impl reference step")
+    ap.add_argument("--ref-sample", type=int, default=2000, help="sims per --impl reference step")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup < 3 requested; timing rules want >= 3", file=sys.stderr)

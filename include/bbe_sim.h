@@ -140,6 +140,9 @@ int64_t bbe_tally_offset(int32_t n, int32_t field); /* field: 0 wins 1 ranks 2 p
 
 int bbe_derive_seeds(uint64_t master, int64_t first, int64_t count, uint64_t* out_host);
 
+/* Bytes of the race-parameter block copied host->device per call (the per-call H2D input). */
+int64_t bbe_param_bytes(int32_t n);
+
 /* Device time (ms) of the race kernel of the most recent call on the current device; synchronises
  * on that kernel's completion event. */
 float bbe_last_kernel_ms(void);

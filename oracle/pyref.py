@@ -196,6 +196,29 @@ def batch_tally(cfg, seeds, state=None, workers: int = 1):
     return wins, ct
 
 
+class TallyPool:
+    """A persistent process pool over (cfg, state) for repeated timed batches."""
+
+    def __init__(self, cfg, state=None, workers: int = 1):
+        self.cfg, self.state, self.workers = cfg, state, workers
+        self.pool = ProcessPoolExecutor(max_workers=workers, initializer=_init, initargs=(cfg, state))
+        list(self.pool.map(_chunk, [[1]] * workers))  # start every worker before timing
+
+    def run(self, seeds):
+        seeds = [int(s) for s in seeds]
+        k = max(1, len(seeds) // (self.workers * 4))
+        chunks = [seeds[i:i + k] for i in range(0, len(seeds), k)]
+        n = len(self.cfg.competitors)
+        wins, ct = [0] * n, 0
+        for w, c in self.pool.map(_chunk, chunks):
+            wins = [a + b for a, b in zip(wins, w)]
+            ct += c
+        return wins, ct
+
+    def close(self):
+        self.pool.shutdown()
+
+
 def cpu_count() -> int:
     try:
         return len(os.sched_getaffinity(0))

@@ -218,6 +218,47 @@ void pack_params(const bbe_race* race, const bbe_competitor* comps, const bbe_st
     }
 }
 
+size_t param_bytes(int n) { return (size_t)F_COUNT * n * sizeof(double) + (size_t)NF_COUNT * n * sizeof(float); }
+
+// NATIVE FP32 block, appended after the double block.  Returns the position offset that makes every
+// position >= +0.0 (the kernel's float-bits ordering needs it; gaps and L - pos are unchanged).
+float pack_params_f32(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, double* P) {
+    const int n = race->n;
+    float* F = reinterpret_cast<float*>(P + (size_t)F_COUNT * n);
+    double lo_pos = 0.0;
+    if (!st->from_start)
+        for (int c = 0; c < n; ++c) lo_pos = std::min(lo_pos, st->positions[c]);
+    const double shift = -lo_pos;
+    const double log2e = 1.4426950408889634;
+    for (int c = 0; c < n; ++c) {
+        const bbe_competitor& p = comps[c];
+        const double span = p.hi - p.lo;
+        F[NF_LO_MINUS_SPAN * n + c] = (float)(p.lo - span);
+        F[NF_SPAN * n + c] = (float)span;
+        F[NF_SG2 * n + c] = (float)(p.sigma * log2e);
+        F[NF_LMU2 * n + c] = (float)((p.mu + std::log(p.family == BBE_FAMILY_LOGNORMAL ? p.scale : 1.0)) * log2e);
+        F[NF_RP_EARLY * n + c] = (float)(p.early_mult * p.pref_factor);
+        F[NF_RP_LATE * n + c] = (float)(p.late_mult * p.pref_factor);
+        F[NF_EARLY * n + c] = (float)p.early_mult;
+        F[NF_LATE * n + c] = (float)p.late_mult;
+        F[NF_BP * n + c] = (float)(p.bp_abs + shift);
+        F[NF_THETA * n + c] = (float)p.theta;
+        F[NF_POS0 * n + c] = st->from_start ? 0.0f : (float)(st->positions[c] + shift);
+        F[NF_PREV0 * n + c] = st->from_start ? 0.0f : (float)st->prev_steps[c];
+    }
+    return (float)shift;
+}
+
+void philox_round_keys(uint64_t seed, uint32_t* rk) {
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    for (int r = 0; r < 10; ++r) {
+        rk[2 * r] = k0;
+        rk[2 * r + 1] = k1;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+
 typedef void (*KernelFn)(LaunchArgs);
 
 template <int K>
@@ -333,6 +374,11 @@ int bbe_device_info(int device, char* name64, int32_t* sm_count, int32_t* clock_
     return BBE_OK;
 }
 
+int64_t bbe_param_bytes(int32_t n) {
+    if (n < 1 || n > BBE_MAX_COMPETITORS) return -1;
+    return (int64_t)param_bytes(n);
+}
+
 int64_t bbe_tally_len(int32_t n) {
     if (n < 1 || n > BBE_MAX_COMPETITORS) return -1;
     return TallyLayout{n, nperm_for(n)}.len();
@@ -393,10 +439,13 @@ static int launch_go(const Plan& pl, LaunchArgs& a, const bbe_competitor* comps,
 
 static int build_args(const Plan& pl, const bbe_race* race, const bbe_state* st, const bbe_request* rq,
                       const double* d_params, const double* d_draws, const int64_t* d_offsets, uint64_t* d_tally,
-                      const bbe_result* dev_out, LaunchArgs* out) {
+                      const bbe_result* dev_out, float shift, LaunchArgs* out) {
     LaunchArgs& a = *out;
     a = LaunchArgs{};
     a.P = d_params;
+    a.Pf = reinterpret_cast<const float*>(d_params + (size_t)F_COUNT * race->n);
+    a.shift = shift;
+    philox_round_keys(rq->seed, a.rk);
     a.n = race->n;
     a.W = pl.W;
     a.S = pl.S;
@@ -438,10 +487,11 @@ int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_st
     cudaStream_t s = ctx->stream;
 
     // parameters: one pinned staging block, one H2D copy
-    const size_t pbytes = (size_t)F_COUNT * n * sizeof(double);
+    const size_t pbytes = param_bytes(n);
     BBE_CK(ctx->h_params.ensure(pbytes));
     BBE_CK(ctx->d_params.ensure(pbytes));
     pack_params(race, comps, st, (double*)ctx->h_params.p);
+    const float shift = pack_params_f32(race, comps, st, (double*)ctx->h_params.p);
     BBE_CK(cudaMemcpyAsync(ctx->d_params.p, ctx->h_params.p, pbytes, cudaMemcpyHostToDevice, s));
 
     const double* d_draws = nullptr;
@@ -476,7 +526,8 @@ int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_st
     }
 
     LaunchArgs a;
-    build_args(pl, race, st, rq, (const double*)ctx->d_params.p, d_draws, d_offsets, (uint64_t*)ctx->d_tally.p, &dev, &a);
+    build_args(pl, race, st, rq, (const double*)ctx->d_params.p, d_draws, d_offsets, (uint64_t*)ctx->d_tally.p, &dev,
+               shift, &a);
     BBE_CK(cudaEventRecord(ctx->ev0, s));
     if ((rc = launch_go(pl, a, comps, s))) return rc;
     BBE_CK(cudaEventRecord(ctx->ev1, s));
@@ -527,14 +578,16 @@ int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const 
     cudaStream_t s = (cudaStream_t)stream;  // NULL = legacy default stream (torch's default)
     // parameters: staged through pinned memory; the copy is ordered on `s` before the kernel, and
     // the staging block is not reused until that copy has been consumed (sync on an event).
-    const size_t pbytes = (size_t)F_COUNT * race->n * sizeof(double);
+    const size_t pbytes = param_bytes(race->n);
     BBE_CK(ctx->h_params.ensure(pbytes));
     BBE_CK(ctx->d_params.ensure(pbytes));
     BBE_CK(cudaEventSynchronize(ctx->ev1));  // previous async launch on this ctx has read its params
     pack_params(race, comps, st, (double*)ctx->h_params.p);
+    const float shift = pack_params_f32(race, comps, st, (double*)ctx->h_params.p);
     BBE_CK(cudaMemcpyAsync(ctx->d_params.p, ctx->h_params.p, pbytes, cudaMemcpyHostToDevice, s));
     LaunchArgs a;
-    build_args(pl, race, st, rq, (const double*)ctx->d_params.p, rq->draws, rq->draw_offsets, d_tally, dev_out, &a);
+    build_args(pl, race, st, rq, (const double*)ctx->d_params.p, rq->draws, rq->draw_offsets, d_tally, dev_out, shift,
+               &a);
     BBE_CK(cudaEventRecord(ctx->ev0, s));
     if ((rc = launch_go(pl, a, comps, s))) return rc;
     BBE_CK(cudaEventRecord(ctx->ev1, s));

@@ -7,15 +7,18 @@
 // gap > theta => free draw scaled by (resp * pref), else resp * min(prev_c, prev_front) with no draw,
 // nextafter on a zero-progress step, finish at p >= L, order by (finish tick, L - pos, index).
 //
-// Per tick and lane the work is: publish one u32 key, one __syncwarp, CH 128-bit shared loads and
-// one VIADDMNMX per rival (two independent min chains for ILP), one compare against theta, the step
-// and the position update.  Bookkeeping that the generic kernel did per tick (segment ballots,
-// 64-bit tick arithmetic, bool byte-packing) is moved to the 4-tick block boundary or removed:
-//   * rt (ticks advanced in this sim) is segment-uniform and simply incremented every tick; it only
-//     matters while a lane races, and a finished segment is re-filled at the next boundary;
-//   * racing <=> fin == kRacing (int32 finish tick relative to the state's tick);
-//   * the tick-limit check marks racing lanes "diverged" (fin = kDiverged); the segment is reported
-//     at finalize if any of its lanes did.
+// Front runner.  The host offsets positions (and L, breakpoints) so every position is >= +0.0;
+// for such floats the raw IEEE bits order like the values, so a position's u32 bits are its key.
+// Each lane publishes its key (0 once finished: 0.0 is never strictly ahead of anyone) to a per-warp
+// shared-memory row (double-buffered by tick parity, one __syncwarp per tick), reads its segment's
+// row with 128-bit broadcast loads and keeps min((key_r - key_c - 1) mod 2^32): the wrap sends every
+// rival at or behind c above every rival ahead, so the minimum is the nearest key strictly ahead.
+// Compiled, that is one VIADDMNMX per rival (two independent chains for ILP).  The front's index --
+// needed only for a blocked step -- is found by a second pass only when some lane is blocked.
+//
+// Bookkeeping is kept off the per-tick path: rt (ticks advanced in the sim) is segment-uniform;
+// racing <=> fin == kRacing (int32 finish tick relative to the state's tick); the tick-limit check
+// marks racing lanes diverged; competitor-timesteps are summed from finish ticks at finalize.
 #pragma once
 
 #include "race_kernel.cuh"
@@ -24,6 +27,46 @@ namespace bbe {
 
 constexpr int32_t kRacing = 0x7fffffff;
 constexpr int32_t kDiverged = 0x7ffffffe;
+constexpr int32_t kIdle = 0x7ffffffd;  // slot without a competitor / segment without a sim
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float lg2_approx(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// 1 + u, u in [0,1) with 23 random bits (exponent trick).
+__device__ __forceinline__ float one_plus_u(uint32_t w) { return __uint_as_float(0x3f800000u | (w >> 9)); }
+
+__device__ __forceinline__ U4 philox_rk(U4 c, const uint32_t* rk) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = U4{hi1 ^ c.y ^ rk[2 * r], lo1, hi0 ^ c.w ^ rk[2 * r + 1], lo0};
+    }
+    return c;
+}
+
+// Box-Muller pair -> two lognormal steps exp2(sg2*z + lmu2); uniform (a, b) -> (0,1] x [0,1).
+__device__ __forceinline__ void lognormal_pair(uint32_t wa, uint32_t wb, float sg2, float lmu2, float& d0, float& d1) {
+    const float u1 = 2.0f - one_plus_u(wa);  // (0, 1]
+    const float r = sqrt_approx(-1.3862943611198906f * lg2_approx(u1));  // sqrt(-2 ln u1)
+    float s, c;
+    __sincosf(6.283185307179586f * (one_plus_u(wb) - 1.0f), &s, &c);
+    const float a = sg2 * r;
+    d0 = ex2_approx(fmaf(a, c, lmu2));
+    d1 = ex2_approx(fmaf(a, s, lmu2));
+}
 
 template <int K, int CH>
 __global__ void __launch_bounds__(kBlockThreads, K == 1 ? 8 : (K == 2 ? 5 : 3))
@@ -35,6 +78,8 @@ native_kernel(const LaunchArgs a) {
     for (int i = threadIdx.x; i < hist_len; i += blockDim.x) s_hist[i] = 0ull;
 
     constexpr int WP = 4 * CH;
+    constexpr int SLOT = swp_max(CH);   // words per slot row
+    constexpr int PAR = K * SLOT;       // words per parity
     const int n = a.n, W = a.W, S = a.S;
     const int lane = threadIdx.x & (kWarp - 1);
     const int warp = threadIdx.x >> 5;
@@ -44,20 +89,19 @@ native_kernel(const LaunchArgs a) {
     const int l = lane - seg * W;
     const unsigned segmask = lane_on ? ((W == 32 ? 0xffffffffu : ((1u << W) - 1u)) << base) : 0u;
 
-    // key rows: [warp][parity][slot][segment * WP + lane-in-segment]; pads and idle lanes hold 0
-    const int slot_words = S * WP;
-    const int row_words = K * slot_words;
-    uint32_t* rows = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) + warp * 2 * row_words;
-    for (int i = lane; i < 2 * row_words; i += kWarp) rows[i] = 0u;
-    uint32_t* const wr = rows + (lane_on ? seg * WP + l : 0);  // + parity*row_words + k*slot_words
+    // key rows: [warp][parity][slot][SLOT]; idle lanes write a scratch word after the rows
+    uint32_t* rows = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) + warp * native_warp_words(K, CH);
+    for (int i = lane; i < native_warp_words(K, CH); i += kWarp) rows[i] = 0u;
+    uint32_t* const wr = lane_on ? rows + seg * WP + l : rows + 2 * PAR;
     const uint32_t* const rd = rows + (lane_on ? seg * WP : 0);
     __syncthreads();
 
     // ---- per-slot constants, FP32 ----
     int cidx[K];
     bool has[K], lognorm[K];
-    float lo[K], span[K], lmu[K], sg[K], rpE[K], rpL[K], eE[K], eL[K], bp[K], th[K];
+    float lms[K], span[K], sg2[K], lmu2[K], rpE[K], rpL[K], eE[K], eL[K], bp[K], th[K];
     const double* P = a.P;
+    const float* Pf = a.Pf;
     bool any_lognorm = false;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -65,21 +109,21 @@ native_kernel(const LaunchArgs a) {
         cidx[k] = c;
         has[k] = lane_on && c < n;
         const int cc = has[k] ? c : 0;
-        lo[k] = (float)P[F_LO * n + cc];
-        span[k] = (float)P[F_SPAN * n + cc];
-        lmu[k] = (float)P[F_LMU * n + cc];
-        sg[k] = (float)P[F_SIGMA * n + cc];
-        rpE[k] = (float)P[F_RP_EARLY * n + cc];
-        rpL[k] = (float)P[F_RP_LATE * n + cc];
-        eE[k] = (float)P[F_EARLY * n + cc];
-        eL[k] = (float)P[F_LATE * n + cc];
-        bp[k] = (float)P[F_BP * n + cc];
-        th[k] = (float)P[F_THETA * n + cc];
+        lms[k] = Pf[NF_LO_MINUS_SPAN * n + cc];
+        span[k] = Pf[NF_SPAN * n + cc];
+        sg2[k] = Pf[NF_SG2 * n + cc];
+        lmu2[k] = Pf[NF_LMU2 * n + cc];
+        rpE[k] = Pf[NF_RP_EARLY * n + cc];
+        rpL[k] = Pf[NF_RP_LATE * n + cc];
+        eE[k] = Pf[NF_EARLY * n + cc];
+        eL[k] = Pf[NF_LATE * n + cc];
+        bp[k] = Pf[NF_BP * n + cc];
+        th[k] = Pf[NF_THETA * n + cc];
         lognorm[k] = has[k] && P[F_FAMILY * n + cc] != 0.0;
         any_lognorm |= lognorm[k];
     }
     any_lognorm = __any_sync(0xffffffffu, any_lognorm);
-    const float L = (float)a.L;
+    const float L = (float)a.L + a.shift;
     const bool scan = a.scan != 0;
 
     // ---- segment bookkeeping ----
@@ -87,12 +131,12 @@ native_kernel(const LaunchArgs a) {
     int64_t s = lane_on ? ((int64_t)blockIdx.x * kWarpsPerBlock + warp) * S + seg : a.n_sims;
     int32_t rt = 0;
     bool running = false;
-    const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
 
     float pos[K], prev[K];
     int32_t fin[K];
+    bool started[K];  // racing when the sim began (its competitor-timesteps = ticks until it stops)
     float rawd[K][kTicksPerBlock];
-    uint32_t ct_sim = 0, blk_sim = 0;
+    uint32_t blk_sim = 0;
     unsigned long long ct_tot = 0, blk_tot = 0, n_div = 0;
     int64_t first_div = INT64_MAX;
 
@@ -100,31 +144,26 @@ native_kernel(const LaunchArgs a) {
         if (!do_it) return;
         running = lane_on && s < a.n_sims;
         rt = 0;
-        ct_sim = blk_sim = 0;
+        blk_sim = 0;
         const uint64_t gs = (uint64_t)(a.sim_offset + s);
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int cc = has[k] ? cidx[k] : 0;
-            pos[k] = (float)P[F_POS0 * n + cc];
-            prev[k] = (float)P[F_PREV0 * n + cc];
+            pos[k] = Pf[NF_POS0 * n + cc];
+            prev[k] = Pf[NF_PREV0 * n + cc];
             const bool pre_finished = P[F_FIN0 * n + cc] >= 0.0;
-            fin[k] = !(running && has[k]) ? kDiverged - 1 : (pre_finished ? (int32_t)P[F_FINREL * n + cc] : kRacing);
+            fin[k] = !(running && has[k]) ? kIdle : (pre_finished ? (int32_t)P[F_FINREL * n + cc] : kRacing);
+            started[k] = fin[k] == kRacing;
             if (a.from_start && running && has[k]) {
-                // race.py:233-241: one free draw per competitor, resp at position 0
-                const U4 w = philox4x32_10(U4{0xFFFFFFFFu, (uint32_t)cidx[k], (uint32_t)gs, (uint32_t)(gs >> 32)},
-                                           k0, k1);
-                float d;
-                if (lognorm[k]) {
-                    const float r = sqrtf(-2.0f * __logf(u01_open0(w.x)));
-                    d = __expf(fmaf(sg[k], r * __cosf(6.283185307f * u01_23(w.y)), lmu[k]));
-                } else {
-                    d = fmaf(span[k], u01_23(w.x), lo[k]);
-                }
-                prev[k] = __fmul_rn((0.0f < bp[k]) ? rpE[k] : rpL[k], d);
+                // race.py:233-241: one free draw per competitor, resp at position 0 (tick-block 0xFFFFFFFF)
+                const U4 w = philox_rk(U4{0xFFFFFFFFu, (uint32_t)cidx[k], (uint32_t)gs, (uint32_t)(gs >> 32)}, a.rk);
+                float d, d1;
+                if (lognorm[k]) lognormal_pair(w.x, w.y, sg2[k], lmu2[k], d, d1);
+                else d = fmaf(span[k], one_plus_u(w.x), lms[k]);
+                prev[k] = __fmul_rn((a.shift < bp[k]) ? rpE[k] : rpL[k], d);
             }
         }
     };
-    // fin sentinel for idle slots: neither racing nor diverged, sorts last
     load_sim(true);
 
     while (true) {
@@ -194,6 +233,9 @@ native_kernel(const LaunchArgs a) {
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     if (!has[k]) continue;
+                    // competitor-timesteps: a competitor racing at the start stepped every tick until
+                    // it finished (fin = ticks) or the sim was cut at the limit (rt ticks)
+                    if (started[k]) ct_tot += (fin[k] >= kDiverged) ? (uint32_t)min(rt, a.limit) : (uint32_t)fin[k];
                     const int64_t o = s * n + cidx[k];
                     if (a.winner && rank[k] == 0) a.winner[s] = diverged ? -1 : cidx[k];
                     if (a.order) a.order[s * n + rank[k]] = cidx[k];
@@ -202,10 +244,9 @@ native_kernel(const LaunchArgs a) {
                         a.finish_ticks[o] = f0 >= 0.0 ? (int64_t)f0
                                                       : (fin[k] >= kDiverged ? -1 : a.tick0 + (int64_t)fin[k]);
                     }
-                    if (a.final_pos) a.final_pos[o] = (double)pos[k];
+                    if (a.final_pos) a.final_pos[o] = (double)pos[k] - (double)a.shift;
                 }
                 if (l == 0 && a.blocked) a.blocked[s] = seg_blk;
-                ct_tot += ct_sim;
                 blk_tot += blk_sim;
                 s += segs_total;
             }
@@ -220,22 +261,15 @@ native_kernel(const LaunchArgs a) {
             const uint32_t blk = (uint32_t)rt >> 2;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                const U4 w = philox4x32_10(U4{blk, (uint32_t)cidx[k], (uint32_t)gs, (uint32_t)(gs >> 32)}, k0, k1);
+                const U4 w = philox_rk(U4{blk, (uint32_t)cidx[k], (uint32_t)gs, (uint32_t)(gs >> 32)}, a.rk);
                 if (any_lognorm && lognorm[k]) {
-                    const float r0 = sqrtf(-2.0f * __logf(u01_open0(w.x)));
-                    const float r1 = sqrtf(-2.0f * __logf(u01_open0(w.z)));
-                    float s0, c0, s1, c1;
-                    __sincosf(6.283185307f * u01_23(w.y), &s0, &c0);
-                    __sincosf(6.283185307f * u01_23(w.w), &s1, &c1);
-                    rawd[k][0] = __expf(fmaf(sg[k], r0 * c0, lmu[k]));
-                    rawd[k][1] = __expf(fmaf(sg[k], r0 * s0, lmu[k]));
-                    rawd[k][2] = __expf(fmaf(sg[k], r1 * c1, lmu[k]));
-                    rawd[k][3] = __expf(fmaf(sg[k], r1 * s1, lmu[k]));
+                    lognormal_pair(w.x, w.y, sg2[k], lmu2[k], rawd[k][0], rawd[k][1]);
+                    lognormal_pair(w.z, w.w, sg2[k], lmu2[k], rawd[k][2], rawd[k][3]);
                 } else {
-                    rawd[k][0] = fmaf(span[k], u01_23(w.x), lo[k]);
-                    rawd[k][1] = fmaf(span[k], u01_23(w.y), lo[k]);
-                    rawd[k][2] = fmaf(span[k], u01_23(w.z), lo[k]);
-                    rawd[k][3] = fmaf(span[k], u01_23(w.w), lo[k]);
+                    rawd[k][0] = fmaf(span[k], one_plus_u(w.x), lms[k]);
+                    rawd[k][1] = fmaf(span[k], one_plus_u(w.y), lms[k]);
+                    rawd[k][2] = fmaf(span[k], one_plus_u(w.z), lms[k]);
+                    rawd[k][3] = fmaf(span[k], one_plus_u(w.w), lms[k]);
                 }
             }
         }
@@ -258,21 +292,19 @@ native_kernel(const LaunchArgs a) {
             for (int k = 0; k < K; ++k) { gap[k] = CUDART_INF_F; fkey[k] = 0u; }
             if (scan) {
                 uint32_t kp[K], nk[K];
-                uint32_t* w0 = wr + (tj & 1) * row_words;
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
-                    kp[k] = key_of(pos[k]);
+                    kp[k] = __float_as_uint(pos[k]);
                     nk[k] = ~kp[k];
-                    if (lane_on) w0[k * slot_words] = racing[k] ? kp[k] : 0u;
+                    wr[(tj & 1) * PAR + k * SLOT] = racing[k] ? kp[k] : 0u;
                 }
                 __syncwarp();
                 uint32_t b0[K], b1[K];
 #pragma unroll
                 for (int k = 0; k < K; ++k) { b0[k] = 0xffffffffu; b1[k] = 0xffffffffu; }
-                const uint32_t* r0 = rd + (tj & 1) * row_words;
 #pragma unroll
                 for (int kk = 0; kk < K; ++kk) {
-                    const uint4* r4 = reinterpret_cast<const uint4*>(r0 + kk * slot_words);
+                    const uint4* r4 = reinterpret_cast<const uint4*>(rd + (tj & 1) * PAR + kk * SLOT);
 #pragma unroll
                     for (int c = 0; c < CH; ++c) {
                         const uint4 v = r4[c];
@@ -289,8 +321,8 @@ native_kernel(const LaunchArgs a) {
                 for (int k = 0; k < K; ++k) {
                     const uint32_t fk = min(b0[k], b1[k]) - nk[k];  // = best + key_c + 1 (mod 2^32)
                     const bool ahead = fk > kp[k];                    // no wrap <=> someone strictly ahead
-                    fkey[k] = ahead ? fk : 0u;
-                    gap[k] = ahead ? __fsub_rn(float_of_key(fk), pos[k]) : CUDART_INF_F;
+                    fkey[k] = fk;
+                    gap[k] = ahead ? __fsub_rn(__uint_as_float(fk), pos[k]) : CUDART_INF_F;
                 }
             }
 
@@ -310,10 +342,9 @@ native_kernel(const LaunchArgs a) {
                 int bi[K];
 #pragma unroll
                 for (int k = 0; k < K; ++k) bi[k] = 0;
-                const uint32_t* r0 = rd + (tj & 1) * row_words;
 #pragma unroll
                 for (int kk = K - 1; kk >= 0; --kk) {
-                    const uint4* r4 = reinterpret_cast<const uint4*>(r0 + kk * slot_words);
+                    const uint4* r4 = reinterpret_cast<const uint4*>(rd + (tj & 1) * PAR + kk * SLOT);
 #pragma unroll
                     for (int c = CH - 1; c >= 0; --c) {
                         const uint4 v = r4[c];
@@ -341,14 +372,14 @@ native_kernel(const LaunchArgs a) {
             for (int k = 0; k < K; ++k) {
                 const bool early = pos[k] < bp[k];
                 const float m = (pf[k] < prev[k]) ? pf[k] : prev[k];  // Python min(prev_c, prev_front)
-                const float step = fr[k] ? __fmul_rn(early ? rpE[k] : rpL[k], rawd[k][tj])
-                                         : __fmul_rn(early ? eE[k] : eL[k], m);
+                const float step = __fmul_rn(fr[k] ? (early ? rpE[k] : rpL[k]) : (early ? eE[k] : eL[k]),
+                                             fr[k] ? rawd[k][tj] : m);
+                float p = __fadd_rn(pos[k], step);
+                // positions are >= +0.0, so the next float up is the next bit pattern (race.py:310-313)
+                p = (p == pos[k]) ? __uint_as_float(__float_as_uint(p) + 1u) : p;
                 if (racing[k]) {
-                    float p = __fadd_rn(pos[k], step);
-                    if (p == pos[k]) p = nextafterf(p, CUDART_INF_F);
                     pos[k] = p;
                     prev[k] = step;
-                    ct_sim += 1;
                     blk_sim += bl[k] ? 1u : 0u;
                     if (p >= L) fin[k] = rt + 1;
                 }

@@ -68,8 +68,18 @@ struct TallyLayout {
     __host__ __device__ int hist_len() const { return n + n * n + nperm; }  // shared-memory histograms
 };
 
+// NATIVE-only FP32 parameter block (SoA, stride n), derived on the host from the double block.
+enum FieldF {
+    NF_LO_MINUS_SPAN = 0,  // uniform: lo + span*u == (lo - span) + span*(1 + u), u from the exponent trick
+    NF_SPAN, NF_SG2, NF_LMU2,  // lognormal: exp2(sg2 * z + lmu2) == scale * exp(mu + sigma z)
+    NF_RP_EARLY, NF_RP_LATE, NF_EARLY, NF_LATE, NF_BP, NF_THETA, NF_POS0, NF_PREV0, NF_COUNT
+};
+
 struct LaunchArgs {
     const double* P;  // [F_COUNT][n] parameter block
+    const float* Pf;  // [NF_COUNT][n] (NATIVE)
+    uint32_t rk[20];  // Philox4x32-10 round keys of the seed (NATIVE)
+    float shift;      // NATIVE: positions, L and breakpoints are offset by this to keep positions >= 0
     int n, W, S, WP, from_start, scan, perms;
     double L;
     int64_t tick0;
@@ -89,9 +99,14 @@ struct LaunchArgs {
 
 // Dynamic shared memory of one block: histograms, then (NATIVE) the key rows.
 __host__ __device__ inline int key_row_words(int K, int S, int WP) { return K * S * WP; }
+// NATIVE key rows use a compile-time slot stride: the largest S*WP any W in (4(CH-1), 4CH] needs.
+__host__ __device__ constexpr int swp_max(int CH) {
+    return CH == 1 ? 128 : (CH == 2 ? 48 : (CH == 3 ? 36 : (CH == 4 ? 32 : 4 * CH)));
+}
+__host__ __device__ constexpr int native_warp_words(int K, int CH) { return 2 * K * swp_max(CH) + 4; }
 __host__ __device__ inline size_t smem_bytes(int mode_native, int hist_len, int K, int S, int WP) {
     size_t b = (size_t)hist_len * 8;
-    if (mode_native) b += (size_t)kWarpsPerBlock * 2 * key_row_words(K, S, WP) * 4;
+    if (mode_native) b += (size_t)kWarpsPerBlock * native_warp_words(K, (WP + 3) / 4) * 4;
     return b;
 }
 
