@@ -78,7 +78,7 @@ native_kernel(const LaunchArgs a) {
     for (int i = threadIdx.x; i < hist_len; i += blockDim.x) s_hist[i] = 0ull;
 
     constexpr int WP = 4 * CH;
-    constexpr int SLOT = swp_max(CH);   // words per slot row
+    constexpr int SLOT = native_slot_words(CH);  // words per slot row (segments, then a pad group)
     constexpr int PAR = K * SLOT;       // words per parity
     const int n = a.n, W = a.W, S = a.S;
     const int lane = threadIdx.x & (kWarp - 1);
@@ -89,10 +89,10 @@ native_kernel(const LaunchArgs a) {
     const int l = lane - seg * W;
     const unsigned segmask = lane_on ? ((W == 32 ? 0xffffffffu : ((1u << W) - 1u)) << base) : 0u;
 
-    // key rows: [warp][parity][slot][SLOT]; idle lanes write a scratch word after the rows
+    // key rows: [warp][parity][slot][SLOT]; lanes without a segment write the pad word of each row
     uint32_t* rows = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) + warp * native_warp_words(K, CH);
     for (int i = lane; i < native_warp_words(K, CH); i += kWarp) rows[i] = 0u;
-    uint32_t* const wr = lane_on ? rows + seg * WP + l : rows + 2 * PAR;
+    uint32_t* const wr = rows + (lane_on ? seg * WP + l : SLOT - 1);
     const uint32_t* const rd = rows + (lane_on ? seg * WP : 0);
     __syncthreads();
 

@@ -103,7 +103,9 @@ __host__ __device__ inline int key_row_words(int K, int S, int WP) { return K * 
 __host__ __device__ constexpr int swp_max(int CH) {
     return CH == 1 ? 128 : (CH == 2 ? 48 : (CH == 3 ? 36 : (CH == 4 ? 32 : 4 * CH)));
 }
-__host__ __device__ constexpr int native_warp_words(int K, int CH) { return 2 * K * swp_max(CH) + 4; }
+// +4: a padding word group at the end of every slot row, where lanes without a segment write.
+__host__ __device__ constexpr int native_slot_words(int CH) { return swp_max(CH) + 4; }
+__host__ __device__ constexpr int native_warp_words(int K, int CH) { return 2 * K * native_slot_words(CH); }
 __host__ __device__ inline size_t smem_bytes(int mode_native, int hist_len, int K, int S, int WP) {
     size_t b = (size_t)hist_len * 8;
     if (mode_native) b += (size_t)kWarpsPerBlock * native_warp_words(K, (WP + 3) / 4) * 4;
