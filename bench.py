@@ -213,7 +213,10 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg, state = load_workload()
     n = cfg.n_competitors
+    from paper_2108_02419_b200.parallel import TallyLayout, reduce_tally
+
     launcher = sim.DeviceLauncher(state, cfg)
+    layout = TallyLayout.for_n(n)
     tally = torch.zeros(launcher.tally_len, dtype=torch.int64, device="cuda")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
     stream = torch.cuda.current_stream()
@@ -224,7 +227,7 @@ def run_ours(args):
         tally.zero_()
         launcher.launch(tally.data_ptr(), sims, seed + i, sim_offset=rank * sims, stream=stream.cuda_stream)
         if world > 1:
-            dist.all_reduce(tally[: launcher.off["first_div"]])
+            reduce_tally(tally, layout)
 
     for i in range(args.warmup):
         step(i)

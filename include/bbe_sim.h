@@ -131,14 +131,20 @@ int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const 
                        const bbe_request* req, const bbe_result* dev_out, uint64_t* d_tally, void* stream);
 
 /* d_tally layout: [wins n][ranks n*n][perms n! or 0][ct][blocked][diverged count][bad-draw count]
- *                 [~(first_diverged + 1) or 0 = none][~(first_bad_draws + 1) or 0 = none]
- * Every field but the last two is SUM-reduced across shards; the last two are MAX-reduced (the bit
- * complement turns "smallest sim index" into "largest value"). */
+ *                 [(2^63-1) - first_diverged, or 0 = none][(2^63-1) - first_bad_draws, or 0 = none]
+ * Every field but the last two is SUM-reduced across shards; the last two are MAX-reduced (signed or
+ * unsigned alike), which keeps the smallest failing sim index. */
 int64_t bbe_tally_len(int32_t n);
 int64_t bbe_tally_offset(int32_t n, int32_t field); /* field: 0 wins 1 ranks 2 perms 3 ct 4 blocked
                                                        5 n_diverged 6 n_bad 7 first_div 8 first_bad */
 
 int bbe_derive_seeds(uint64_t master, int64_t first, int64_t count, uint64_t* out_host);
+
+/* agents.py:164 draws each dry-run seed as rng.getrandbits(64) from the bettor's CPython
+ * random.Random (MT19937).  This advances such a generator by `count` getrandbits(64) calls in
+ * place -- `state625` is random.Random.getstate()[1] (624 state words + position) as uint32 --
+ * and, when `out` is not NULL, stores the values drawn (low word first, as CPython builds them). */
+int bbe_mt_getrandbits64(uint32_t* state625, int64_t count, uint64_t* out);
 
 /* Bytes of the race-parameter block copied host->device per call (the per-call H2D input). */
 int64_t bbe_param_bytes(int32_t n);

@@ -374,6 +374,56 @@ int bbe_device_info(int device, char* name64, int32_t* sm_count, int32_t* clock_
     return BBE_OK;
 }
 
+int bbe_mt_getrandbits64(uint32_t* st, int64_t count, uint64_t* out) {
+    if (!st || count < 0) return fail(BBE_EINVAL, "bad arguments");
+    uint32_t* mt = st;
+    uint32_t idx = st[624];
+    if (idx > 624) return fail(BBE_EINVAL, "MT19937 position out of range");
+    auto twist = [mt]() {  // regenerate the 624-word block, in place (MT19937)
+        auto mix = [](uint32_t a, uint32_t b, uint32_t m) {
+            const uint32_t y = (a & 0x80000000u) | (b & 0x7fffffffu);
+            return m ^ (y >> 1) ^ (0u - (y & 1u) & 0x9908b0dfu);
+        };
+        int k = 0;
+        for (; k < 624 - 397; ++k) mt[k] = mix(mt[k], mt[k + 1], mt[k + 397]);
+        for (; k < 623; ++k) mt[k] = mix(mt[k], mt[k + 1], mt[k + 397 - 624]);
+        mt[623] = mix(mt[623], mt[0], mt[396]);
+    };
+    auto temper = [](uint32_t y) {
+        y ^= y >> 11;
+        y ^= (y << 7) & 0x9d2c5680u;
+        y ^= (y << 15) & 0xefc60000u;
+        return y ^ (y >> 18);
+    };
+    int64_t words = 2 * count;
+    if (!out) {  // advance only: whole blocks need no tempering
+        while (words > 0) {
+            if (idx >= 624) { twist(); idx = 0; }
+            const int64_t take = std::min<int64_t>(words, 624 - idx);
+            idx += (uint32_t)take;
+            words -= take;
+        }
+    } else {
+        int64_t i = 0;
+        while (i < count) {
+            if (idx >= 623) {  // need two words; handle the block edge one word at a time
+                uint32_t w[2];
+                for (int j = 0; j < 2; ++j) {
+                    if (idx >= 624) { twist(); idx = 0; }
+                    w[j] = temper(mt[idx++]);
+                }
+                out[i++] = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
+                continue;
+            }
+            const int64_t pairs = std::min<int64_t>(count - i, (624 - idx) / 2);
+            for (int64_t p = 0; p < pairs; ++p, idx += 2)
+                out[i++] = (uint64_t)temper(mt[idx]) | ((uint64_t)temper(mt[idx + 1]) << 32);
+        }
+    }
+    st[624] = idx;
+    return BBE_OK;
+}
+
 int64_t bbe_param_bytes(int32_t n) {
     if (n < 1 || n > BBE_MAX_COMPETITORS) return -1;
     return (int64_t)param_bytes(n);
@@ -551,8 +601,8 @@ int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_st
     if (out->perms && pl.nperm) std::memcpy(out->perms, T + TL.perms(), (size_t)pl.nperm * sizeof(uint64_t));
     out->competitor_steps = T[TL.ct()];
     out->blocked_steps = T[TL.blocked()];
-    out->first_diverged = T[TL.first_div()] ? (int64_t)(~T[TL.first_div()]) - 1 : -1;
-    out->first_bad_draws = T[TL.first_bad()] ? (int64_t)(~T[TL.first_bad()]) - 1 : -1;
+    out->first_diverged = decode_first(T[TL.first_div()]);
+    out->first_bad_draws = decode_first(T[TL.first_bad()]);
     float ms = 0.f;
     if (ns) cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
     out->kernel_ms = ms;

@@ -403,7 +403,7 @@ native_kernel(const LaunchArgs a) {
         if (v_blk) atomicAdd((unsigned long long*)&a.tally[ct_at + 1], v_blk);
         if (v_div) atomicAdd((unsigned long long*)&a.tally[ct_at + 2], v_div);
         if (first_div != INT64_MAX)
-            atomicMax((unsigned long long*)&a.tally[ct_at + 4], ~(unsigned long long)(first_div + 1));
+            atomicMax((unsigned long long*)&a.tally[ct_at + 4], encode_first(first_div));
     }
     __syncthreads();
     for (int i = threadIdx.x; i < hist_len; i += blockDim.x) {

@@ -52,6 +52,15 @@ enum Field {
     F_COUNT
 };
 
+// "First failing sim" tally fields hold (2^63 - 1) - index (0 = none): a MAX reduction -- atomicMax
+// in a kernel, or a signed int64 all-reduce across ranks -- then keeps the smallest index.
+__host__ __device__ inline unsigned long long encode_first(int64_t index) {
+    return 0x7fffffffffffffffull - (unsigned long long)index;
+}
+__host__ __device__ inline int64_t decode_first(unsigned long long v) {
+    return v ? (int64_t)(0x7fffffffffffffffull - v) : -1;
+}
+
 // Tally layout in u64 (see bbe_tally_offset in bbe_sim.h).
 struct TallyLayout {
     int n, nperm;
@@ -611,9 +620,9 @@ race_kernel(const LaunchArgs a) {
         if (v_bad) atomicAdd((unsigned long long*)&a.tally[ct_at + 3], v_bad);
         // first_* stored as ~(index + 1) so that MAX picks the smallest index and 0 means none
         if (first_div != INT64_MAX)
-            atomicMax((unsigned long long*)&a.tally[ct_at + 4], ~(unsigned long long)(first_div + 1));
+            atomicMax((unsigned long long*)&a.tally[ct_at + 4], encode_first(first_div));
         if (first_bad != INT64_MAX)
-            atomicMax((unsigned long long*)&a.tally[ct_at + 5], ~(unsigned long long)(first_bad + 1));
+            atomicMax((unsigned long long*)&a.tally[ct_at + 5], encode_first(first_bad));
     }
     __syncthreads();
     for (int i = threadIdx.x; i < hist_len; i += blockDim.x) {

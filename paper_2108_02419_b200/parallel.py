@@ -1,0 +1,127 @@
+"""Multi-GPU sharding of a simulation batch: one process per GPU, one tally all-reduce.
+
+Sims are independent (batch.py:1-8), so the global sim index range [0, N) is split
+into contiguous per-rank shards.  Every per-sim random stream is a pure function of the global sim
+index (NATIVE: Philox counter; MT: the sim's own seed; INJECT: its CSR draw range), so the reduced
+tallies are bit-identical for any number of ranks -- the GPU analogue of run_batch's worker-count
+invariance (batch.py:110-124, tests/test_batch.py:38-42).
+
+The only collective is the reduction of the tally vector (``bbe_tally_len(n)`` u64 counters,
+< 1 KB for n = 10): SUM over the counters, MAX over the two complement-encoded "first failing
+sim" fields (include/bbe_sim.h).  On NCCL it is enqueued on the same stream right after the kernel.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+TALLY_FIELDS = ("wins", "ranks", "perms", "ct", "blocked", "n_div", "n_bad", "first_div", "first_bad")
+
+
+def shard_range(n_sims: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous shard [lo, hi) of rank in world; sizes differ by at most one."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError(f"bad rank/world {rank}/{world}")
+    return n_sims * rank // world, n_sims * (rank + 1) // world
+
+
+@dataclass
+class TallyLayout:
+    n: int
+    nperm: int
+
+    @classmethod
+    def for_n(cls, n: int) -> "TallyLayout":
+        import math
+
+        return cls(n, math.factorial(n) if n <= 6 else 0)
+
+    @property
+    def ct(self) -> int:
+        return self.n + self.n * self.n + self.nperm
+
+    @property
+    def length(self) -> int:
+        return self.ct + 6
+
+    @property
+    def sum_len(self) -> int:
+        """Prefix reduced with SUM; the last two fields are reduced with MAX."""
+        return self.ct + 4
+
+
+def reduce_tally(tally, layout: TallyLayout, group=None) -> None:
+    """In-place all-reduce of one rank's tally tensor (torch int64; CUDA for NCCL, CPU for gloo)."""
+    import torch.distributed as dist
+
+    dist.all_reduce(tally[: layout.sum_len], op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(tally[layout.sum_len:], op=dist.ReduceOp.MAX, group=group)
+
+
+@dataclass
+class Tally:
+    wins: np.ndarray
+    ranks: np.ndarray
+    perms: np.ndarray | None
+    competitor_steps: int
+    blocked_steps: int
+    n_diverged: int
+    n_bad_draws: int
+    first_diverged: int
+    first_bad_draws: int
+
+
+def decode_tally(t: np.ndarray, layout: TallyLayout) -> Tally:
+    t = np.asarray(t).astype(np.uint64)
+    n = layout.n
+
+    def first(v):
+        v = int(v)
+        return -1 if v == 0 else (2**63 - 1) - v
+
+    return Tally(
+        wins=t[:n].copy(),
+        ranks=t[n:n + n * n].reshape(n, n).copy(),
+        perms=t[n + n * n:layout.ct].copy() if layout.nperm else None,
+        competitor_steps=int(t[layout.ct]),
+        blocked_steps=int(t[layout.ct + 1]),
+        n_diverged=int(t[layout.ct + 2]),
+        n_bad_draws=int(t[layout.ct + 3]),
+        first_diverged=first(t[layout.ct + 4]),
+        first_bad_draws=first(t[layout.ct + 5]),
+    )
+
+
+def encode_first(index: int) -> int:
+    """Encoding of a failing sim index as stored in the tally: (2^63 - 1) - index, 0 = none."""
+    return 0 if index < 0 else (2**63 - 1) - index
+
+
+def simulate_sharded(state, config, n_sims: int, seed: int = 0, *, group=None, lanes_per_slot: int = 0) -> Tally:
+    """NATIVE-mode batch over all ranks of ``group`` (one GPU per rank, NCCL).
+
+    Each rank simulates its contiguous shard of [0, n_sims) with global sim indices, the device
+    tallies are all-reduced, and every rank returns the job total.
+    """
+    import torch
+    import torch.distributed as dist
+
+    from .sim import DeviceLauncher, SimDivergedError
+
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    lo, hi = shard_range(int(n_sims), rank, world)
+    launcher = DeviceLauncher(state, config, lanes_per_slot=lanes_per_slot)
+    layout = TallyLayout.for_n(len(config.competitors))
+    assert layout.length == launcher.tally_len
+    tally = torch.zeros(layout.length, dtype=torch.int64, device="cuda")
+    launcher.launch(tally.data_ptr(), hi - lo, seed, sim_offset=lo,
+                    stream=torch.cuda.current_stream().cuda_stream)
+    if world > 1:
+        reduce_tally(tally, layout, group)
+    out = decode_tally(tally.cpu().numpy().view(np.uint64), layout)
+    if out.n_diverged:
+        raise SimDivergedError(out.first_diverged, f"race exceeded tick_limit in sim {out.first_diverged}")
+    return out

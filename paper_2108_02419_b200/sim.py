@@ -48,6 +48,7 @@ EXPORTED_SYMBOLS = (
     "bbe_device_info",
     "bbe_last_kernel_ms",
     "bbe_param_bytes",
+    "bbe_mt_getrandbits64",
 )
 
 
@@ -131,6 +132,8 @@ def lib():
         L.bbe_derive_seeds.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, _P(ctypes.c_uint64)]
         L.bbe_derive_seeds.restype = ctypes.c_int
         L.bbe_last_kernel_ms.restype = ctypes.c_float
+        L.bbe_mt_getrandbits64.argtypes = [_P(ctypes.c_uint32), ctypes.c_int64, _P(ctypes.c_uint64)]
+        L.bbe_mt_getrandbits64.restype = ctypes.c_int
         L.bbe_param_bytes.argtypes = [ctypes.c_int32]
         L.bbe_param_bytes.restype = ctypes.c_int64
         L.bbe_last_error.restype = ctypes.c_char_p

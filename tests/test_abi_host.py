@@ -53,11 +53,17 @@ def test_derive_seeds_matches_reference():
         assert int(out[0]) == int(d["seed"])
 
 
-def test_dry_run_seeds_match_sequential_getrandbits():
+@pytest.mark.parametrize("d,pre", [(1, 0), (257, 0), (312, 3), (5000, 1)])
+def test_dry_run_seeds_match_sequential_getrandbits(d, pre):
+    """bbe_mt_getrandbits64 advances a CPython Random exactly like d x getrandbits(64) (agents.py:164)."""
     a, b = random.Random(11), random.Random(11)
-    seeds = dry_run_seeds(a, 257)
-    assert [int(s) for s in seeds] == [b.getrandbits(64) for _ in range(257)]
-    assert a.random() == b.random()  # stream position identical afterwards
+    for _ in range(pre):
+        a.random(), b.random()
+    seeds = dry_run_seeds(a, d)
+    assert [int(s) for s in seeds] == [b.getrandbits(64) for _ in range(d)]
+    assert a.random() == b.random() and a.randrange(7) == b.randrange(7)  # same position afterwards
+    c = random.Random(11)
+    assert dry_run_seeds(c, d, want=False) is None and c.getstate() != random.Random(11).getstate()
 
 
 def test_validation_mirrors_reference_errors():

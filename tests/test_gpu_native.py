@@ -197,3 +197,14 @@ def test_records_consistent_with_tallies():
     assert int(res.blocked.sum()) == res.blocked_steps
     ticks_run = res.finish_ticks.max(axis=1) - st.tick
     assert (ticks_run > 0).all()
+
+
+def test_simulate_sharded_single_rank_matches_batch():
+    from paper_2108_02419_b200.parallel import simulate_sharded
+
+    g = c2()
+    cfg, st = config_from_dict(g["config"]), state_from_dict(g["state"])
+    t = simulate_sharded(st, cfg, 50_000, 3)
+    r = sim.simulate_batch(st, cfg, 50_000, 3)
+    assert (t.wins == r.wins).all() and (t.ranks == r.ranks).all()
+    assert t.competitor_steps == r.competitor_steps and t.first_diverged == -1
