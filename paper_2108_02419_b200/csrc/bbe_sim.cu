@@ -16,7 +16,7 @@
 #include <vector>
 
 #include "../../include/bbe_sim.h"
-#include "race_kernel.cuh"
+#include "exact_kernel.cuh"
 #include "native_kernel.cuh"
 
 using namespace bbe;
@@ -75,6 +75,8 @@ struct DevCtx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     HostBuf h_params, h_tally;
     DevBuf d_params, d_tally, d_draws, d_offsets, d_winner, d_order, d_fin, d_fpos, d_blocked, d_dused;
+    DevBuf d_seeds, d_mt_states, d_mt_scratch;  // MT mode
+    bool mt_table = false;                       // c_mt_init uploaded on this device
 };
 
 std::mutex g_ctx_mu;
@@ -140,7 +142,7 @@ int validate(const bbe_race* race, const bbe_competitor* comps, const bbe_state*
     if (rq->mode == BBE_MODE_INJECT) {
         if (!rq->draws || !rq->draw_offsets) return fail(BBE_EINVAL, "inject mode needs draws and draw_offsets");
     } else if (rq->mode == BBE_MODE_MT) {
-        return fail(BBE_EINVAL, "mode MT is not available in this build");
+        if (n > kWarp) return fail(BBE_EINVAL, "mode MT supports at most 32 competitors");
     } else if (rq->mode != BBE_MODE_NATIVE) {
         return fail(BBE_EINVAL, "unknown mode");
     }
@@ -277,12 +279,13 @@ KernelFn native_for_ch(int ch) {
 }
 
 KernelFn pick_kernel(int mode, int k, int ch) {
+    if (mode == BBE_MODE_MT) return k == 1 ? exact_kernel<1, MT> : nullptr;
     if (mode == BBE_MODE_INJECT) {
         switch (k) {
-            case 1: return race_kernel<double, 1, INJECT, 1>;
-            case 2: return race_kernel<double, 2, INJECT, 1>;
-            case 3: return race_kernel<double, 3, INJECT, 1>;
-            case 4: return race_kernel<double, 4, INJECT, 1>;
+            case 1: return exact_kernel<1, INJECT>;
+            case 2: return exact_kernel<2, INJECT>;
+            case 3: return exact_kernel<3, INJECT>;
+            case 4: return exact_kernel<4, INJECT>;
         }
     } else {
         switch (k) {
@@ -296,7 +299,7 @@ KernelFn pick_kernel(int mode, int k, int ch) {
 }
 
 struct Plan {
-    int n, K, W, S, CH, WP, nperm, tally_len;
+    int mode, n, K, W, S, CH, WP, nperm, tally_len;
     size_t smem;
     KernelFn fn;
     int grid;
@@ -304,17 +307,20 @@ struct Plan {
 
 int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_request* rq, int want_perms, Plan* pl) {
     const int n = race->n;
+    pl->mode = rq->mode;
     pl->n = n;
-    pl->K = choose_k(n, rq->lanes_per_slot_hint);
+    pl->K = rq->mode == BBE_MODE_MT ? 1 : choose_k(n, rq->lanes_per_slot_hint);
     if (pl->K < 0) return fail(BBE_EINVAL, "field too large for one warp");
     pl->W = (n + pl->K - 1) / pl->K;
+    if (rq->mode == BBE_MODE_MT) pl->W = std::max(pl->W, 8);  // <= 4 MT states (2.5 KB each) per warp
     pl->S = kWarp / pl->W;
     pl->CH = (pl->W + 3) / 4;
     pl->WP = 4 * pl->CH;
     pl->nperm = want_perms ? nperm_for(n) : 0;
     TallyLayout TL{n, pl->nperm};
     pl->tally_len = TL.len();
-    pl->smem = smem_bytes(rq->mode == BBE_MODE_NATIVE, (TL.hist_len() + 1) & ~1, pl->K, pl->S, pl->WP);
+    const int kmode = rq->mode == BBE_MODE_NATIVE ? NATIVE : (rq->mode == BBE_MODE_MT ? MT : INJECT);
+    pl->smem = smem_bytes(kmode, (TL.hist_len() + 1) & ~1, pl->K, pl->S, pl->WP);
     pl->fn = pick_kernel(rq->mode, pl->K, pl->CH);
     if (!pl->fn) return fail(BBE_EINVAL, "no kernel for this configuration");
     if (pl->smem > 48 * 1024) {
@@ -477,13 +483,72 @@ int bbe_derive_seeds(uint64_t master, int64_t first, int64_t count, uint64_t* ou
     return BBE_OK;
 }
 
-static int launch_go(const Plan& pl, LaunchArgs& a, const bbe_competitor* comps, cudaStream_t stream) {
+static int launch_one(const Plan& pl, const LaunchArgs& a, cudaStream_t stream) {
+    if (a.n_sims == 0) return BBE_OK;
+    // persistent grid: never more blocks than this launch's sims need
+    const int64_t sims_per_block = (int64_t)kWarpsPerBlock * pl.S;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pl.grid, (a.n_sims + sims_per_block - 1) / sims_per_block));
+    pl.fn<<<grid, kBlockThreads, pl.smem, stream>>>(a);
+    BBE_CK(cudaGetLastError());
+    return BBE_OK;
+}
+
+constexpr int64_t kMtChunk = 65536;  // sims seeded per MT chunk: 2 x 160 MB of state + scratch
+
+// init_genrand(19650218) (CPython _randommodule.c), the start of every init_by_array
+static void mt_init_table(uint32_t* t) {
+    t[0] = 19650218u;
+    for (int i = 1; i < kMtWords; ++i) t[i] = 1812433253u * (t[i - 1] ^ (t[i - 1] >> 30)) + (uint32_t)i;
+}
+
+static uint64_t h_run_of(uint64_t master) {  // splitmix64(splitmix64(master) ^ fnv1a("s:run"))
+    uint64_t h = 0xCBF29CE484222325ull;
+    for (char ch : std::string("s:run")) h = (h ^ (unsigned char)ch) * 0x100000001B3ull;
+    return splitmix64_dev(splitmix64_dev(master) ^ h);
+}
+
+// Launch the race kernel for the whole request (MT: chunked seeding + race per chunk).  `d_seeds`
+// (MT, device, per-sim) may be NULL -> derive_seed(seed_master, "run", global index).
+static int launch_all(DevCtx* ctx, const Plan& pl, LaunchArgs a, const bbe_competitor* comps, const uint64_t* d_seeds,
+                      uint64_t seed_master, cudaStream_t stream) {
     a.scan = 0;
     for (int c = 0; c < a.n; ++c)
         if (comps[c].theta > 0.0) a.scan = 1;
-    if (a.n_sims == 0) return BBE_OK;
-    pl.fn<<<pl.grid, kBlockThreads, pl.smem, stream>>>(a);
-    BBE_CK(cudaGetLastError());
+    if (pl.mode != BBE_MODE_MT) return launch_one(pl, a, stream);
+
+    if (!ctx->mt_table) {
+        uint32_t t[kMtWords];
+        mt_init_table(t);
+        BBE_CK(cudaMemcpyToSymbol(c_mt_init, t, sizeof(t)));
+        ctx->mt_table = true;
+    }
+    a.nv_magic = 4 * std::exp(-0.5) / std::sqrt(2.0);  // random.NV_MAGICCONST, host libm
+    const int64_t total = a.n_sims;
+    const int64_t chunk = std::min<int64_t>(total, kMtChunk);
+    const int64_t pad = (chunk + 31) & ~31;
+    BBE_CK(ctx->d_mt_states.ensure((size_t)pad * kMtWords * 4));
+    BBE_CK(ctx->d_mt_scratch.ensure((size_t)pad * kMtWords * 4));
+    const uint64_t h_run = h_run_of(seed_master);
+    const int64_t off0 = a.sim_offset;
+    const int n = a.n;
+    for (int64_t c0 = 0; c0 < total; c0 += chunk) {
+        const int64_t cn = std::min(chunk, total - c0);
+        mt_seed_kernel<<<(unsigned)((cn + 127) / 128), 128, 0, stream>>>(
+            d_seeds ? d_seeds + c0 : nullptr, h_run, off0 + c0, cn, pad, (uint32_t*)ctx->d_mt_scratch.p,
+            (uint32_t*)ctx->d_mt_states.p);
+        BBE_CK(cudaGetLastError());
+        LaunchArgs b = a;
+        b.n_sims = cn;
+        b.sim_offset = off0 + c0;
+        b.mt_states = (const uint32_t*)ctx->d_mt_states.p;
+        if (b.winner) b.winner += c0;
+        if (b.order) b.order += c0 * n;
+        if (b.finish_ticks) b.finish_ticks += c0 * n;
+        if (b.final_pos) b.final_pos += c0 * n;
+        if (b.blocked) b.blocked += c0;
+        int rc = launch_one(pl, b, stream);
+        if (rc) return rc;
+    }
     return BBE_OK;
 }
 
@@ -557,6 +622,12 @@ int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_st
         d_draws = (const double*)ctx->d_draws.p;
         d_offsets = (const int64_t*)ctx->d_offsets.p;
     }
+    const uint64_t* d_seeds = nullptr;
+    if (rq->mode == BBE_MODE_MT && rq->seeds && ns) {
+        BBE_CK(ctx->d_seeds.ensure((size_t)ns * sizeof(uint64_t)));
+        BBE_CK(cudaMemcpyAsync(ctx->d_seeds.p, rq->seeds, (size_t)ns * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+        d_seeds = (const uint64_t*)ctx->d_seeds.p;
+    }
 
     const size_t tbytes = (size_t)pl.tally_len * sizeof(uint64_t);
     BBE_CK(ctx->d_tally.ensure(tbytes));
@@ -579,7 +650,7 @@ int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_st
     build_args(pl, race, st, rq, (const double*)ctx->d_params.p, d_draws, d_offsets, (uint64_t*)ctx->d_tally.p, &dev,
                shift, &a);
     BBE_CK(cudaEventRecord(ctx->ev0, s));
-    if ((rc = launch_go(pl, a, comps, s))) return rc;
+    if ((rc = launch_all(ctx, pl, a, comps, d_seeds, rq->seed_master, s))) return rc;
     BBE_CK(cudaEventRecord(ctx->ev1, s));
 
     BBE_CK(cudaMemcpyAsync(ctx->h_tally.p, ctx->d_tally.p, tbytes, cudaMemcpyDeviceToHost, s));
@@ -639,7 +710,7 @@ int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const 
     build_args(pl, race, st, rq, (const double*)ctx->d_params.p, rq->draws, rq->draw_offsets, d_tally, dev_out, shift,
                &a);
     BBE_CK(cudaEventRecord(ctx->ev0, s));
-    if ((rc = launch_go(pl, a, comps, s))) return rc;
+    if ((rc = launch_all(ctx, pl, a, comps, rq->seeds, rq->seed_master, s))) return rc;
     BBE_CK(cudaEventRecord(ctx->ev1, s));
     return BBE_OK;
 }

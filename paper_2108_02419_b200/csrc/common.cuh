@@ -1,0 +1,114 @@
+// common.cuh -- shared definitions of the race kernels (parameter blocks, tally layout, launch
+// arguments, Philox4x32-10, warp helpers).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+namespace bbe {
+
+constexpr int kWarp = 32;
+constexpr int kBlockThreads = 128;
+constexpr int kWarpsPerBlock = kBlockThreads / kWarp;
+constexpr int kTicksPerBlock = 4;  // Philox4x32 yields 4 words per call: one per tick
+
+// Parameter block fields (SoA, stride n), host-packed in double (see bbe_sim.cu: pack_params).
+enum Field {
+    F_LO = 0, F_SPAN, F_LMU, F_SIGMA, F_SCALE, F_MU, F_RP_EARLY, F_RP_LATE, F_EARLY, F_LATE, F_BP,
+    F_THETA, F_POS0, F_PREV0, F_FIN0, F_FAMILY,
+    F_FINREL,  // finish tick relative to the state's tick, order-compressed to int32 (racing: unused)
+    F_COUNT
+};
+
+// NATIVE-only FP32 parameter block (SoA, stride n), derived on the host from the double block.
+enum FieldF {
+    NF_LO_MINUS_SPAN = 0,  // uniform: lo + span*u == (lo - span) + span*(1 + u), u from the exponent trick
+    NF_SPAN, NF_SG2, NF_LMU2,  // lognormal: exp2(sg2 * z + lmu2) == scale * exp(mu + sigma z)
+    NF_RP_EARLY, NF_RP_LATE, NF_EARLY, NF_LATE, NF_BP, NF_THETA, NF_POS0, NF_PREV0, NF_COUNT
+};
+
+enum Mode { NATIVE = 0, INJECT = 1, MT = 2 };
+
+// "First failing sim" tally fields hold (2^63 - 1) - index (0 = none): a MAX reduction -- atomicMax
+// in a kernel, or a signed int64 all-reduce across ranks -- then keeps the smallest index.
+__host__ __device__ inline unsigned long long encode_first(int64_t index) {
+    return 0x7fffffffffffffffull - (unsigned long long)index;
+}
+__host__ __device__ inline int64_t decode_first(unsigned long long v) {
+    return v ? (int64_t)(0x7fffffffffffffffull - v) : -1;
+}
+
+// Tally layout in u64 (see bbe_tally_offset in bbe_sim.h).
+struct TallyLayout {
+    int n, nperm;
+    __host__ __device__ int wins() const { return 0; }
+    __host__ __device__ int ranks() const { return n; }
+    __host__ __device__ int perms() const { return n + n * n; }
+    __host__ __device__ int ct() const { return n + n * n + nperm; }
+    __host__ __device__ int blocked() const { return ct() + 1; }
+    __host__ __device__ int n_div() const { return ct() + 2; }
+    __host__ __device__ int n_bad() const { return ct() + 3; }
+    __host__ __device__ int first_div() const { return ct() + 4; }
+    __host__ __device__ int first_bad() const { return ct() + 5; }
+    __host__ __device__ int len() const { return ct() + 6; }
+    __host__ __device__ int hist_len() const { return n + n * n + nperm; }  // shared-memory histograms
+};
+
+struct LaunchArgs {
+    const double* P;  // [F_COUNT][n] parameter block
+    const float* Pf;  // [NF_COUNT][n] (NATIVE)
+    uint32_t rk[20];  // Philox4x32-10 round keys of the seed (NATIVE)
+    float shift;      // NATIVE: positions, L and breakpoints are offset by this to keep positions >= 0
+    int n, W, S, WP, from_start, scan, perms;
+    double L;
+    int64_t tick0;
+    int32_t limit;  // tick_limit clamped to int32 (ticks run per sim)
+    int64_t n_sims, sim_offset;
+    uint64_t seed;
+    const double* draws;          // INJECT
+    const int64_t* draw_offsets;  // INJECT [n_sims+1]
+    const uint32_t* mt_states;    // MT: [n_sims][624] seeded MT19937 states
+    double nv_magic;              // MT: random.NV_MAGICCONST = 4*exp(-0.5)/sqrt(2.0), host libm
+    uint64_t* tally;              // device, TallyLayout
+    int32_t* winner;              // optional per-sim outputs
+    int32_t* order;
+    int64_t* finish_ticks;
+    double* final_pos;
+    int64_t* blocked;
+    int64_t* draws_used;
+};
+
+// ---- dynamic shared memory ----
+// NATIVE key rows use a compile-time slot stride: the largest S*WP any W in (4(CH-1), 4CH] needs,
+// +4 for a padding word group at the end of every slot row (where lanes without a segment write).
+__host__ __device__ constexpr int swp_max(int CH) {
+    return CH == 1 ? 128 : (CH == 2 ? 48 : (CH == 3 ? 36 : (CH == 4 ? 32 : 4 * CH)));
+}
+__host__ __device__ constexpr int native_slot_words(int CH) { return swp_max(CH) + 4; }
+__host__ __device__ constexpr int native_warp_words(int K, int CH) { return 2 * K * native_slot_words(CH); }
+constexpr int kMtWords = 624;
+__host__ __device__ inline size_t smem_bytes(int mode, int hist_len_even, int K, int S, int WP) {
+    size_t b = (size_t)hist_len_even * 8;
+    if (mode == NATIVE) b += (size_t)kWarpsPerBlock * native_warp_words(K, (WP + 3) / 4) * 4;
+    if (mode == MT) b += (size_t)kWarpsPerBlock * S * kMtWords * 4;
+    return b;
+}
+
+// ---- Philox4x32-10 (Salmon et al., SC'11), in registers ----
+struct U4 { uint32_t x, y, z, w; };
+
+__device__ __forceinline__ U4 philox_rk(U4 c, const uint32_t* rk) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = U4{hi1 ^ c.y ^ rk[2 * r], lo1, hi0 ^ c.w ^ rk[2 * r + 1], lo0};
+    }
+    return c;
+}
+
+template <typename T>
+__device__ __forceinline__ T shfl(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+
+}  // namespace bbe

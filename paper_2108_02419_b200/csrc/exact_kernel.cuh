@@ -1,0 +1,463 @@
+// exact_kernel.cuh -- the bit-exact FP64 race kernel: BBE_MODE_INJECT and BBE_MODE_MT.
+//
+// Reference semantics (all /root/reference/pkg/src/racemarket/race.py):
+//   :93-96   responsiveness: early_mult if pos < breakpoint*L else late_mult
+//   :233-241 initial_state: positions 0, prev[c] = resp(0)*pref*draw (index order)   [from_start]
+//   :244-264 _front_runner: nearest STILL-RACING rival STRICTLY ahead; equal gaps -> lowest index
+//   :267-274 _resolve_step: free (no front, or gap > theta): (resp*pref)*draw, consumes a draw;
+//            blocked: resp*min(prev_c, prev_front), consumes nothing
+//   :287-320 advance_race: synchronous; p = pos+step; p==pos -> nextafter(p,+inf); prev = step;
+//            finish tick = t if p >= L
+//   :323-332 _finish_order: sort by (finish_tick, L - pos, index)
+//   :381-386 / :402-404 tick-limit check before each advance (absolute / relative)
+// Every operation is the reference's own IEEE double operation in the reference's order (explicit
+// __dadd_rn/__dmul_rn/__dsub_rn/__ddiv_rn: no FMA contraction), so given the same draws the kernel
+// reproduces positions, finish ticks, order and blocked counts bit for bit.
+//
+// Mapping: one sim per SEGMENT of W consecutive lanes, competitor c = k*W + l in lane l, slot k;
+// S = 32/W sims per warp; persistent grid, a finished segment takes its next sim at a 4-tick block
+// boundary.  Rival positions are read with __shfl_sync; the front-runner scan is the reference's
+// gap arithmetic with strict compares in index order (lowest-index tie rule).
+//
+// Draw sources:
+//   INJECT  recorded reference draws (CSR per sim); a free slot's offset in the tick = popc of free
+//           slots of lower competitor index in its segment -- the reference's consumption order.
+//   MT      per-sim CPython MT19937 (mt_stream.cuh) in shared memory: uniform draws of a run of free
+//           competitors are taken in parallel (2 words each, offsets by popc); a lognormal competitor
+//           runs the Kinderman-Monahan loop of random.normalvariate alone, in index order.
+#pragma once
+
+#include "common.cuh"
+#include "mt_stream.cuh"
+
+namespace bbe {
+
+template <int K, int MODE>
+__global__ void __launch_bounds__(kBlockThreads)
+exact_kernel(const LaunchArgs a) {
+    static_assert(MODE == INJECT || MODE == MT, "exact kernel modes");
+    static_assert(MODE != MT || K == 1, "MT mode maps one competitor per lane");
+    extern __shared__ __align__(16) unsigned long long s_dyn[];
+    const TallyLayout TL{a.n, a.perms};
+    const int hist_len = TL.hist_len();
+    unsigned long long* s_hist = s_dyn;
+    for (int i = threadIdx.x; i < hist_len; i += blockDim.x) s_hist[i] = 0ull;
+
+    const int n = a.n, W = a.W, S = a.S;
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int warp = threadIdx.x >> 5;
+    const int seg = lane / W;
+    const bool lane_on = seg < S;
+    const int base = lane_on ? seg * W : 0;
+    const int l = lane - seg * W;
+    const unsigned segmask = lane_on ? ((W == 32 ? 0xffffffffu : ((1u << W) - 1u)) << base) : 0u;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    uint32_t* const mt = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) +
+                         (warp * S + (lane_on ? seg : 0)) * kMtWords;  // MT: this segment's state
+    __syncthreads();
+
+    // ---- per-slot constants (the lane->competitor map is fixed for the kernel) ----
+    int cidx[K];
+    bool has[K], lognorm[K];
+    double lo[K], span[K], mu[K], sigma[K], scale[K], rpE[K], rpL[K], eE[K], eL[K], bp[K], th[K];
+    double pos0[K], prev0[K];
+    int64_t fin0[K];
+    const double* P = a.P;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int c = k * W + l;
+        cidx[k] = c;
+        has[k] = lane_on && c < n;
+        const int cc = has[k] ? c : 0;
+        lo[k] = P[F_LO * n + cc];
+        span[k] = P[F_SPAN * n + cc];
+        mu[k] = P[F_MU * n + cc];
+        sigma[k] = P[F_SIGMA * n + cc];
+        scale[k] = P[F_SCALE * n + cc];
+        rpE[k] = P[F_RP_EARLY * n + cc];
+        rpL[k] = P[F_RP_LATE * n + cc];
+        eE[k] = P[F_EARLY * n + cc];
+        eL[k] = P[F_LATE * n + cc];
+        bp[k] = P[F_BP * n + cc];
+        th[k] = P[F_THETA * n + cc];
+        pos0[k] = P[F_POS0 * n + cc];
+        prev0[k] = P[F_PREV0 * n + cc];
+        fin0[k] = has[k] ? (int64_t)P[F_FIN0 * n + cc] : INT64_MAX;
+        lognorm[k] = has[k] && P[F_FAMILY * n + cc] != 0.0;
+    }
+    const double L = a.L;
+    const double NEG_INF = -CUDART_INF;
+
+    // ---- segment bookkeeping (replicated in every lane of the segment) ----
+    const int64_t segs_total = (int64_t)gridDim.x * kWarpsPerBlock * S;
+    int64_t s = lane_on ? ((int64_t)blockIdx.x * kWarpsPerBlock + warp) * S + seg : a.n_sims;
+    const int64_t start = a.tick0;
+    int32_t rt = 0;
+    int64_t cursor = 0, cursor_end = 0;  // INJECT
+    int q = kMtWords;                    // MT: CPython's position in the current 624-word block
+    bool running = false, diverged = false, bad = false;
+
+    double pos[K], prev[K], pv[K];
+    int64_t fin[K];
+    bool racing[K];
+    uint32_t ct_sim = 0, blk_sim = 0;
+    unsigned long long ct_tot = 0, blk_tot = 0, n_div = 0, n_bad = 0;
+    int64_t first_div = INT64_MAX, first_bad = INT64_MAX;
+
+    // ---- MT19937 stream helpers (warp-uniform calls) ----
+    // Regenerate this segment's block in place (MT19937 twist), W lanes per chunk; segments that do
+    // not need it idle through the loop.  W <= 32 < 227 keeps every "new" dependency in an earlier chunk.
+    auto mt_twist = [&](bool need) {
+        __syncwarp();
+        for (int c0 = 0; c0 < kMtWords; c0 += W) {
+            const int i = c0 + l;
+            const bool act = need && i < kMtWords;
+            uint32_t x = 0, y = 0, m = 0;
+            if (act) {
+                x = mt[i];
+                y = mt[i + 1 < kMtWords ? i + 1 : 0];
+                m = mt[i < kMtWords - kMtM ? i + kMtM : i + kMtM - kMtWords];
+            }
+            __syncwarp();
+            if (act) mt[i] = mt_mix(x, y, m);
+            __syncwarp();
+        }
+    };
+    // Take words [q+off, q+off+cnt) of this segment's stream (segment total T), twisting when the
+    // segment's reads cross the end of the block exactly where CPython's genrand_uint32 would.
+    auto mt_fetch = [&](int off, int cnt, int T, uint32_t* w) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int idx = q + off + t;
+            if (t < cnt && idx < kMtWords) w[t] = mt_temper(mt[idx]);
+        }
+        const bool need = lane_on && T > 0 && q + T > kMtWords;
+        if (__any_sync(0xffffffffu, need)) mt_twist(need);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int idx = q + off + t;
+            if (t < cnt && idx >= kMtWords) w[t] = mt_temper(mt[idx - kMtWords]);
+        }
+        if (lane_on && T > 0) q = (q + T > kMtWords) ? q + T - kMtWords : q + T;
+    };
+    // One step draw per lane with `want`, in competitor-index order within each segment:
+    // uniform(lo, hi) = lo + (hi - lo) * random(); scale * lognormvariate(mu, sigma) via the
+    // Kinderman-Monahan loop of random.normalvariate (Lib/random.py).  Warp-uniform call.
+    auto mt_draws = [&](bool want) -> double {
+        double d = 1.0;
+        bool pend = want;
+        while (__any_sync(0xffffffffu, pend)) {
+            const unsigned Pm = __ballot_sync(0xffffffffu, pend) & segmask;
+            const unsigned Lg = __ballot_sync(0xffffffffu, pend && lognorm[0]) & segmask;
+            const unsigned stop = Lg & (0u - Lg);  // first pending lognormal competitor
+            const unsigned run = stop ? (Pm & (stop - 1u)) : Pm;
+            const bool in_run = (run >> lane) & 1u;
+            {
+                uint32_t w[4];
+                mt_fetch(2 * __popc(run & lt_mask), in_run ? 2 : 0, 2 * __popc(run), w);
+                if (in_run) {
+                    d = __dadd_rn(lo[0], __dmul_rn(span[0], mt_random53(w[0], w[1])));
+                    pend = false;
+                }
+            }
+            const bool is_stop = (stop >> lane) & 1u;
+            bool trying = stop != 0u;
+            while (__any_sync(0xffffffffu, trying)) {
+                uint32_t w[4];
+                mt_fetch(0, (is_stop && trying) ? 4 : 0, trying ? 4 : 0, w);
+                bool acc = false;
+                if (is_stop && trying) {
+                    const double u1 = mt_random53(w[0], w[1]);
+                    const double u2 = __dsub_rn(1.0, mt_random53(w[2], w[3]));
+                    const double z = __ddiv_rn(__dmul_rn(a.nv_magic, __dsub_rn(u1, 0.5)), u2);
+                    const double zz = __ddiv_rn(__dmul_rn(z, z), 4.0);
+                    acc = zz <= -log(u2);
+                    if (acc) {
+                        d = __dmul_rn(scale[0], exp(__dadd_rn(mu[0], __dmul_rn(z, sigma[0]))));
+                        pend = false;
+                    }
+                }
+                if (__ballot_sync(0xffffffffu, acc) & segmask) trying = false;
+            }
+        }
+        return d;
+    };
+
+    // refill the segment with its next sim; warp-uniform (every lane calls it)
+    auto load_sim = [&](bool do_it) {
+        if (do_it) {
+            running = lane_on && s < a.n_sims;
+            diverged = false;
+            bad = false;
+            rt = 0;
+            ct_sim = blk_sim = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                pos[k] = pos0[k];
+                prev[k] = prev0[k];
+                fin[k] = fin0[k];
+                racing[k] = running && has[k] && fin0[k] < 0;
+            }
+            if (MODE == INJECT && running) {
+                cursor = a.draw_offsets[s];
+                cursor_end = a.draw_offsets[s + 1];
+            }
+            if (MODE == MT && running) {
+                for (int i = l; i < kMtWords; i += W) mt[i] = a.mt_states[s * kMtWords + i];
+                q = kMtWords;  // random.Random(seed): the first draw twists
+            }
+        }
+        if (MODE == MT) __syncwarp();
+        if (a.from_start) {
+            // race.py:233-241: one free draw per competitor, in index order, resp at position 0
+            double d[K];
+            if constexpr (MODE == MT) {
+                d[0] = mt_draws(do_it && running && has[0]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const int64_t at = cursor + cidx[k];
+                    d[k] = at < cursor_end ? a.draws[at] : 1.0;
+                }
+            }
+            if (do_it && running) {
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    if (has[k]) prev[k] = __dmul_rn((0.0 < bp[k]) ? rpE[k] : rpL[k], d[k]);
+                if (MODE == INJECT) {
+                    if (cursor + n > cursor_end) bad = true;  // stream shorter than the priming draws
+                    cursor += n;
+                }
+            }
+        }
+        if (do_it) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) pv[k] = racing[k] ? pos[k] : NEG_INF;
+        }
+    };
+
+    load_sim(true);
+
+    while (true) {
+        // ---------------- block boundary: finalize finished segments, refill, exit test ----------
+        bool seg_live = false;
+#pragma unroll
+        for (int k = 0; k < K; ++k) seg_live |= racing[k];
+        const unsigned live_mask = __ballot_sync(0xffffffffu, seg_live);
+        const bool seg_done = running && ((live_mask & segmask) == 0u);
+        if (__any_sync(0xffffffffu, seg_done)) {
+            double lp[K];
+            int rank[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) { lp[k] = __dsub_rn(L, pos[k]); rank[k] = 0; }
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) {
+                for (int j = 0; j < W; ++j) {
+                    const int64_t fr = shfl(fin[kk], base + j);
+                    const double dr = shfl(lp[kk], base + j);
+                    const int i = kk * W + j;
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const bool less = fr < fin[k] || (fr == fin[k] && (dr < lp[k] || (dr == lp[k] && i < cidx[k])));
+                        rank[k] += (i < n && less) ? 1 : 0;
+                    }
+                }
+            }
+            uint32_t seg_blk = 0;
+            for (int j = 0; j < W; ++j) seg_blk += shfl(blk_sim, base + j);
+            int64_t lehmer = 0;
+            if (a.perms) {
+                // Lehmer index of the finish order: sum_c #{c' < c : rank(c') > rank(c)} * (n-1-rank(c))!
+                int cnt[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) cnt[k] = 0;
+#pragma unroll
+                for (int kk = 0; kk < K; ++kk)
+                    for (int j = 0; j < W; ++j) {
+                        const int rr = shfl(rank[kk], base + j);
+                        const int i = kk * W + j;
+#pragma unroll
+                        for (int k = 0; k < K; ++k) cnt[k] += (i < n && i < cidx[k] && rr > rank[k]) ? 1 : 0;
+                    }
+                int64_t term = 0;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    if (!has[k]) continue;
+                    int64_t f = 1;
+                    for (int qq = 2; qq <= n - 1 - rank[k]; ++qq) f *= qq;
+                    term += cnt[k] * f;
+                }
+                for (int j = 0; j < W; ++j) lehmer += shfl(term, base + j);
+            }
+            if (seg_done) {
+                const int64_t gs = a.sim_offset + s;
+                if (MODE == INJECT) bad = bad || cursor != cursor_end;
+                if (diverged) {
+                    if (l == 0) { n_div++; first_div = min(first_div, gs); }
+                } else if (bad) {
+                    if (l == 0) { n_bad++; first_bad = min(first_bad, gs); }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        if (!has[k]) continue;
+                        if (rank[k] == 0) atomicAdd(&s_hist[TL.wins() + cidx[k]], 1ull);
+                        atomicAdd(&s_hist[TL.ranks() + cidx[k] * n + rank[k]], 1ull);
+                    }
+                    if (a.perms && l == 0) atomicAdd(&s_hist[TL.perms() + lehmer], 1ull);
+                }
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    if (!has[k]) continue;
+                    const int64_t o = s * n + cidx[k];
+                    if (a.winner && rank[k] == 0) a.winner[s] = diverged ? -1 : cidx[k];
+                    if (a.order) a.order[s * n + rank[k]] = cidx[k];
+                    if (a.finish_ticks) a.finish_ticks[o] = fin[k] == INT64_MAX ? -1 : fin[k];
+                    if (a.final_pos) a.final_pos[o] = pos[k];
+                }
+                if (l == 0) {
+                    if (a.blocked) a.blocked[s] = seg_blk;
+                    if (MODE == INJECT && a.draws_used) a.draws_used[s] = cursor - a.draw_offsets[s];
+                }
+                ct_tot += ct_sim;
+                blk_tot += blk_sim;
+                s += segs_total;
+            }
+            load_sim(seg_done);
+        }
+        if (!__any_sync(0xffffffffu, running)) break;
+
+        // ---------------- 4 synchronous ticks -------------------------------------------------------
+        for (int tj = 0; tj < kTicksPerBlock; ++tj) {
+            bool any_racing = false;
+#pragma unroll
+            for (int k = 0; k < K; ++k) any_racing |= racing[k];
+            const unsigned rmask = __ballot_sync(0xffffffffu, any_racing);
+            const bool seg_running = (rmask & segmask) != 0u;
+            if (rmask == 0u) break;  // every segment finished inside this block
+
+            // tick-limit check before the advance (race.py:381-386, 402-404)
+            if (seg_running && rt >= a.limit) {
+                diverged = true;
+#pragma unroll
+                for (int k = 0; k < K; ++k) { racing[k] = false; pv[k] = NEG_INF; }
+            }
+
+            // ---- front runner (race.py:244-264): gap = p_i - p_c, strict compares in index order ----
+            double gap[K];
+            int bi[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) { gap[k] = CUDART_INF; bi[k] = 0; }
+            if (a.scan) {
+#pragma unroll
+                for (int kk = 0; kk < K; ++kk) {
+#pragma unroll 2
+                    for (int j = 0; j < W; ++j) {
+                        const double pr = shfl(pv[kk], base + j);
+#pragma unroll
+                        for (int k = 0; k < K; ++k) {
+                            const double g = __dsub_rn(pr, pos[k]);
+                            const bool t = (g > 0.0) & (g < gap[k]);
+                            gap[k] = t ? g : gap[k];
+                            bi[k] = t ? (kk << 5) | j : bi[k];
+                        }
+                    }
+                }
+            }
+
+            // ---- step resolution (race.py:267-274) ----
+            bool fr[K], bl[K];
+            bool any_blocked = false;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                fr[k] = racing[k] && gap[k] > th[k];
+                bl[k] = racing[k] && !fr[k];
+                any_blocked |= bl[k];
+            }
+            double pf[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) pf[k] = 0.0;
+            if (__any_sync(0xffffffffu, any_blocked)) {
+#pragma unroll
+                for (int kk = 0; kk < K; ++kk) {
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const double v = shfl(prev[kk], base + (bi[k] & 31));
+                        pf[k] = ((bi[k] >> 5) == kk) ? v : pf[k];
+                    }
+                }
+            }
+            double draw[K];
+            if constexpr (MODE == INJECT) {
+                // free slots consume the stream in competitor-index order (slot-major, then lane)
+                int seg_total = 0;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const unsigned fm = __ballot_sync(0xffffffffu, fr[k]) & segmask;
+                    const int64_t at = cursor + seg_total + __popc(fm & lt_mask);
+                    draw[k] = (fr[k] && at < cursor_end) ? __ldg(a.draws + at) : 1.0;
+                    seg_total += __popc(fm);
+                }
+                cursor += seg_total;
+                if (cursor > cursor_end) {  // stream too short: stop this sim, report at finalize
+                    bad = true;
+#pragma unroll
+                    for (int k = 0; k < K; ++k) { racing[k] = false; fr[k] = bl[k] = false; }
+                }
+            } else {
+                draw[0] = mt_draws(fr[0]);
+            }
+
+            // ---- synchronous update (race.py:299-320) ----
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const bool early = pos[k] < bp[k];
+                double step;
+                if (fr[k]) {
+                    step = __dmul_rn(early ? rpE[k] : rpL[k], draw[k]);
+                } else {
+                    const double m = (pf[k] < prev[k]) ? pf[k] : prev[k];  // Python min(prev_c, prev_front)
+                    step = __dmul_rn(early ? eE[k] : eL[k], m);
+                }
+                if (racing[k]) {
+                    double p = __dadd_rn(pos[k], step);
+                    if (p == pos[k]) p = nextafter(p, CUDART_INF);
+                    pos[k] = p;
+                    prev[k] = step;
+                    ct_sim += 1;
+                    blk_sim += bl[k] ? 1 : 0;
+                    if (p >= L) { fin[k] = start + rt + 1; racing[k] = false; }
+                }
+                pv[k] = racing[k] ? pos[k] : NEG_INF;
+            }
+            if (seg_running && !diverged) rt += 1;
+        }
+    }
+
+    // ---------------- flush: per-lane totals -> warp -> global; block histograms -> global ------
+    unsigned long long v_ct = ct_tot, v_blk = blk_tot, v_div = n_div, v_bad = n_bad;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        v_ct += __shfl_xor_sync(0xffffffffu, v_ct, off);
+        v_blk += __shfl_xor_sync(0xffffffffu, v_blk, off);
+        v_div += __shfl_xor_sync(0xffffffffu, v_div, off);
+        v_bad += __shfl_xor_sync(0xffffffffu, v_bad, off);
+        first_div = min(first_div, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)first_div, off));
+        first_bad = min(first_bad, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)first_bad, off));
+    }
+    const int ct_at = TL.ct();
+    if (lane == 0) {
+        if (v_ct) atomicAdd((unsigned long long*)&a.tally[ct_at + 0], v_ct);
+        if (v_blk) atomicAdd((unsigned long long*)&a.tally[ct_at + 1], v_blk);
+        if (v_div) atomicAdd((unsigned long long*)&a.tally[ct_at + 2], v_div);
+        if (v_bad) atomicAdd((unsigned long long*)&a.tally[ct_at + 3], v_bad);
+        if (first_div != INT64_MAX) atomicMax((unsigned long long*)&a.tally[ct_at + 4], encode_first(first_div));
+        if (first_bad != INT64_MAX) atomicMax((unsigned long long*)&a.tally[ct_at + 5], encode_first(first_bad));
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < hist_len; i += blockDim.x) {
+        const unsigned long long v = s_hist[i];
+        if (v) atomicAdd((unsigned long long*)&a.tally[i], v);
+    }
+}
+
+}  // namespace bbe

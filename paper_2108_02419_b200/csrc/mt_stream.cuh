@@ -1,0 +1,114 @@
+// mt_stream.cuh -- CPython's random.Random (MT19937) on the GPU, for BBE_MODE_MT.
+//
+// The reference seeds every dry run with make_rng(seed) = random.Random(seed & (2^64-1))
+// (seeding.py:62-64, agents.py:164, batch.py:117-119) and draws steps with uniform() and
+// lognormvariate() (race.py:46-47, 68-69).  Reproducing that stream per simulation makes the GPU
+// result identical to the reference's for the same seeds.  Algorithms restated from CPython 3.12
+// Modules/_randommodule.c (init_genrand, init_by_array, genrand_uint32, random_random) and
+// Lib/random.py (uniform, normalvariate, lognormvariate).
+//
+// Layout: (1) mt_seed_kernel, one thread per sim, runs init_by_array's two serial passes
+// (pass-1 words spill to a word-major scratch so every store and load is coalesced) and writes the
+// seeded 624-word state sim-major through a 32x32 shared-memory transpose; (2) the race kernel keeps
+// each segment's state in shared memory and regenerates it in place, W lanes per 624-word twist.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bbe {
+
+constexpr int kMtN = 624;
+constexpr int kMtM = 397;
+
+// init_genrand(19650218): the table every init_by_array starts from (host-computed).
+__constant__ uint32_t c_mt_init[kMtN];
+
+__host__ __device__ inline uint64_t splitmix64_dev(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+// derive_seed(master, "run", i) (seeding.py:50-59); h_run = splitmix64(splitmix64(master) ^ fnv("s:run"))
+__device__ __forceinline__ uint64_t derive_seed_run_dev(uint64_t h_run, uint64_t i) {
+    uint64_t h = 0xCBF29CE484222325ull;
+    h = (h ^ (uint64_t)'i') * 0x100000001B3ull;
+    h = (h ^ (uint64_t)':') * 0x100000001B3ull;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) h = (h ^ ((i >> (56 - 8 * k)) & 0xffu)) * 0x100000001B3ull;
+    return splitmix64_dev(h_run ^ h);
+}
+
+__device__ __forceinline__ uint32_t mt_temper(uint32_t y) {
+    y ^= y >> 11;
+    y ^= (y << 7) & 0x9d2c5680u;
+    y ^= (y << 15) & 0xefc60000u;
+    return y ^ (y >> 18);
+}
+
+__device__ __forceinline__ uint32_t mt_mix(uint32_t a, uint32_t b, uint32_t m) {
+    const uint32_t y = (a & 0x80000000u) | (b & 0x7fffffffu);
+    return m ^ (y >> 1) ^ ((0u - (y & 1u)) & 0x9908b0dfu);
+}
+
+// random_random(): (a*2^26 + b) * 2^-53 with a = w0>>5, b = w1>>6 -- an exact 53-bit fraction.
+__device__ __forceinline__ double mt_random53(uint32_t w0, uint32_t w1) {
+    const uint64_t u = ((uint64_t)(w0 >> 5) << 26) | (uint64_t)(w1 >> 6);
+    return __dmul_rn((double)u, 1.0 / 9007199254740992.0);
+}
+
+// One thread per sim: random.Random(seed) for a u64 seed = init_by_array(key = 32-bit LE words of
+// the seed, one word when seed < 2^32).  states: [n][624] u32; scratch: [624][n_pad] u32.
+__global__ void __launch_bounds__(128) mt_seed_kernel(const uint64_t* seeds, uint64_t h_run, int64_t sim_offset,
+                                                      int64_t n, int64_t n_pad, uint32_t* scratch, uint32_t* states) {
+    __shared__ uint32_t tile[4][32][33];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t warp_base = s - lane;
+    const bool on = s < n;
+    const uint64_t seed = on ? (seeds ? seeds[s] : derive_seed_run_dev(h_run, (uint64_t)(sim_offset + s))) : 0ull;
+    const uint32_t key0 = (uint32_t)seed, key1 = (uint32_t)(seed >> 32);
+    const int keylen = key1 ? 2 : 1;
+
+    // pass 1 (k = 624 iterations): i = 1..623, then wrap (mt[0] = mt[623]) and i = 1 once more
+    uint32_t prev = c_mt_init[0];
+    int j = 0;
+    for (int i = 1; i < kMtN; ++i) {
+        const uint32_t v = (c_mt_init[i] ^ ((prev ^ (prev >> 30)) * 1664525u)) + (j ? key1 : key0) + (uint32_t)j;
+        if (on) scratch[(int64_t)i * n_pad + s] = v;
+        prev = v;
+        if (++j >= keylen) j = 0;
+    }
+    const uint32_t m0 = prev;
+    const uint32_t p1 = on ? scratch[n_pad + s] : 0u;
+    const uint32_t m1 = (p1 ^ ((m0 ^ (m0 >> 30)) * 1664525u)) + (j ? key1 : key0) + (uint32_t)j;
+
+    // pass 2 (k = 623 iterations): i = 2..623, then wrap and i = 1; mt[0] = 0x80000000 at the end.
+    // Words 2..623 stream out through the transpose tile, 32 at a time.
+    prev = m1;
+    for (int i = 2; i < kMtN; ++i) {
+        const uint32_t p = on ? scratch[(int64_t)i * n_pad + s] : 0u;
+        const uint32_t v = (p ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)i;
+        prev = v;
+        tile[warp][i & 31][lane] = v;
+        if ((i & 31) == 31 || i == kMtN - 1) {
+            __syncwarp();
+            const int blk0 = i & ~31;
+            const int w = blk0 + lane;  // this lane writes word w of each of the warp's 32 sims
+            for (int r = 0; r < 32; ++r) {
+                const int64_t sr = warp_base + r;
+                if (sr < n && w >= 2 && w <= i) states[sr * kMtN + w] = tile[warp][lane][r];
+            }
+            __syncwarp();
+        }
+    }
+    const uint32_t f1 = (m1 ^ ((prev ^ (prev >> 30)) * 1566083941u)) - 1u;
+    if (on) {
+        states[s * kMtN + 0] = 0x80000000u;
+        states[s * kMtN + 1] = f1;
+    }
+}
+
+}  // namespace bbe

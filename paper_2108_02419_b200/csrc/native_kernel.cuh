@@ -21,7 +21,7 @@
 // marks racing lanes diverged; competitor-timesteps are summed from finish ticks at finalize.
 #pragma once
 
-#include "race_kernel.cuh"
+#include "common.cuh"
 
 namespace bbe {
 
@@ -46,16 +46,6 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 }
 // 1 + u, u in [0,1) with 23 random bits (exponent trick).
 __device__ __forceinline__ float one_plus_u(uint32_t w) { return __uint_as_float(0x3f800000u | (w >> 9)); }
-
-__device__ __forceinline__ U4 philox_rk(U4 c, const uint32_t* rk) {
-#pragma unroll
-    for (int r = 0; r < 10; ++r) {
-        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
-        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
-        c = U4{hi1 ^ c.y ^ rk[2 * r], lo1, hi0 ^ c.w ^ rk[2 * r + 1], lo0};
-    }
-    return c;
-}
 
 // Box-Muller pair -> two lognormal steps exp2(sg2*z + lmu2); uniform (a, b) -> (0,1] x [0,1).
 __device__ __forceinline__ void lognormal_pair(uint32_t wa, uint32_t wb, float sg2, float lmu2, float& d0, float& d1) {
