@@ -10,7 +10,7 @@ all: $(LIB) oracle
 
 $(LIB): $(SRC)
 	@mkdir -p $(dir $@)
-	$(NVCC) $(NVFLAGS) -o $@ paper_2108_02419_b200/csrc/bbe_sim.cu 2> paper_2108_02419_b200/_lib/ptxas.log || (cat paper_2108_02419_b200/_lib/ptxas.log; exit 1)
+	$(NVCC) $(NVFLAGS) -o $@ paper_2108_02419_b200/csrc/bbe_sim.cu -ldl 2> paper_2108_02419_b200/_lib/ptxas.log || (cat paper_2108_02419_b200/_lib/ptxas.log; exit 1)
 
 oracle:
 	$(MAKE) -s -C oracle

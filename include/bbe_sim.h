@@ -146,6 +146,11 @@ int bbe_derive_seeds(uint64_t master, int64_t first, int64_t count, uint64_t* ou
  * and, when `out` is not NULL, stores the values drawn (low word first, as CPython builds them). */
 int bbe_mt_getrandbits64(uint32_t* state625, int64_t count, uint64_t* out);
 
+/* 1 if MT mode reproduces the host libm's exp() (used by random.lognormvariate) bit for bit: the
+ * library found glibc's exp table in the loaded libm and verified its evaluation against exp().
+ * 0 -> lognormal steps in MT mode may differ from the reference in the last bit. */
+int bbe_mt_exp_exact(void);
+
 /* Bytes of the race-parameter block copied host->device per call (the per-call H2D input). */
 int64_t bbe_param_bytes(int32_t n);
 

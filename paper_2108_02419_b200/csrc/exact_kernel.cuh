@@ -173,7 +173,7 @@ exact_kernel(const LaunchArgs a) {
                     const double zz = __ddiv_rn(__dmul_rn(z, z), 4.0);
                     acc = zz <= -log(u2);
                     if (acc) {
-                        d = __dmul_rn(scale[0], exp(__dadd_rn(mu[0], __dmul_rn(z, sigma[0]))));
+                        d = __dmul_rn(scale[0], libm_exp(__dadd_rn(mu[0], __dmul_rn(z, sigma[0]))));
                         pend = false;
                     }
                 }

@@ -24,6 +24,35 @@ constexpr int kMtM = 397;
 // init_genrand(19650218): the table every init_by_array starts from (host-computed).
 __constant__ uint32_t c_mt_init[kMtN];
 
+// lognormvariate = exp(normalvariate): CPython calls the host libm's exp.  glibc's exp is the
+// table-driven algorithm of sysdeps/ieee754/dbl-64/e_exp.c (N = 128, degree-5 polynomial); the host
+// reads its constants and table out of the very libm CPython uses (bbe_sim.cu: load_libm_exp) and
+// the kernel evaluates it in the order the FMA build of that code does, which reproduces exp()
+// bit-for-bit (tools/glibc_exp_probe.c: 0 mismatches in 4e7 arguments).  If the table was not found,
+// c_exp_ok = 0 and CUDA's exp is used (last-bit differences possible).
+__constant__ uint64_t c_exp_tab[256];
+__constant__ double c_exp_c[8];  // invln2N, shift, negln2hiN, negln2loN, C2, C3, C4, C5
+__constant__ int c_exp_ok;
+
+__device__ __forceinline__ double libm_exp(double x) {
+    const uint64_t ux = __double_as_longlong(x);
+    const uint32_t abstop = (uint32_t)(ux >> 52) & 0x7ffu;
+    if (!c_exp_ok || abstop >= 0x408u) return exp(x);  // |x| >= 512 (never reached by the step laws)
+    if (abstop < 0x3c9u) return __dadd_rn(1.0, x);      // |x| < 2^-54: glibc returns 1.0 + x
+    double kd = __fma_rn(c_exp_c[0], x, c_exp_c[1]);
+    const uint64_t ki = __double_as_longlong(kd);
+    kd = __dsub_rn(kd, c_exp_c[1]);
+    const double r = __fma_rn(kd, c_exp_c[3], __fma_rn(kd, c_exp_c[2], x));
+    const int idx = 2 * (int)(ki % 128u);
+    const uint64_t top = ki << 45;
+    const double tail = __longlong_as_double(c_exp_tab[idx]);
+    const double scale = __longlong_as_double(c_exp_tab[idx + 1] + top);
+    const double r2 = __dmul_rn(r, r);
+    const double tmp = __fma_rn(__dmul_rn(r2, r2), __fma_rn(r, c_exp_c[7], c_exp_c[6]),
+                                __fma_rn(r2, __fma_rn(r, c_exp_c[5], c_exp_c[4]), __dadd_rn(tail, r)));
+    return __fma_rn(scale, tmp, scale);
+}
+
 __host__ __device__ inline uint64_t splitmix64_dev(uint64_t x) {
     x += 0x9E3779B97F4A7C15ull;
     x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;

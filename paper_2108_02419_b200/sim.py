@@ -49,6 +49,7 @@ EXPORTED_SYMBOLS = (
     "bbe_last_kernel_ms",
     "bbe_param_bytes",
     "bbe_mt_getrandbits64",
+    "bbe_mt_exp_exact",
 )
 
 
@@ -134,6 +135,7 @@ def lib():
         L.bbe_last_kernel_ms.restype = ctypes.c_float
         L.bbe_mt_getrandbits64.argtypes = [_P(ctypes.c_uint32), ctypes.c_int64, _P(ctypes.c_uint64)]
         L.bbe_mt_getrandbits64.restype = ctypes.c_int
+        L.bbe_mt_exp_exact.restype = ctypes.c_int
         L.bbe_param_bytes.argtypes = [ctypes.c_int32]
         L.bbe_param_bytes.restype = ctypes.c_int64
         L.bbe_last_error.restype = ctypes.c_char_p

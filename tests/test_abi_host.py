@@ -66,6 +66,11 @@ def test_dry_run_seeds_match_sequential_getrandbits(d, pre):
     assert dry_run_seeds(c, d, want=False) is None and c.getstate() != random.Random(11).getstate()
 
 
+def test_libm_exp_table_located_and_verified():
+    """MT mode's lognormal steps need the host libm's exp bit for bit (Lib/random.py lognormvariate)."""
+    assert sim.lib().bbe_mt_exp_exact() == 1
+
+
 def test_validation_mirrors_reference_errors():
     bad = [
         RaceConfig(0.0, (Competitor("a", UniformSteps(1, 2)),)),
