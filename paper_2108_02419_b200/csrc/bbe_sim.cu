@@ -344,8 +344,6 @@ extern "C" {
 
 int bbe_version(void) { return BBE_ABI_VERSION; }
 
-int bbe_mt_exp_exact(void) { return libm_exp_table().ok ? 1 : 0; }
-
 float bbe_last_kernel_ms(void) {
     DevCtx* ctx = nullptr;
     if (get_ctx(&ctx)) return -1.f;
@@ -791,5 +789,7 @@ int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const 
     BBE_CK(cudaEventRecord(ctx->ev1, s));
     return BBE_OK;
 }
+
+int bbe_mt_exp_exact(void) { return libm_exp_table().ok ? 1 : 0; }
 
 }  // extern "C"
