@@ -286,17 +286,24 @@ def run_ours(args):
         # e2e through the public API (host buffers; agent stream advance + H2D params + D2H tally)
         import random
 
-        agent = random.Random(11)
-        e2e_t = []
-        for i in range(args.warmup + args.steps):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            probs = rp_predict(state, cfg, sims, agent)
-            e2e_t.append(time.perf_counter() - t0)
-        assert abs(sum(probs) - 1.0) < 1e-9
-        e2e_s = statistics.mean(e2e_t[args.warmup:])
+        def time_calls(mode, steps):
+            agent = random.Random(11)
+            ts = []
+            for i in range(args.warmup + steps):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                probs = rp_predict(state, cfg, sims, agent, mode=mode)
+                ts.append(time.perf_counter() - t0)
+            assert abs(sum(probs) - 1.0) < 1e-9
+            return statistics.mean(ts[args.warmup:])
+
+        e2e_s = time_calls("native", args.steps)
         h2d = int(sim.lib().bbe_param_bytes(n))  # the race-parameter block, the call's only H2D input
         d2h = launcher.tally_len * 8
+        # MT mode: the reference's own MT19937 streams, bit-identical results (seeds are H2D inputs)
+        mt_steps = max(3, min(args.steps, 20))
+        e2e_mt_s = time_calls("mt", mt_steps)
+        mt_kernel_ms = launcher.last_kernel_ms()  # seed kernel + race kernel of the last MT call
 
         cpu = cpu_baseline_pyref(cfg, state, args.cpu_sample) if args.cpu_sample else None
         cpu_c = cpu_baseline_c(cfg, state, args.cpu_c_sample) if args.cpu_c_sample else None
@@ -314,7 +321,10 @@ def run_ours(args):
                          "ops_per_ct": ops, "f_free": f_free, "kernel_ms": k_ms,
                          "peak_source": f"{sms} SMs x 128 FP32/INT32 lanes x {max_mhz:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)"},
             "e2e": {"value": sims / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "api": "paper_2108_02419_b200.agents.rp_predict", "ms_per_call": e2e_s * 1e3},
+                    "api": "paper_2108_02419_b200.agents.rp_predict(mode='native')", "ms_per_call": e2e_s * 1e3},
+            "mt_exact": {"e2e_value": sims / e2e_mt_s, "unit": UNIT, "ms_per_call": e2e_mt_s * 1e3,
+                         "device_ms": mt_kernel_ms, "h2d_bytes_per_step": h2d + 8 * sims, "d2h_bytes_per_step": d2h,
+                         "api": "rp_predict(mode='mt'): bit-identical to the reference for the same seeds"},
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

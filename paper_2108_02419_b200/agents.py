@@ -42,12 +42,13 @@ def dry_run_seeds(rng, d: int, *, want: bool = True) -> np.ndarray | None:
     return np.frombuffer(bits.to_bytes(8 * d, "little"), dtype="<u8").astype(np.uint64) if want else None
 
 
-def rp_predict(state, config, d: int, rng, *, mode: str = "native") -> tuple[float, ...]:
+def rp_predict(state, config, d: int, rng, *, mode: str = "mt") -> tuple[float, ...]:
     """Laplace-smoothed win probabilities from d dry-run continuations, computed on the GPU.
 
-    mode="native": Philox stream keyed by the first dry-run seed (statistically equal to the
-    reference); mode="mt": every continuation replays the reference's own MT19937 stream from its
-    dry-run seed, so the probabilities equal the reference's exactly.
+    mode="mt" (default): every continuation replays the reference's own MT19937 stream from its
+    dry-run seed, so the probabilities equal the reference's exactly (a true drop-in).
+    mode="native": Philox stream keyed by the first dry-run seed -- statistically equal to the
+    reference (binomial bounds, tests/test_gpu_native.py) and the fastest path.
     """
     n = len(config.competitors)
     if d <= 0:

@@ -230,7 +230,7 @@ class Trajectory:
 # -- GPU-backed entry points (thin wrappers over sim.py) ----------------------------------------
 
 
-def simulate_from(state, config, seed: int, *, mode: str = "native") -> tuple[str, ...]:
+def simulate_from(state, config, seed: int, *, mode: str = "mt") -> tuple[str, ...]:
     """Finish order of one continuation of ``state`` (race.py:393-406) computed on the GPU.
 
     ``mode="mt"`` (default) reproduces the reference's CPython MT19937 stream from ``seed`` in-kernel,
@@ -241,8 +241,9 @@ def simulate_from(state, config, seed: int, *, mode: str = "native") -> tuple[st
     return _sf(state, config, seed, mode=mode)
 
 
-def run_race(config, seed: int, record: bool = True, *, mode: str = "native") -> Trajectory:
-    """One race from the start line (race.py:373-390) on the GPU."""
+def run_race(config, seed: int, record: bool = True, *, mode: str = "mt") -> Trajectory:
+    """One race from the start line (race.py:373-390) on the GPU (``mode="mt"``: the reference's
+    result for the same seed)."""
     from .sim import run_race as _rr
 
     return _rr(config, seed, record=record, mode=mode)

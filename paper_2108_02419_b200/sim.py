@@ -324,14 +324,16 @@ def simulate_batch(
 # -- reference-shaped single-race entry points ---------------------------------------------------
 
 
-def simulate_from(state, config, seed: int, *, mode: str = "native") -> tuple[str, ...]:
-    """One continuation (race.py:393-406) on the GPU; returns the finish order as ids."""
+def simulate_from(state, config, seed: int, *, mode: str = "mt") -> tuple[str, ...]:
+    """One continuation (race.py:393-406) on the GPU; returns the finish order as ids.
+
+    mode="mt" (default): the reference's MT19937 stream from ``seed`` -- the reference's own result."""
     r = simulate_batch(state, config, 1, seed, mode=mode, records=True, ranks=False,
                        seeds=np.array([seed & M64], np.uint64) if mode == "mt" else None)
     return tuple(r.ids[c] for c in r.order[0])
 
 
-def run_race(config, seed: int, record: bool = True, *, mode: str = "native") -> Trajectory:
+def run_race(config, seed: int, record: bool = True, *, mode: str = "mt") -> Trajectory:
     """One race from the start line (race.py:373-390) on the GPU.
 
     record=True (snapshots of every tick) is not produced by the batched kernel; it raises.
