@@ -117,21 +117,30 @@ __global__ void __launch_bounds__(128) mt_seed_kernel(const uint64_t* seeds, uin
     // pass 2 (k = 623 iterations): i = 2..623, then wrap and i = 1; mt[0] = 0x80000000 at the end.
     // Words 2..623 stream out through the transpose tile, 32 at a time.
     prev = m1;
-    for (int i = 2; i < kMtN; ++i) {
-        const uint32_t p = on ? scratch[(int64_t)i * n_pad + s] : 0u;
-        const uint32_t v = (p ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)i;
-        prev = v;
-        tile[warp][i & 31][lane] = v;
-        if ((i & 31) == 31 || i == kMtN - 1) {
-            __syncwarp();
-            const int blk0 = i & ~31;
-            const int w = blk0 + lane;  // this lane writes word w of each of the warp's 32 sims
-            for (int r = 0; r < 32; ++r) {
-                const int64_t sr = warp_base + r;
-                if (sr < n && w >= 2 && w <= i) states[sr * kMtN + w] = tile[warp][lane][r];
-            }
-            __syncwarp();
+    for (int blk0 = 0; blk0 < kMtN; blk0 += 32) {
+        // the 32 pass-1 words of this block are independent loads: issue them all before the chain
+        uint32_t p[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+            const int i = blk0 + t;
+            p[t] = (on && i >= 2 && i < kMtN) ? scratch[(int64_t)i * n_pad + s] : 0u;
         }
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+            const int i = blk0 + t;
+            if (i >= 2 && i < kMtN) {
+                const uint32_t v = (p[t] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)i;
+                prev = v;
+                tile[warp][t][lane] = v;
+            }
+        }
+        __syncwarp();
+        const int w = blk0 + lane;  // this lane writes word w of each of the warp's 32 sims
+        for (int r = 0; r < 32; ++r) {
+            const int64_t sr = warp_base + r;
+            if (sr < n && w >= 2 && w < kMtN) states[sr * kMtN + w] = tile[warp][lane][r];
+        }
+        __syncwarp();
     }
     const uint32_t f1 = (m1 ^ ((prev ^ (prev >> 30)) * 1566083941u)) - 1u;
     if (on) {
