@@ -118,6 +118,13 @@ typedef struct {
     int64_t first_bad_draws; /* INJECT: first sim whose draw stream mismatched, -1 none */
     float kernel_ms;         /* device time of the race kernel(s) */
     int32_t lanes_per_slot;  /* K actually used */
+    /* Trajectories (INJECT / MT only; run_race(record=True), race.py:378-389): positions and previous
+     * steps after every tick, [n_sims][traj_cap+1][n] each (row t = after tick t, row 0 = the start);
+     * rows past a sim's last tick are not written.  traj_cap = 0 disables recording. */
+    double* traj_positions;
+    double* traj_prev_steps;
+    int32_t traj_cap;
+    int32_t _pad;
 } bbe_result;
 
 int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_state* state,

@@ -78,6 +78,7 @@ struct DevCtx {
     HostBuf h_params, h_tally;
     DevBuf d_params, d_tally, d_draws, d_offsets, d_winner, d_order, d_fin, d_fpos, d_blocked, d_dused;
     DevBuf d_seeds, d_mt_states, d_mt_scratch;  // MT mode
+    DevBuf d_traj;                               // trajectories (positions, previous steps)
     bool mt_table = false;                       // c_mt_init uploaded on this device
 };
 
@@ -621,6 +622,10 @@ static int launch_all(DevCtx* ctx, const Plan& pl, LaunchArgs a, const bbe_compe
         if (b.finish_ticks) b.finish_ticks += c0 * n;
         if (b.final_pos) b.final_pos += c0 * n;
         if (b.blocked) b.blocked += c0;
+        if (b.traj_pos) {
+            b.traj_pos += c0 * ((int64_t)b.traj_cap + 1) * n;
+            b.traj_prev += c0 * ((int64_t)b.traj_cap + 1) * n;
+        }
         int rc = launch_one(pl, b, stream);
         if (rc) return rc;
     }
@@ -658,6 +663,9 @@ static int build_args(const Plan& pl, const bbe_race* race, const bbe_state* st,
         a.final_pos = dev_out->final_positions;
         a.blocked = dev_out->blocked;
         a.draws_used = dev_out->draws_used;
+        a.traj_pos = dev_out->traj_cap > 0 ? dev_out->traj_positions : nullptr;
+        a.traj_prev = dev_out->traj_cap > 0 ? dev_out->traj_prev_steps : nullptr;
+        a.traj_cap = dev_out->traj_cap;
     }
     return BBE_OK;
 }
@@ -720,6 +728,15 @@ int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_st
         BBE_CK(ctx->d_dused.ensure(ns * sizeof(int64_t)));
         dev.draws_used = (int64_t*)ctx->d_dused.p;
     }
+    size_t traj_elems = 0;
+    if (out->traj_cap > 0 && out->traj_positions && out->traj_prev_steps) {
+        if (rq->mode == BBE_MODE_NATIVE) return fail(BBE_EINVAL, "trajectories are recorded by the exact modes (mt, inject)");
+        traj_elems = (size_t)ns * ((size_t)out->traj_cap + 1) * n;
+        BBE_CK(ctx->d_traj.ensure(2 * traj_elems * sizeof(double)));
+        dev.traj_positions = (double*)ctx->d_traj.p;
+        dev.traj_prev_steps = (double*)ctx->d_traj.p + traj_elems;
+        dev.traj_cap = out->traj_cap;
+    }
 
     LaunchArgs a;
     build_args(pl, race, st, rq, (const double*)ctx->d_params.p, d_draws, d_offsets, (uint64_t*)ctx->d_tally.p, &dev,
@@ -738,6 +755,10 @@ int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_st
     if (out->blocked && ns) BBE_CK(cudaMemcpyAsync(out->blocked, dev.blocked, ns * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     if (dev.draws_used && ns)
         BBE_CK(cudaMemcpyAsync(out->draws_used, dev.draws_used, ns * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    if (traj_elems) {
+        BBE_CK(cudaMemcpyAsync(out->traj_positions, dev.traj_positions, traj_elems * sizeof(double), cudaMemcpyDeviceToHost, s));
+        BBE_CK(cudaMemcpyAsync(out->traj_prev_steps, dev.traj_prev_steps, traj_elems * sizeof(double), cudaMemcpyDeviceToHost, s));
+    }
     BBE_CK(cudaStreamSynchronize(s));
 
     const uint64_t* T = (const uint64_t*)ctx->h_tally.p;

@@ -70,6 +70,9 @@ struct LaunchArgs {
     const int64_t* draw_offsets;  // INJECT [n_sims+1]
     const uint32_t* mt_states;    // MT: [n_sims][624] seeded MT19937 states
     double nv_magic;              // MT: random.NV_MAGICCONST = 4*exp(-0.5)/sqrt(2.0), host libm
+    double* traj_pos;             // exact modes, optional: [n_sims][traj_cap+1][n] positions per tick
+    double* traj_prev;            //   and previous steps (run_race(record=True), race.py:378-389)
+    int32_t traj_cap;             //   ticks recorded per sim (longer sims are reported via n_ticks)
     uint64_t* tally;              // device, TallyLayout
     int32_t* winner;              // optional per-sim outputs
     int32_t* order;

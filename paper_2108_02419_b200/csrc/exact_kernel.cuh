@@ -183,6 +183,17 @@ exact_kernel(const LaunchArgs a) {
         return d;
     };
 
+    // trajectory snapshot after tick t of the current sim (t = 0: the state the sim starts from)
+    auto record = [&](int32_t t) {
+        const int64_t row = (s * ((int64_t)a.traj_cap + 1) + t) * n;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (!has[k]) continue;
+            a.traj_pos[row + cidx[k]] = pos[k];
+            a.traj_prev[row + cidx[k]] = prev[k];
+        }
+    };
+
     // refill the segment with its next sim; warp-uniform (every lane calls it)
     auto load_sim = [&](bool do_it) {
         if (do_it) {
@@ -233,6 +244,7 @@ exact_kernel(const LaunchArgs a) {
         if (do_it) {
 #pragma unroll
             for (int k = 0; k < K; ++k) pv[k] = racing[k] ? pos[k] : NEG_INF;
+            if (a.traj_pos && running) record(0);
         }
     };
 
@@ -429,7 +441,10 @@ exact_kernel(const LaunchArgs a) {
                 }
                 pv[k] = racing[k] ? pos[k] : NEG_INF;
             }
-            if (seg_running && !diverged) rt += 1;
+            if (seg_running && !diverged) {
+                rt += 1;
+                if (a.traj_pos && rt <= a.traj_cap) record(rt);
+            }
         }
     }
 

@@ -108,7 +108,9 @@ class BbeResult(ctypes.Structure):
                 ("blocked", _P(ctypes.c_int64)), ("draws_used", _P(ctypes.c_int64)),
                 ("competitor_steps", ctypes.c_uint64), ("blocked_steps", ctypes.c_uint64),
                 ("first_diverged", ctypes.c_int64), ("first_bad_draws", ctypes.c_int64),
-                ("kernel_ms", ctypes.c_float), ("lanes_per_slot", ctypes.c_int32)]
+                ("kernel_ms", ctypes.c_float), ("lanes_per_slot", ctypes.c_int32),
+                ("traj_positions", _P(ctypes.c_double)), ("traj_prev_steps", _P(ctypes.c_double)),
+                ("traj_cap", ctypes.c_int32), ("_pad", ctypes.c_int32)]
 
 
 _lib = None
@@ -230,6 +232,8 @@ class SimResult:
     blocked_steps: int
     kernel_ms: float
     lanes_per_slot: int
+    traj_positions: np.ndarray | None = None
+    traj_prev_steps: np.ndarray | None = None
 
     def win_probabilities(self, laplace: bool = True) -> tuple[float, ...]:
         """(w + 1) / (d + n) as agents.py:166, or plain frequencies."""
@@ -267,6 +271,8 @@ def simulate_batch(
     ranks: bool = True,
     perms: bool = False,
     records: bool = False,
+    winners: bool = False,
+    trajectory_ticks: int = 0,
     lanes_per_slot: int = 0,
 ) -> SimResult:
     """Run ``n_sims`` independent continuations of ``state`` (or races from the start line when
@@ -274,8 +280,12 @@ def simulate_batch(
 
     mode="native": Philox stream keyed by ``seed``; sim i uses counter (tick block, competitor,
     sim_offset + i), so any sharding of the index range reproduces the same per-sim outcomes.
+    mode="mt": sim i replays random.Random(seeds[i]) (or derive_seed(seed_master, "run",
+    sim_offset + i) when ``seeds`` is None) -- the reference's own result.
     mode="inject": replay recorded reference draws (``draws`` / CSR ``draw_offsets``) -- bit-exact.
-    records=True also returns per-sim winner, order, finish ticks, final positions, blocked counts.
+    records=True also returns per-sim winner, order, finish ticks, final positions, blocked counts;
+    winners=True only the per-sim winner; trajectory_ticks=T (exact modes) positions and previous
+    steps after each of the first T ticks of every sim.
     """
     if mode not in MODES:
         raise ValueError(f"unknown mode {mode!r}")
@@ -296,29 +306,38 @@ def simulate_batch(
         req.draw_offsets = _ptr(draw_offsets, ctypes.c_int64)
     if seeds is not None:
         seeds = np.ascontiguousarray(seeds, np.uint64)
+        if len(seeds) != n_sims:
+            raise ValueError("seeds needs one entry per sim")
         req.seeds = _ptr(seeds, ctypes.c_uint64)
     wins = np.zeros(n, np.uint64)
     rk = np.zeros((n, n), np.uint64) if ranks else None
     pm = np.zeros(math.factorial(n), np.uint64) if (perms and n <= MAX_PERM_COMPETITORS) else None
-    winner = order = fin = fpos = blk = used = None
-    if records:
+    winner = order = fin = fpos = blk = used = tpos = tprev = None
+    if records or winners:
         winner = np.zeros(n_sims, np.int32)
+    if records:
         order = np.zeros((n_sims, n), np.int32)
         fin = np.zeros((n_sims, n), np.int64)
         fpos = np.zeros((n_sims, n), np.float64)
         blk = np.zeros(n_sims, np.int64)
         used = np.zeros(n_sims, np.int64) if mode == "inject" else None
+    cap = int(trajectory_ticks)
+    if cap > 0:
+        tpos = np.zeros((n_sims, cap + 1, n), np.float64)
+        tprev = np.zeros((n_sims, cap + 1, n), np.float64)
     res = BbeResult(_ptr(wins, ctypes.c_uint64), _ptr(rk, ctypes.c_uint64), _ptr(pm, ctypes.c_uint64),
                     _ptr(winner, ctypes.c_int32), _ptr(order, ctypes.c_int32), _ptr(fin, ctypes.c_int64),
                     _ptr(fpos, ctypes.c_double), _ptr(blk, ctypes.c_int64), _ptr(used, ctypes.c_int64),
-                    0, 0, -1, -1, 0.0, 0)
+                    0, 0, -1, -1, 0.0, 0, _ptr(tpos, ctypes.c_double), _ptr(tprev, ctypes.c_double), cap, 0)
     rc = lib().bbe_simulate(ctypes.byref(pk.race), pk.comps, ctypes.byref(st), ctypes.byref(req), ctypes.byref(res))
     del keep
     if rc != BBE_OK:
         _raise(rc, res)
-    return SimResult(pk.ids, n_sims, wins, rk, pm, winner, order, fin, fpos, blk, used,
-                     int(res.competitor_steps), int(res.blocked_steps), float(res.kernel_ms),
-                     int(res.lanes_per_slot))
+    out = SimResult(pk.ids, n_sims, wins, rk, pm, winner, order, fin, fpos, blk, used,
+                    int(res.competitor_steps), int(res.blocked_steps), float(res.kernel_ms),
+                    int(res.lanes_per_slot))
+    out.traj_positions, out.traj_prev_steps = tpos, tprev
+    return out
 
 
 # -- reference-shaped single-race entry points ---------------------------------------------------
@@ -333,25 +352,40 @@ def simulate_from(state, config, seed: int, *, mode: str = "mt") -> tuple[str, .
     return tuple(r.ids[c] for c in r.order[0])
 
 
-def run_race(config, seed: int, record: bool = True, *, mode: str = "mt") -> Trajectory:
+def run_race(config, seed: int, record: bool = True, *, mode: str = "mt", with_prev_steps: bool = False):
     """One race from the start line (race.py:373-390) on the GPU.
 
-    record=True (snapshots of every tick) is not produced by the batched kernel; it raises.
+    record=True returns the per-tick position snapshots (``Trajectory.ticks``) recorded by the exact
+    kernel (mode "mt" or "inject"); with_prev_steps=True also returns the per-tick previous steps as
+    a second value (the state an in-play bettor reconstructs, agents.py:348-358).
     """
+    seeds = np.array([seed & M64], np.uint64) if mode == "mt" else None
+    cap = 0
     if record:
-        raise NotImplementedError("per-tick trajectory recording is not implemented on the GPU path; "
-                                  "use record=False")
-    r = simulate_batch(None, config, 1, seed, mode=mode, records=True, ranks=False,
-                       seeds=np.array([seed & M64], np.uint64) if mode == "mt" else None)
-    return Trajectory(
+        if mode == "native":
+            raise ValueError("record=True needs an exact mode (mt)")
+        cap = int(min(config.tick_limit, 4096))
+    while True:
+        r = simulate_batch(None, config, 1, seed, mode=mode, records=True, ranks=False, seeds=seeds,
+                           trajectory_ticks=cap)
+        n_ticks = int(r.finish_ticks[0].max())
+        if not record or n_ticks <= cap:
+            break
+        cap = n_ticks  # the race outlived the first guess: record again with room for every tick
+    ticks = prevs = None
+    if record:
+        ticks = tuple(tuple(float(p) for p in row) for row in r.traj_positions[0, : n_ticks + 1])
+        prevs = r.traj_prev_steps[0, : n_ticks + 1].copy()
+    traj = Trajectory(
         competitor_ids=r.ids,
         dt=config.dt,
-        ticks=None,
+        ticks=ticks,
         finish_ticks=tuple(int(t) for t in r.finish_ticks[0]),
         finish_order=tuple(r.ids[c] for c in r.order[0]),
         final_positions=tuple(float(p) for p in r.final_positions[0]),
         blocked_steps=int(r.blocked[0]),
     )
+    return (traj, prevs) if with_prev_steps else traj
 
 
 # -- device-resident path (bench `value`, multi-GPU shards) --------------------------------------

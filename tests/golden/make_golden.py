@@ -229,8 +229,26 @@ def make_c2_json():
                    "agent_next_random": after}, fh, indent=0)
 
 
+def make_sessions_json():
+    """wake_schedule (session.py:104-121) for a few agent populations."""
+    from racemarket.agents import AgentParams
+    from racemarket.session import wake_schedule
+
+    cases = []
+    for seed, periods, jitters, horizon in [(7, [1.0] * 5, [1.0] * 5, 12.0),
+                                            (20260818, [1.0, 2.5, 0.5], [1.0, 0.0, 3.0], 30.0),
+                                            (3, [1.0] * 100, [1.0] * 100, 5.0)]:
+        params = [AgentParams("rp", reevaluate_every=p, wake_jitter=j) for p, j in zip(periods, jitters)]
+        wakes = wake_schedule(params, horizon, seed)
+        cases.append({"seed": seed, "reevaluate_every": periods, "wake_jitter": jitters, "horizon": horizon,
+                      "wakes": [list(w) for w in wakes]})
+    with open(os.path.join(HERE, "sessions.json"), "w") as fh:
+        json.dump({"wake_schedules": cases}, fh)
+
+
 if __name__ == "__main__":
     make_rng_json()
     make_c2_json()
     make_races_json()
+    make_sessions_json()
     print("golden vectors written to", HERE)
