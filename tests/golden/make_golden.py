@@ -246,7 +246,19 @@ def make_sessions_json():
         json.dump({"wake_schedules": cases}, fh)
 
 
+def make_derby_experiment():
+    """The reference's canonical (defaults-applied) form of configs/derby.json, minus the session."""
+    from racemarket.config import config_to_dict
+
+    with open(DERBY) as fh:
+        canon = config_to_dict(parse_config(json.load(fh)))
+    canon.pop("session", None)
+    with open(os.path.join(HERE, "derby_experiment.json"), "w") as fh:
+        json.dump(canon, fh, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
+    make_derby_experiment()
     make_rng_json()
     make_c2_json()
     make_races_json()

@@ -95,3 +95,44 @@ def test_dry_run_session_c4_shape():
     for t, i, p in out.predictions[:60]:
         tick = 0 if t <= 3.0 else int(np.ceil(t - 3.0 - 1e-9))
         assert rp_predict(states[tick], base, 50, rngs[i], mode="mt") == p
+
+
+def test_cli_products(tmp_path):
+    """python -m paper_2108_02419_b200 race|batch|bench|compare writes the reference's file formats."""
+    import csv
+    import json
+    import os
+
+    from golden_io import GOLDEN
+    from paper_2108_02419_b200.__main__ import main
+    from paper_2108_02419_b200.products import read_pmf_csv
+
+    cfgp = os.path.join(GOLDEN, "derby_experiment.json")
+    assert main(["race", "--config", cfgp, "--out", str(tmp_path / "r")]) == 0
+    rows = list(csv.reader(open(tmp_path / "r" / "finish.csv")))
+    assert rows[0] == ["competitor_id", "finish_tick", "finish_rank"] and len(rows) == 6
+    # the reference's own race for derive_seed(20260818, "race") (cli.py:80-88)
+    cfg = _race_from_doc(cfgp)
+    o = oracle.run_race(cfg, oracle_seed_race())
+    ticks = {r[0]: int(r[1]) for r in rows[1:]}
+    assert [ticks[cid] for cid in cfg.competitor_ids] == [int(t) for t in o.finish_ticks]
+    assert json.load(open(cfgp))["seed"] == 20260818
+    assert main(["batch", "--config", cfgp, "--out", str(tmp_path / "b"), "--replications", "500"]) == 0
+    assert main(["batch", "--config", cfgp, "--out", str(tmp_path / "b2"), "--replications", "500"]) == 0
+    a, b = read_pmf_csv(tmp_path / "b" / "pmf.csv"), read_pmf_csv(tmp_path / "b2" / "pmf.csv")
+    assert a == b and a.n_samples == 500
+    assert main(["compare", str(tmp_path / "b" / "pmf.csv"), str(tmp_path / "b2" / "pmf.csv")]) == 0
+    runs = list(csv.reader(open(tmp_path / "b" / "runs.csv")))
+    assert runs[0] == ["run", "winner", "winner_ticks", "n_ticks", "finish_order"] and len(runs) == 501
+
+
+def _race_from_doc(path):
+    from paper_2108_02419_b200.products import load_experiment
+
+    return load_experiment(path)[1]
+
+
+def oracle_seed_race():
+    from paper_2108_02419_b200.seeding import derive_seed
+
+    return derive_seed(20260818, "race")

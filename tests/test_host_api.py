@@ -89,3 +89,23 @@ def test_batch_config_validation():
     import pickle
 
     assert pickle.loads(pickle.dumps(e)).run_index == 7
+
+
+def test_race_section_parser_matches_reference_defaults():
+    """products.parse_race applies the reference's defaults (config.py:93-178); derby.json parses."""
+    from paper_2108_02419_b200.products import ConfigError, load_experiment, parse_race
+    from golden_io import config_from_dict, c2
+
+    # the reference's canonical form of configs/derby.json (config_to_dict(parse_config(...)), make_golden.py)
+    doc, cfg, seed = load_experiment(os.path.join(GOLDEN, "derby_experiment.json"))
+    assert seed == 20260818 and cfg.n_competitors == 5 and cfg.conditions == 0.35
+    ref10 = config_from_dict(c2()["config"])  # the reference's parse of the same file, resized to 10
+    for mine, ref in zip(cfg.competitors, ref10.competitors[:5]):
+        assert (mine.steps, mine.preference, mine.pref_sensitivity, mine.theta, mine.responsiveness) == \
+            (ref.steps, ref.preference, ref.pref_sensitivity, ref.theta, ref.responsiveness)
+    with pytest.raises(ConfigError):
+        parse_race({"competitors": [{"id": "a-b", "steps": {"family": "uniform", "lo": 1, "hi": 2}}]})
+    with pytest.raises(ConfigError):
+        parse_race({"competitors": [{"id": "a", "steps": {"family": "gamma"}}]})
+    with pytest.raises(ConfigError):
+        parse_race({"competitors": [], "track_length": 10})
