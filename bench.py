@@ -188,6 +188,48 @@ def run_reference(args):
     return 0
 
 
+def sweep_configs(args, torch, sim):
+    """The other BASELINE.json configs, device-resident NATIVE launches (one warm-up + one timed each):
+    C1 = 5 x U(10,20), L=2000 from the start line (1,000 sims, the reference's CPU case, and 10^6);
+    C3 = 20 x U(10,20), L=2000, 10^7 sims; derby20 = derby.json resized to 20, 10^6 sims."""
+    from golden_io import c2, config_from_dict
+    from paper_2108_02419_b200.batch import resize_race
+    from paper_2108_02419_b200.race import Competitor, RaceConfig, UniformSteps
+
+    def uniform_field(n):
+        return RaceConfig(2000.0, tuple(Competitor(f"c{i + 1}", UniformSteps(10.0, 20.0)) for i in range(n)))
+
+    derby10 = config_from_dict(c2()["config"])
+    derby5 = resize_race(derby10, 5)
+    runs = [("C1_5x_U10_20_from_start_1e3", uniform_field(5), 1_000),
+            ("C1_5x_U10_20_from_start_1e6", uniform_field(5), 1_000_000),
+            ("C3_20x_U10_20_from_start_1e7", uniform_field(20), args.c3_sims),
+            ("derby20_from_start_1e6", resize_race(derby5, 20), 1_000_000)]
+    out = {}
+    stream = torch.cuda.current_stream()
+    for name, cfg, n_sims in runs:
+        L = sim.DeviceLauncher(None, cfg)
+        tally = torch.zeros(L.tally_len, dtype=torch.int64, device="cuda")
+        L.launch(tally.data_ptr(), min(n_sims, 100_000), 1, stream=stream.cuda_stream)
+        torch.cuda.synchronize()
+        tally.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        L.launch(tally.data_ptr(), n_sims, 2, stream=stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        t = tally.cpu()
+        ct = int(t[L.off["ct"]])
+        blocked = int(t[L.off["blocked"]])
+        n = len(cfg.competitors)
+        ops = ops_per_ct(n, 1.0 - blocked / ct)
+        out[name] = {"sims": n_sims, "ms": ms, "races_per_s": n_sims / (ms / 1e3), "ct_per_s": ct / (ms / 1e3),
+                     "ct_per_race": ct / n_sims, "issue_roofline_frac": ct * ops / (ms / 1e3) / 37.22e12,
+                     "scan_needed": any(c.theta > 0 for c in cfg.competitors)}
+    return out
+
+
 def load_traffic():
     p = os.path.join(ROOT, "profiles", "race_kernel_ncu.json")
     if os.path.exists(p):
@@ -305,6 +347,7 @@ def run_ours(args):
         e2e_mt_s = time_calls("mt", mt_steps)
         mt_kernel_ms = launcher.last_kernel_ms()  # seed kernel + race kernel of the last MT call
 
+        sweep = sweep_configs(args, torch, sim) if args.sweep else None
         cpu = cpu_baseline_pyref(cfg, state, args.cpu_sample) if args.cpu_sample else None
         cpu_c = cpu_baseline_c(cfg, state, args.cpu_c_sample) if args.cpu_c_sample else None
         line = {
@@ -330,6 +373,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "cpu_baseline_c": cpu_c,
             "device": name,
+            "other_configs": sweep,
         }
     if world > 1:
         dist.barrier()
@@ -349,6 +393,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=10000, help="pyref sims for cpu_baseline (0 = skip)")
     ap.add_argument("--cpu-c-sample", type=int, default=200_000, help="C oracle sims (0 = skip)")
     ap.add_argument("--ref-sample", type=int, default=2000, help="sims per --impl reference step")
+    ap.add_argument("--sweep", type=int, default=1, help="also time the other BASELINE configs (0 = skip)")
+    ap.add_argument("--c3-sims", type=int, default=10_000_000)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup < 3 requested; timing rules want >= 3", file=sys.stderr)
