@@ -223,10 +223,13 @@ def sweep_configs(args, torch, sim):
         ct = int(t[L.off["ct"]])
         blocked = int(t[L.off["blocked"]])
         n = len(cfg.competitors)
-        ops = ops_per_ct(n, 1.0 - blocked / ct)
+        scan = any(c.theta > 0 for c in cfg.competitors)
+        # with every theta = 0 no competitor can be blocked (gap > 0 = theta), so the front-runner
+        # scan's result is never used: the algorithmic ops drop the 4(n-1) scan term
+        ops = ops_per_ct(n, 1.0 - blocked / ct) - (0 if scan else 4 * (n - 1))
         out[name] = {"sims": n_sims, "ms": ms, "races_per_s": n_sims / (ms / 1e3), "ct_per_s": ct / (ms / 1e3),
-                     "ct_per_race": ct / n_sims, "issue_roofline_frac": ct * ops / (ms / 1e3) / 37.22e12,
-                     "scan_needed": any(c.theta > 0 for c in cfg.competitors)}
+                     "ct_per_race": ct / n_sims, "ops_per_ct": ops,
+                     "issue_roofline_frac": ct * ops / (ms / 1e3) / 37.22e12, "scan_needed": scan}
     return out
 
 

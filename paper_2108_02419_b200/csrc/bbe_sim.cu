@@ -496,7 +496,7 @@ static int launch_one(const Plan& pl, const LaunchArgs& a, cudaStream_t stream) 
     return BBE_OK;
 }
 
-constexpr int64_t kMtChunk = 65536;  // sims seeded per MT chunk: 2 x 160 MB of state + scratch
+constexpr int64_t kMtChunk = 131072;  // sims seeded per MT chunk: 2 x 320 MB of state + scratch
 
 // init_genrand(19650218) (CPython _randommodule.c), the start of every init_by_array
 static void mt_init_table(uint32_t* t) {

@@ -169,10 +169,21 @@ exact_kernel(const LaunchArgs a) {
                 if (is_stop && trying) {
                     const double u1 = mt_random53(w[0], w[1]);
                     const double u2 = __dsub_rn(1.0, mt_random53(w[2], w[3]));
-                    const double z = __ddiv_rn(__dmul_rn(a.nv_magic, __dsub_rn(u1, 0.5)), u2);
-                    const double zz = __ddiv_rn(__dmul_rn(z, z), 4.0);
-                    acc = zz <= -log(u2);
+                    // accept iff z*z/4 <= -log(u2) (Lib/random.py normalvariate).  Decide in FP32 when
+                    // the two sides are far apart (relative 1e-4, absolute 1e-5: >25x the FP32 error of
+                    // either side), else in FP64 exactly as CPython does -- the same decision either way.
+                    const float z32 = __fdividef((float)a.nv_magic * ((float)u1 - 0.5f), (float)u2);
+                    const float zz32 = 0.25f * z32 * z32;
+                    const float l32 = -__logf((float)u2);
+                    const float gap32 = zz32 - l32;
+                    if (fabsf(gap32) > 1e-4f * fmaxf(fabsf(zz32), fabsf(l32)) + 1e-5f) {
+                        acc = gap32 < 0.0f;
+                    } else {
+                        const double zx = __ddiv_rn(__dmul_rn(a.nv_magic, __dsub_rn(u1, 0.5)), u2);
+                        acc = __dmul_rn(__dmul_rn(zx, zx), 0.25) <= -log(u2);  // z*z/4.0 (exact scaling)
+                    }
                     if (acc) {
+                        const double z = __ddiv_rn(__dmul_rn(a.nv_magic, __dsub_rn(u1, 0.5)), u2);
                         d = __dmul_rn(scale[0], libm_exp(__dadd_rn(mu[0], __dmul_rn(z, sigma[0]))));
                         pend = false;
                     }

@@ -92,13 +92,13 @@ def test_run_batch_seeds_derived_on_device():
         assert r.order[i].tolist() == o.order.tolist()
 
 
-def test_chunked_seeding_over_65536_sims():
+def test_chunked_seeding_over_131072_sims():
     from paper_2108_02419_b200.race import Competitor, RaceConfig, UniformSteps
 
     cfg = RaceConfig(60.0, tuple(Competitor(f"c{i + 1}", UniformSteps(5.0, 9.0)) for i in range(3)))
-    n = 70_000
+    n = 140_000
     r = sim.simulate_batch(None, cfg, n, mode="mt", seed_master=3, records=True)
-    for i in (0, 65535, 65536, 69999):
+    for i in (0, 131071, 131072, 139999):
         o = oracle.run_race(cfg, oracle.derive_seed_run(3, i))
         assert r.order[i].tolist() == o.order.tolist() and r.final_positions[i].tolist() == o.final_positions.tolist()
     ob = oracle.batch(cfg, n, master=3, threads=8)
