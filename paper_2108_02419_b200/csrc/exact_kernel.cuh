@@ -27,6 +27,8 @@
 //           runs the Kinderman-Monahan loop of random.normalvariate alone, in index order.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "mt_stream.cuh"
 
@@ -123,28 +125,36 @@ exact_kernel(const LaunchArgs a) {
             __syncwarp();
         }
     };
-    // Take words [q+off, q+off+cnt) of this segment's stream (segment total T), twisting when the
-    // segment's reads cross the end of the block exactly where CPython's genrand_uint32 would.
-    auto mt_fetch = [&](int off, int cnt, int T, uint32_t* w) {
+    // Take C words [q+off, q+off+C) of this segment's stream for lanes with `act` (segment total T),
+    // twisting when the segment's reads cross the end of the block exactly where CPython's
+    // genrand_uint32 would.  Common case: one tempered LDS per word; the twist path is warp-uniform.
+    auto mt_fetch = [&](auto Cw, bool act, int off, int T, uint32_t* w) {
+        constexpr int C = decltype(Cw)::value;
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
+        for (int t = 0; t < C; ++t) {
             const int idx = q + off + t;
-            if (t < cnt && idx < kMtWords) w[t] = mt_temper(mt[idx]);
+            w[t] = mt_temper(mt[idx < kMtWords ? idx : kMtWords - 1]);
         }
         const bool need = lane_on && T > 0 && q + T > kMtWords;
-        if (__any_sync(0xffffffffu, need)) mt_twist(need);
+        if (__any_sync(0xffffffffu, need)) {
+            mt_twist(need);
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const int idx = q + off + t;
-            if (t < cnt && idx >= kMtWords) w[t] = mt_temper(mt[idx - kMtWords]);
+            for (int t = 0; t < C; ++t) {
+                const int idx = q + off + t;
+                if (act && idx >= kMtWords) w[t] = mt_temper(mt[idx - kMtWords]);
+            }
         }
         if (lane_on && T > 0) q = (q + T > kMtWords) ? q + T - kMtWords : q + T;
     };
+    using W2 = std::integral_constant<int, 2>;
+    using W4 = std::integral_constant<int, 4>;
     // One step draw per lane with `want`, in competitor-index order within each segment:
     // uniform(lo, hi) = lo + (hi - lo) * random(); scale * lognormvariate(mu, sigma) via the
     // Kinderman-Monahan loop of random.normalvariate (Lib/random.py).  Warp-uniform call.
     auto mt_draws = [&](bool want) -> double {
         double d = 1.0;
+        double ln_u1 = 0.0, ln_u2 = 1.0;  // the accepted Kinderman-Monahan pair of a lognormal lane
+        bool ln_draw = false;
         bool pend = want;
         while (__any_sync(0xffffffffu, pend)) {
             const unsigned Pm = __ballot_sync(0xffffffffu, pend) & segmask;
@@ -152,9 +162,9 @@ exact_kernel(const LaunchArgs a) {
             const unsigned stop = Lg & (0u - Lg);  // first pending lognormal competitor
             const unsigned run = stop ? (Pm & (stop - 1u)) : Pm;
             const bool in_run = (run >> lane) & 1u;
-            {
-                uint32_t w[4];
-                mt_fetch(2 * __popc(run & lt_mask), in_run ? 2 : 0, 2 * __popc(run), w);
+            if (__any_sync(0xffffffffu, run != 0u)) {
+                uint32_t w[2];
+                mt_fetch(W2{}, in_run, 2 * __popc(run & lt_mask), 2 * __popc(run), w);
                 if (in_run) {
                     d = __dadd_rn(lo[0], __dmul_rn(span[0], mt_random53(w[0], w[1])));
                     pend = false;
@@ -164,7 +174,7 @@ exact_kernel(const LaunchArgs a) {
             bool trying = stop != 0u;
             while (__any_sync(0xffffffffu, trying)) {
                 uint32_t w[4];
-                mt_fetch(0, (is_stop && trying) ? 4 : 0, trying ? 4 : 0, w);
+                mt_fetch(W4{}, is_stop && trying, 0, trying ? 4 : 0, w);
                 bool acc = false;
                 if (is_stop && trying) {
                     const double u1 = mt_random53(w[0], w[1]);
@@ -183,13 +193,20 @@ exact_kernel(const LaunchArgs a) {
                         acc = __dmul_rn(__dmul_rn(zx, zx), 0.25) <= -log(u2);  // z*z/4.0 (exact scaling)
                     }
                     if (acc) {
-                        const double z = __ddiv_rn(__dmul_rn(a.nv_magic, __dsub_rn(u1, 0.5)), u2);
-                        d = __dmul_rn(scale[0], libm_exp(__dadd_rn(mu[0], __dmul_rn(z, sigma[0]))));
+                        ln_u1 = u1;
+                        ln_u2 = u2;
+                        ln_draw = true;
                         pend = false;
                     }
                 }
                 if (__ballot_sync(0xffffffffu, acc) & segmask) trying = false;
             }
+        }
+        // lognormvariate's value for every accepted pair at once (the stream order is already fixed):
+        // z = NV*(u1-0.5)/u2, scale * exp(mu + z*sigma) with the host libm's exp
+        if (ln_draw) {
+            const double z = __ddiv_rn(__dmul_rn(a.nv_magic, __dsub_rn(ln_u1, 0.5)), ln_u2);
+            d = __dmul_rn(scale[0], libm_exp(__dadd_rn(mu[0], __dmul_rn(z, sigma[0]))));
         }
         return d;
     };
