@@ -21,6 +21,8 @@
 // marks racing lanes diverged; competitor-timesteps are summed from finish ticks at finalize.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace bbe {
@@ -265,23 +267,26 @@ native_kernel(const LaunchArgs a) {
         }
 
         // ---------------- 4 synchronous ticks ----------------
-#pragma unroll
-        for (int tj = 0; tj < kTicksPerBlock; ++tj) {
+        // The tick-limit check (race.py:381-386 / 402-404) can only fire in a block that reaches the
+        // limit; every other block runs the tick without it.
+        auto tick = [&](const int tj, auto check_limit) {
             bool racing[K];
-            const bool over = rt >= a.limit;  // race.py:381-386 / 402-404, before the advance
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 racing[k] = fin[k] == kRacing;
-                if (racing[k] && over) { fin[k] = kDiverged; racing[k] = false; }
+                if (decltype(check_limit)::value && racing[k] && rt >= a.limit) {
+                    fin[k] = kDiverged;
+                    racing[k] = false;
+                }
             }
 
             // ---- front runner: nearest key strictly ahead (race.py:244-264) ----
             float gap[K];
-            uint32_t fkey[K];
+            uint32_t fkey[K], kp[K];
 #pragma unroll
-            for (int k = 0; k < K; ++k) { gap[k] = CUDART_INF_F; fkey[k] = 0u; }
+            for (int k = 0; k < K; ++k) { gap[k] = CUDART_INF_F; fkey[k] = 0u; kp[k] = 0u; }
             if (scan) {
-                uint32_t kp[K], nk[K];
+                uint32_t nk[K];
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     kp[k] = __float_as_uint(pos[k]);
@@ -327,7 +332,21 @@ native_kernel(const LaunchArgs a) {
             float pf[K];
 #pragma unroll
             for (int k = 0; k < K; ++k) pf[k] = 0.0f;
-            if (__any_sync(0xffffffffu, any_bl)) {
+            if (K == 1 && __any_sync(0xffffffffu, any_bl)) {
+                // one competitor per lane: for each blocked lane b (warp-uniform loop), the lanes of b's
+                // segment holding b's front key vote; the lowest such lane is the lowest index
+                unsigned bm = __ballot_sync(0xffffffffu, bl[0]);
+                const uint32_t mine = racing[0] ? kp[0] : 0u;
+                while (bm) {
+                    const int b = __ffs(bm) - 1;
+                    bm &= bm - 1u;
+                    const uint32_t x = __shfl_sync(0xffffffffu, fkey[0], b);
+                    const unsigned sm = __shfl_sync(0xffffffffu, segmask, b);
+                    const unsigned m = __ballot_sync(0xffffffffu, mine == x) & sm;
+                    const float v = __shfl_sync(0xffffffffu, prev[0], __ffs(m) - 1);
+                    if (lane == b) pf[0] = v;
+                }
+            } else if (K > 1 && __any_sync(0xffffffffu, any_bl)) {
                 // front index: lowest competitor index holding the front key (slot-major, then lane)
                 int bi[K];
 #pragma unroll
@@ -375,6 +394,13 @@ native_kernel(const LaunchArgs a) {
                 }
             }
             rt += 1;
+        };
+        if (__any_sync(0xffffffffu, running && rt + kTicksPerBlock > a.limit)) {
+#pragma unroll
+            for (int tj = 0; tj < kTicksPerBlock; ++tj) tick(tj, std::true_type{});
+        } else {
+#pragma unroll
+            for (int tj = 0; tj < kTicksPerBlock; ++tj) tick(tj, std::false_type{});
         }
     }
 
