@@ -1,6 +1,6 @@
 // native_kernel.cuh -- the throughput kernel: Philox draws, FP32 race state (BBE_MODE_NATIVE).
 //
-// Same model as race_kernel.cuh (race.py:233-332 semantics, listed there); the arithmetic is FP32
+// Same model as exact_kernel.cuh (race.py:233-332 semantics, listed there); the arithmetic is FP32
 // and the random stream is Philox4x32-10, so outcomes are statistically -- not bitwise -- equal to
 // the reference's.  Everything else is the reference's rule set: synchronous ticks from
 // start-of-tick positions, nearest still-racing rival strictly ahead with the lowest-index tie rule,
@@ -26,6 +26,19 @@
 #include "common.cuh"
 
 namespace bbe {
+
+// Build-time variants for A/B measurement (tools/ab_build.sh); the defaults are the measured best
+// (C2 on B200: vote-based front recovery 0.474 ms, split limit check 0.443 ms, neither 0.437 ms;
+// 10 blocks/SM at 51 registers 0.483 ms).
+#ifndef BBE_VOTE_RECOVERY
+#define BBE_VOTE_RECOVERY 0
+#endif
+#ifndef BBE_SPLIT_LIMIT
+#define BBE_SPLIT_LIMIT 0
+#endif
+#ifndef BBE_NATIVE_MINBLOCKS_K1
+#define BBE_NATIVE_MINBLOCKS_K1 8
+#endif
 
 constexpr int32_t kRacing = 0x7fffffff;
 constexpr int32_t kDiverged = 0x7ffffffe;
@@ -61,7 +74,7 @@ __device__ __forceinline__ void lognormal_pair(uint32_t wa, uint32_t wb, float s
 }
 
 template <int K, int CH>
-__global__ void __launch_bounds__(kBlockThreads, K == 1 ? 8 : (K == 2 ? 5 : 3))
+__global__ void __launch_bounds__(kBlockThreads, K == 1 ? BBE_NATIVE_MINBLOCKS_K1 : (K == 2 ? 5 : 3))
 native_kernel(const LaunchArgs a) {
     extern __shared__ __align__(16) unsigned long long s_dyn[];
     const TallyLayout TL{a.n, a.perms};
@@ -332,7 +345,7 @@ native_kernel(const LaunchArgs a) {
             float pf[K];
 #pragma unroll
             for (int k = 0; k < K; ++k) pf[k] = 0.0f;
-            if (K == 1 && __any_sync(0xffffffffu, any_bl)) {
+            if (BBE_VOTE_RECOVERY && K == 1 && __any_sync(0xffffffffu, any_bl)) {
                 // one competitor per lane: for each blocked lane b (warp-uniform loop), the lanes of b's
                 // segment holding b's front key vote; the lowest such lane is the lowest index
                 unsigned bm = __ballot_sync(0xffffffffu, bl[0]);
@@ -346,7 +359,7 @@ native_kernel(const LaunchArgs a) {
                     const float v = __shfl_sync(0xffffffffu, prev[0], __ffs(m) - 1);
                     if (lane == b) pf[0] = v;
                 }
-            } else if (K > 1 && __any_sync(0xffffffffu, any_bl)) {
+            } else if ((K > 1 || !BBE_VOTE_RECOVERY) && __any_sync(0xffffffffu, any_bl)) {
                 // front index: lowest competitor index holding the front key (slot-major, then lane)
                 int bi[K];
 #pragma unroll
@@ -395,7 +408,7 @@ native_kernel(const LaunchArgs a) {
             }
             rt += 1;
         };
-        if (__any_sync(0xffffffffu, running && rt + kTicksPerBlock > a.limit)) {
+        if (!BBE_SPLIT_LIMIT || __any_sync(0xffffffffu, running && rt + kTicksPerBlock > a.limit)) {
 #pragma unroll
             for (int tj = 0; tj < kTicksPerBlock; ++tj) tick(tj, std::true_type{});
         } else {
