@@ -153,6 +153,10 @@ int bbe_derive_seeds(uint64_t master, int64_t first, int64_t count, uint64_t* ou
  * and, when `out` is not NULL, stores the values drawn (low word first, as CPython builds them). */
 int bbe_mt_getrandbits64(uint32_t* state625, int64_t count, uint64_t* out);
 
+/* The same advance with the position held separately (as CPython's RandomObject stores it:
+ * `int index; uint32_t state[624]`), writing only the first out_len values (out may be NULL). */
+int bbe_mt_advance64(uint32_t* state624, int32_t* pos, int64_t count, uint64_t* out, int64_t out_len);
+
 /* 1 if MT mode reproduces the host libm's exp() (used by random.lognormvariate) bit for bit: the
  * library found glibc's exp table in the loaded libm and verified its evaluation against exp().
  * 0 -> lognormal steps in MT mode may differ from the reference in the last bit. */

@@ -20,14 +20,56 @@ from .sim import _P, lib, simulate_batch
 M64 = (1 << 64) - 1
 
 
-def dry_run_seeds(rng, d: int, *, want: bool = True) -> np.ndarray | None:
-    """Advance ``rng`` by d ``getrandbits(64)`` calls (agents.py:164); return the d seeds if ``want``.
+_INPLACE_OK: bool | None = None
+_IDX_OFF, _STATE_OFF = 16, 20  # CPython RandomObject: PyObject_HEAD (16 B), int index, uint32_t state[624]
 
-    A ``random.Random`` is advanced in C on its MT19937 state; any other generator object falls back
-    to calling its own ``getrandbits`` (host bookkeeping only -- no simulation happens here).
+
+def _inplace_ok() -> bool:
+    """Whether this interpreter lays out random.Random as CPython's _randommodule.c RandomObject
+    (checked once against getstate(); the in-place path is used only if it matches exactly)."""
+    global _INPLACE_OK
+    if _INPLACE_OK is None:
+        try:
+            r = random.Random(12345)
+            r.random()
+            st = r.getstate()[1]
+            base = id(r)
+            idx = ctypes.c_int.from_address(base + _IDX_OFF).value
+            words = list((ctypes.c_uint32 * 624).from_address(base + _STATE_OFF))
+            _INPLACE_OK = idx == st[624] and words == list(st[:624])
+        except Exception:  # pragma: no cover - non-CPython
+            _INPLACE_OK = False
+    return _INPLACE_OK
+
+
+def _advance(rng, d: int, out: np.ndarray | None, out_len: int) -> bool:
+    """Advance a random.Random by d getrandbits(64) in place in C; False if not possible here."""
+    if type(rng) is not random.Random or not _inplace_ok():
+        return False
+    base = id(rng)
+    rc = lib().bbe_mt_advance64(ctypes.c_void_p(base + _STATE_OFF), ctypes.c_void_p(base + _IDX_OFF), d,
+                                None if out is None else out.ctypes.data_as(_P(ctypes.c_uint64)), out_len)
+    if rc != 0:
+        raise RuntimeError("bbe_mt_advance64 failed")
+    return True
+
+
+def dry_run_seeds(rng, d: int, *, want: bool = True, first_only: bool = False) -> np.ndarray | None:
+    """Advance ``rng`` by d ``getrandbits(64)`` calls (agents.py:164); return the d seeds if ``want``
+    (only the first one if ``first_only``).
+
+    A ``random.Random`` is advanced in C on its own MT19937 state -- in place when the interpreter's
+    object layout is the verified CPython one, else through getstate()/setstate(); any other
+    generator object falls back to its own ``getrandbits`` (host bookkeeping only).
     """
     if d <= 0:
         return np.zeros(0, np.uint64) if want else None
+    if want:
+        out = np.zeros(1 if first_only else d, np.uint64)
+        if _advance(rng, d, out, len(out)):
+            return out
+    elif _advance(rng, d, None, 0):
+        return None
     if type(rng) is random.Random:
         version, internal, gauss = rng.getstate()
         st = np.array(internal, dtype=np.uint32)
@@ -57,7 +99,7 @@ def rp_predict(state, config, d: int, rng, *, mode: str = "mt") -> tuple[float, 
     if mode == "mt":
         res = simulate_batch(state, config, d, mode="mt", seeds=dry_run_seeds(rng, d), ranks=False)
     else:
-        key = int(dry_run_seeds(rng, 1)[0])  # the first dry-run seed keys the Philox stream
-        dry_run_seeds(rng, d - 1, want=False)  # the other d-1 draws only advance the stream
+        # the first dry-run seed keys the Philox stream; the other d-1 draws only advance the stream
+        key = int(dry_run_seeds(rng, d, first_only=True)[0])
         res = simulate_batch(state, config, d, key, mode=mode, ranks=False)
     return tuple((int(w) + 1) / (d + n) for w in res.wins)

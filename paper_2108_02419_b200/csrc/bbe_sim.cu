@@ -343,6 +343,8 @@ int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_request* rq, int want
 
 extern "C" {
 
+uint32_t bbe_host_mt_getrandbits64(uint32_t* mt, uint32_t idx, int64_t count, uint64_t* out, int64_t out_len);
+
 int bbe_version(void) { return BBE_ABI_VERSION; }
 
 float bbe_last_kernel_ms(void) {
@@ -385,51 +387,14 @@ int bbe_device_info(int device, char* name64, int32_t* sm_count, int32_t* clock_
 
 int bbe_mt_getrandbits64(uint32_t* st, int64_t count, uint64_t* out) {
     if (!st || count < 0) return fail(BBE_EINVAL, "bad arguments");
-    uint32_t* mt = st;
-    uint32_t idx = st[624];
-    if (idx > 624) return fail(BBE_EINVAL, "MT19937 position out of range");
-    auto twist = [mt]() {  // regenerate the 624-word block, in place (MT19937)
-        auto mix = [](uint32_t a, uint32_t b, uint32_t m) {
-            const uint32_t y = (a & 0x80000000u) | (b & 0x7fffffffu);
-            return m ^ (y >> 1) ^ (0u - (y & 1u) & 0x9908b0dfu);
-        };
-        int k = 0;
-        for (; k < 624 - 397; ++k) mt[k] = mix(mt[k], mt[k + 1], mt[k + 397]);
-        for (; k < 623; ++k) mt[k] = mix(mt[k], mt[k + 1], mt[k + 397 - 624]);
-        mt[623] = mix(mt[623], mt[0], mt[396]);
-    };
-    auto temper = [](uint32_t y) {
-        y ^= y >> 11;
-        y ^= (y << 7) & 0x9d2c5680u;
-        y ^= (y << 15) & 0xefc60000u;
-        return y ^ (y >> 18);
-    };
-    int64_t words = 2 * count;
-    if (!out) {  // advance only: whole blocks need no tempering
-        while (words > 0) {
-            if (idx >= 624) { twist(); idx = 0; }
-            const int64_t take = std::min<int64_t>(words, 624 - idx);
-            idx += (uint32_t)take;
-            words -= take;
-        }
-    } else {
-        int64_t i = 0;
-        while (i < count) {
-            if (idx >= 623) {  // need two words; handle the block edge one word at a time
-                uint32_t w[2];
-                for (int j = 0; j < 2; ++j) {
-                    if (idx >= 624) { twist(); idx = 0; }
-                    w[j] = temper(mt[idx++]);
-                }
-                out[i++] = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
-                continue;
-            }
-            const int64_t pairs = std::min<int64_t>(count - i, (624 - idx) / 2);
-            for (int64_t p = 0; p < pairs; ++p, idx += 2)
-                out[i++] = (uint64_t)temper(mt[idx]) | ((uint64_t)temper(mt[idx + 1]) << 32);
-        }
-    }
-    st[624] = idx;
+    if (st[624] > 624) return fail(BBE_EINVAL, "MT19937 position out of range");
+    st[624] = bbe_host_mt_getrandbits64(st, st[624], count, out, count);  // host_mt.cpp
+    return BBE_OK;
+}
+
+int bbe_mt_advance64(uint32_t* state624, int32_t* pos, int64_t count, uint64_t* out, int64_t out_len) {
+    if (!state624 || !pos || count < 0 || *pos < 0 || *pos > 624) return fail(BBE_EINVAL, "bad arguments");
+    *pos = (int32_t)bbe_host_mt_getrandbits64(state624, (uint32_t)*pos, count, out, out ? out_len : 0);
     return BBE_OK;
 }
 

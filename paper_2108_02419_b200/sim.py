@@ -50,6 +50,7 @@ EXPORTED_SYMBOLS = (
     "bbe_param_bytes",
     "bbe_mt_getrandbits64",
     "bbe_mt_exp_exact",
+    "bbe_mt_advance64",
 )
 
 
@@ -138,6 +139,9 @@ def lib():
         L.bbe_mt_getrandbits64.argtypes = [_P(ctypes.c_uint32), ctypes.c_int64, _P(ctypes.c_uint64)]
         L.bbe_mt_getrandbits64.restype = ctypes.c_int
         L.bbe_mt_exp_exact.restype = ctypes.c_int
+        L.bbe_mt_advance64.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, _P(ctypes.c_uint64),
+                                       ctypes.c_int64]
+        L.bbe_mt_advance64.restype = ctypes.c_int
         L.bbe_param_bytes.argtypes = [ctypes.c_int32]
         L.bbe_param_bytes.restype = ctypes.c_int64
         L.bbe_last_error.restype = ctypes.c_char_p
@@ -168,8 +172,23 @@ class Packed:
     ids: tuple
 
 
+_last_packed: tuple = (None, None)  # (config object, Packed): bettors re-predict on one frozen config
+
+
 def pack_config(config) -> Packed:
-    """RaceConfig -> (bbe_race, bbe_competitor[n]).  Validates like RaceConfig.validate."""
+    """RaceConfig -> (bbe_race, bbe_competitor[n]).  Validates like RaceConfig.validate.
+
+    Race configs are frozen dataclasses, so the last packed config is reused when the same object
+    comes back (every bettor of a session predicts on the session's one config)."""
+    global _last_packed
+    if _last_packed[0] is config:
+        return _last_packed[1]
+    pk = _pack_config(config)
+    _last_packed = (config, pk)
+    return pk
+
+
+def _pack_config(config) -> Packed:
     validate_config(config)
     n = len(config.competitors)
     if n > MAX_COMPETITORS:

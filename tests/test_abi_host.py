@@ -64,6 +64,25 @@ def test_dry_run_seeds_match_sequential_getrandbits(d, pre):
     assert a.random() == b.random() and a.randrange(7) == b.randrange(7)  # same position afterwards
     c = random.Random(11)
     assert dry_run_seeds(c, d, want=False) is None and c.getstate() != random.Random(11).getstate()
+    e, f = random.Random(5), random.Random(5)
+    assert int(dry_run_seeds(e, d, first_only=True)[0]) == f.getrandbits(64)
+    for _ in range(d - 1):
+        f.getrandbits(64)
+    assert e.getstate() == f.getstate()
+
+
+def test_inplace_mt_layout_verified():
+    from paper_2108_02419_b200 import agents
+
+    assert agents._inplace_ok()  # CPython 3.12: RandomObject {PyObject_HEAD; int index; uint32_t state[624]}
+
+
+def test_non_random_generators_fall_back_to_getrandbits():
+    class Sys(random.Random):  # a subclass is not advanced in place
+        pass
+
+    a, b = Sys(3), random.Random(3)
+    assert [int(s) for s in dry_run_seeds(a, 9)] == [b.getrandbits(64) for _ in range(9)]
 
 
 def test_libm_exp_table_located_and_verified():
