@@ -1,0 +1,108 @@
+"""Edge cases the reference handles (degenerate fields, finished states, divergence,
+maximum sizes), through every mode of the kernel."""
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2108_02419_b200 import sim
+from paper_2108_02419_b200.race import (
+    Competitor,
+    LogNormalSteps,
+    RaceConfig,
+    RaceConfigError,
+    RaceState,
+    Responsiveness,
+    UniformSteps,
+)
+
+pytestmark = pytest.mark.gpu
+
+
+def _field(n, theta=0.0, L=80.0):
+    return RaceConfig(L, tuple(Competitor(f"c{i}", UniformSteps(2.0 + i % 3, 6.0 + i % 4), theta=theta * (i % 2))
+                               for i in range(n)))
+
+
+@pytest.mark.parametrize("mode", ["native", "mt"])
+def test_zero_sims_and_single_competitor(mode):
+    cfg = _field(1)
+    r = sim.simulate_batch(None, cfg, 0, 1, mode=mode, seed_master=1)
+    assert r.wins.tolist() == [0] and r.competitor_steps == 0
+    r = sim.simulate_batch(None, cfg, 1000, 1, mode=mode, seed_master=1, records=True)
+    assert r.wins.tolist() == [1000] and (r.order == 0).all()
+    if mode == "mt":
+        o = oracle.run_race(cfg, oracle.derive_seed_run(1, 7))
+        assert r.final_positions[7].tolist() == o.final_positions.tolist()
+
+
+@pytest.mark.parametrize("mode", ["native", "mt", "inject"])
+def test_state_already_finished(mode):
+    cfg = _field(3)
+    st = RaceState(12, [90.0, 85.0, 81.0], [5.0, 5.0, 5.0], [11, 12, 12])
+    kw = {}
+    if mode == "inject":
+        kw = dict(draws=np.zeros(0), draw_offsets=np.zeros(4, np.int64))
+    if mode == "mt":
+        kw = dict(seeds=np.arange(3, dtype=np.uint64))
+    r = sim.simulate_batch(st, cfg, 3, 5, mode=mode, records=True, **kw)
+    # finish tick first, then larger overshoot (L - pos smaller): c0 (11), then c1 (85 > 81), then c2
+    assert (r.order == [0, 1, 2]).all() and r.competitor_steps == 0
+    assert (r.finish_ticks == [11, 12, 12]).all()
+
+
+@pytest.mark.parametrize("mode", ["native", "mt"])
+def test_divergence_everywhere(mode):
+    cfg = RaceConfig(100.0, (Competitor("a", UniformSteps(1.0, 1.0)), Competitor("b", UniformSteps(1.0, 1.0))),
+                     tick_limit=10)
+    with pytest.raises(sim.SimDivergedError) as e:
+        sim.simulate_batch(None, cfg, 500, 1, mode=mode, seed_master=1, sim_offset=40)
+    assert e.value.sim_index == 40
+    st = RaceState(50, [10.0, 20.0], [1.0, 1.0], [None, None])
+    with pytest.raises(sim.SimDivergedError):
+        sim.simulate_batch(st, cfg, 5, 1, mode=mode, seeds=np.arange(5, dtype=np.uint64) if mode == "mt" else None)
+    # a limit that is exactly enough: 2 ticks from 98 with unit steps
+    ok = RaceConfig(100.0, cfg.competitors, tick_limit=2)
+    st2 = RaceState(50, [98.0, 98.5], [1.0, 1.0], [None, None])
+    r = sim.simulate_batch(st2, ok, 4, 1, mode=mode, seeds=np.arange(4, dtype=np.uint64) if mode == "mt" else None,
+                           records=True)
+    assert (r.finish_ticks == [52, 52]).all() and (r.order == [1, 0]).all()
+
+
+def test_negative_positions_are_shifted_not_misordered():
+    """Native mode keys positions by their float bits after an offset; a state with negative
+    positions must behave like the same state shifted (statistically) and order exactly."""
+    fixed = lambda v: UniformSteps(v, v)  # noqa: E731
+    cfg = RaceConfig(10.0, (Competitor("a", fixed(4.0), theta=3.0), Competitor("b", fixed(3.0))))
+    st = RaceState(0, [-5.0, -3.0], [2.0, 2.0], [None, None])
+    r = sim.simulate_batch(st, cfg, 16, 1, records=True)
+    o = oracle.simulate_from(st, cfg, 1)  # degenerate draws: the same race for any seed
+    assert (r.order == o.order.tolist()).all() and (r.finish_ticks == o.finish_ticks.tolist()).all()
+    assert (r.final_positions == o.final_positions.tolist()).all() and (r.blocked == o.blocked).all()
+
+
+@pytest.mark.parametrize("n", [31, 32, 33, 64, 97, 128])
+def test_large_fields_native_layouts(n):
+    cfg = _field(n, theta=1.5, L=60.0)
+    r = sim.simulate_batch(None, cfg, 20_000, 9, records=True)
+    assert int(r.wins.sum()) == 20_000 and (np.sort(r.order, axis=1) == np.arange(n)).all()
+    ref = oracle.batch(cfg, 4000, master=9, threads=8)
+    # mean race length in competitor-timesteps agrees with the reference's within 1 %
+    assert abs(r.competitor_steps / 20_000 - ref["ct"] / 4000) / (ref["ct"] / 4000) < 0.01
+
+
+def test_mt_rejects_fields_over_32():
+    with pytest.raises(RaceConfigError):
+        sim.simulate_batch(None, _field(33), 10, mode="mt", seed_master=1)
+
+
+def test_lognormal_zero_sigma_and_responsiveness_edges():
+    comps = (Competitor("a", LogNormalSteps(1.0, 0.0, 2.0)),
+             Competitor("b", UniformSteps(5.0, 6.0), responsiveness=Responsiveness(0.5, 2.0, 0.0)),
+             Competitor("c", UniformSteps(5.0, 6.0), responsiveness=Responsiveness(2.0, 0.5, 1.0)))
+    cfg = RaceConfig(50.0, comps)
+    seeds = oracle.rp_seeds(3, 500)
+    r = sim.simulate_batch(None, cfg, 500, mode="mt", seeds=seeds, records=True)
+    for i in (0, 1, 499):
+        o = oracle.run_race(cfg, int(seeds[i]))
+        assert r.final_positions[i].tolist() == o.final_positions.tolist()
