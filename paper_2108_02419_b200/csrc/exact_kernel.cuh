@@ -55,7 +55,8 @@ exact_kernel(const LaunchArgs a) {
     const unsigned segmask = lane_on ? ((W == 32 ? 0xffffffffu : ((1u << W) - 1u)) << base) : 0u;
     const unsigned lt_mask = (1u << lane) - 1u;
     uint32_t* const mt = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) +
-                         (warp * S + (lane_on ? seg : 0)) * kMtWords;  // MT: this segment's state
+                         (warp * S + (lane_on ? seg : 0)) * (kMtWords + kMtSideWords);  // MT: segment state
+    uint32_t* const side = mt + kMtWords;  // MT: unread words saved across an early twist
     __syncthreads();
 
     // ---- per-slot constants (the lane->competitor map is fixed for the kernel) ----
@@ -97,6 +98,7 @@ exact_kernel(const LaunchArgs a) {
     int32_t rt = 0;
     int64_t cursor = 0, cursor_end = 0;  // INJECT
     int q = kMtWords;                    // MT: CPython's position in the current 624-word block
+    int sp = 0, se = 0;                  // MT: unread words side[sp, se) precede mt[q, 624)
     bool running = false, diverged = false, bad = false;
 
     double pos[K], prev[K], pv[K];
@@ -125,29 +127,45 @@ exact_kernel(const LaunchArgs a) {
             __syncwarp();
         }
     };
-    // Take C words [q+off, q+off+C) of this segment's stream for lanes with `act` (segment total T),
-    // twisting when the segment's reads cross the end of the block exactly where CPython's
-    // genrand_uint32 would.  Common case: one tempered LDS per word; the twist path is warp-uniform.
-    auto mt_fetch = [&](auto Cw, bool act, int off, int T, uint32_t* w) {
-        constexpr int C = decltype(Cw)::value;
+    // The segment's unread stream is a window: side[sp, se) (words saved from the previous block)
+    // followed by mt[q, 624).  Before a round that may read up to 4W words, a window shorter than
+    // that is topped up: the unread words of the block move to `side` and the block is twisted in
+    // place -- early, but the stream is the same, since the twist reads the whole old block.
+    auto mt_window_fill = [&]() {
+        const bool low = running && lane_on && (se - sp) + (kMtWords - q) < 4 * W;
+        if (!__any_sync(0xffffffffu, low)) return;
+        const int keep = se - sp, tail = kMtWords - q;  // keep + tail < 4W: at most 4 words per lane
+        uint32_t carry[4];
+        int nc = 0;
 #pragma unroll
-        for (int t = 0; t < C; ++t) {
-            const int idx = q + off + t;
-            w[t] = mt_temper(mt[idx < kMtWords ? idx : kMtWords - 1]);
-        }
-        const bool need = lane_on && T > 0 && q + T > kMtWords;
-        if (__any_sync(0xffffffffu, need)) {
-            mt_twist(need);
-#pragma unroll
-            for (int t = 0; t < C; ++t) {
-                const int idx = q + off + t;
-                if (act && idx >= kMtWords) w[t] = mt_temper(mt[idx - kMtWords]);
+        for (int t = 0; t < 4; ++t) {
+            const int i = l + t * W;  // new side index
+            carry[t] = 0u;
+            if (low && i < keep + tail) {
+                carry[t] = i < keep ? side[sp + i] : mt[q + i - keep];
+                nc = t + 1;
             }
         }
-        if (lane_on && T > 0) q = (q + T > kMtWords) ? q + T - kMtWords : q + T;
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (t < nc) side[l + t * W] = carry[t];
+        mt_twist(low);  // starts and ends with __syncwarp
+        if (low) {
+            sp = 0;
+            se = keep + tail;
+            q = 0;
+        }
     };
-    using W2 = std::integral_constant<int, 2>;
-    using W4 = std::integral_constant<int, 4>;
+    auto mt_word = [&](int k) -> uint32_t {  // window offset k -> raw word
+        const int ns = se - sp;
+        return k < ns ? side[sp + k] : mt[min(q + k - ns, kMtWords - 1)];
+    };
+    auto mt_consume = [&](int c) {
+        const int ns = se - sp;
+        if (c <= ns) sp += c;
+        else { q += c - ns; sp = se = 0; }
+    };
     // One step draw per lane with `want`, in competitor-index order within each segment:
     // uniform(lo, hi) = lo + (hi - lo) * random(); scale * lognormvariate(mu, sigma) via the
     // Kinderman-Monahan loop of random.normalvariate (Lib/random.py).  Warp-uniform call.
@@ -156,27 +174,26 @@ exact_kernel(const LaunchArgs a) {
         double ln_u1 = 0.0, ln_u2 = 1.0;  // the accepted Kinderman-Monahan pair of a lognormal lane
         bool ln_draw = false;
         bool pend = want;
+        // Speculative rounds: every pending competitor takes its words at the offset it would have if
+        // each pending lognormal draw accepted its next Kinderman-Monahan trial (2 words per uniform
+        // draw, 4 per trial).  Draws up to the first rejected trial in index order are then final;
+        // the rejected one consumed its 4 words and retries first in the next round.
         while (__any_sync(0xffffffffu, pend)) {
-            const unsigned Pm = __ballot_sync(0xffffffffu, pend) & segmask;
-            const unsigned Lg = __ballot_sync(0xffffffffu, pend && lognorm[0]) & segmask;
-            const unsigned stop = Lg & (0u - Lg);  // first pending lognormal competitor
-            const unsigned run = stop ? (Pm & (stop - 1u)) : Pm;
-            const bool in_run = (run >> lane) & 1u;
-            if (__any_sync(0xffffffffu, run != 0u)) {
-                uint32_t w[2];
-                mt_fetch(W2{}, in_run, 2 * __popc(run & lt_mask), 2 * __popc(run), w);
-                if (in_run) {
-                    d = __dadd_rn(lo[0], __dmul_rn(span[0], mt_random53(w[0], w[1])));
-                    pend = false;
-                }
+            mt_window_fill();
+            const int need = pend ? (lognorm[0] ? 4 : 2) : 0;
+            int incl = need;  // inclusive prefix sum over the segment's lanes, in index order
+#pragma unroll
+            for (int o = 1; o < kWarp; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (l >= o) incl += v;
             }
-            const bool is_stop = (stop >> lane) & 1u;
-            bool trying = stop != 0u;
-            while (__any_sync(0xffffffffu, trying)) {
-                uint32_t w[4];
-                mt_fetch(W4{}, is_stop && trying, 0, trying ? 4 : 0, w);
-                bool acc = false;
-                if (is_stop && trying) {
+            const int off = incl - need;
+            uint32_t w[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) w[t] = mt_temper(mt_word(off + t));
+            bool ok = true;
+            if (pend && lognorm[0]) {
+                {
                     const double u1 = mt_random53(w[0], w[1]);
                     const double u2 = __dsub_rn(1.0, mt_random53(w[2], w[3]));
                     // accept iff z*z/4 <= -log(u2) (Lib/random.py normalvariate).  Decide in FP32 when
@@ -186,21 +203,31 @@ exact_kernel(const LaunchArgs a) {
                     const float zz32 = 0.25f * z32 * z32;
                     const float l32 = -__logf((float)u2);
                     const float gap32 = zz32 - l32;
+                    bool acc;
                     if (fabsf(gap32) > 1e-4f * fmaxf(fabsf(zz32), fabsf(l32)) + 1e-5f) {
                         acc = gap32 < 0.0f;
                     } else {
                         const double zx = __ddiv_rn(__dmul_rn(a.nv_magic, __dsub_rn(u1, 0.5)), u2);
                         acc = __dmul_rn(__dmul_rn(zx, zx), 0.25) <= -log(u2);  // z*z/4.0 (exact scaling)
                     }
-                    if (acc) {
-                        ln_u1 = u1;
-                        ln_u2 = u2;
-                        ln_draw = true;
-                        pend = false;
-                    }
+                    ok = acc;
+                    ln_u1 = u1;
+                    ln_u2 = u2;
                 }
-                if (__ballot_sync(0xffffffffu, acc) & segmask) trying = false;
             }
+            const unsigned bad = __ballot_sync(0xffffffffu, pend && !ok) & segmask;
+            const unsigned first_bad = bad & (0u - bad);
+            const bool done = pend && (first_bad == 0u || (1u << lane) < first_bad);
+            // words consumed this round: up to and including the rejected trial, or all of them
+            const int last = lane_on ? base + W - 1 : lane;
+            const int used_all = __shfl_sync(0xffffffffu, incl, last);
+            const int used_bad = __shfl_sync(0xffffffffu, off, first_bad ? __ffs(first_bad) - 1 : lane) + 4;
+            if (done) {
+                if (lognorm[0]) ln_draw = true;
+                else d = __dadd_rn(lo[0], __dmul_rn(span[0], mt_random53(w[0], w[1])));
+                pend = false;
+            }
+            if (lane_on && running) mt_consume(first_bad ? used_bad : used_all);
         }
         // lognormvariate's value for every accepted pair at once (the stream order is already fixed):
         // z = NV*(u1-0.5)/u2, scale * exp(mu + z*sigma) with the host libm's exp
@@ -244,6 +271,7 @@ exact_kernel(const LaunchArgs a) {
             if (MODE == MT && running) {
                 for (int i = l; i < kMtWords; i += W) mt[i] = a.mt_states[s * kMtWords + i];
                 q = kMtWords;  // random.Random(seed): the first draw twists
+                sp = se = 0;
             }
         }
         if (MODE == MT) __syncwarp();

@@ -36,6 +36,9 @@ namespace bbe {
 #ifndef BBE_SPLIT_LIMIT
 #define BBE_SPLIT_LIMIT 0
 #endif
+#ifndef BBE_SPREAD_TAIL
+#define BBE_SPREAD_TAIL 1
+#endif
 #ifndef BBE_NATIVE_MINBLOCKS_K1
 #define BBE_NATIVE_MINBLOCKS_K1 8
 #endif
@@ -133,7 +136,12 @@ native_kernel(const LaunchArgs a) {
 
     // ---- segment bookkeeping ----
     const int64_t segs_total = (int64_t)gridDim.x * kWarpsPerBlock * S;
-    int64_t s = lane_on ? ((int64_t)blockIdx.x * kWarpsPerBlock + warp) * S + seg : a.n_sims;
+    // Segment slot -> first sim.  Slots are numbered block-fastest, so the sims of the last, partial
+    // round land on one segment in each of many blocks (spread over every SM) instead of filling
+    // the first few blocks and leaving most SMs idle at the tail.
+    const int64_t slot = BBE_SPREAD_TAIL ? (int64_t)(warp * S + seg) * gridDim.x + blockIdx.x
+                                         : ((int64_t)blockIdx.x * kWarpsPerBlock + warp) * S + seg;
+    int64_t s = lane_on ? slot : a.n_sims;
     int32_t rt = 0;
     bool running = false;
 
