@@ -111,20 +111,30 @@ exact_kernel(const LaunchArgs a) {
     // ---- MT19937 stream helpers (warp-uniform calls) ----
     // Regenerate this segment's block in place (MT19937 twist), W lanes per chunk; segments that do
     // not need it idle through the loop.  W <= 32 < 227 keeps every "new" dependency in an earlier chunk.
+    // All 32 lanes of the warp twist one needing segment at a time (20 chunks of 32 words), so a
+    // segment's twist costs the same whether or not its warp-mates need one.
+    uint32_t* const warp_mt = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) +
+                              warp * S * (kMtWords + kMtSideWords);
     auto mt_twist = [&](bool need) {
+        unsigned todo = __ballot_sync(0xffffffffu, need && l == 0);  // one bit per needing segment
         __syncwarp();
-        for (int c0 = 0; c0 < kMtWords; c0 += W) {
-            const int i = c0 + l;
-            const bool act = need && i < kMtWords;
-            uint32_t x = 0, y = 0, m = 0;
-            if (act) {
-                x = mt[i];
-                y = mt[i + 1 < kMtWords ? i + 1 : 0];
-                m = mt[i < kMtWords - kMtM ? i + kMtM : i + kMtM - kMtWords];
+        while (todo) {
+            const int leader = __ffs(todo) - 1;
+            todo &= todo - 1u;
+            uint32_t* const t = warp_mt + (leader / W) * (kMtWords + kMtSideWords);
+            for (int c0 = 0; c0 < kMtWords; c0 += kWarp) {
+                const int i = c0 + lane;
+                const bool act = i < kMtWords;
+                uint32_t x = 0, y = 0, m = 0;
+                if (act) {
+                    x = t[i];
+                    y = t[i + 1 < kMtWords ? i + 1 : 0];
+                    m = t[i < kMtWords - kMtM ? i + kMtM : i + kMtM - kMtWords];
+                }
+                __syncwarp();
+                if (act) t[i] = mt_mix(x, y, m);
+                __syncwarp();
             }
-            __syncwarp();
-            if (act) mt[i] = mt_mix(x, y, m);
-            __syncwarp();
         }
     };
     // The segment's unread stream is a window: side[sp, se) (words saved from the previous block)
