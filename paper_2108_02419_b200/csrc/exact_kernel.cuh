@@ -57,6 +57,14 @@ exact_kernel(const LaunchArgs a) {
     uint32_t* const mt = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) +
                          (warp * S + (lane_on ? seg : 0)) * (kMtWords + kMtSideWords);  // MT: segment state
     uint32_t* const side = mt + kMtWords;  // MT: unread words saved across an early twist
+    // start-of-tick positions, per warp: [parity][slot][segment * WP2 + lane-in-segment], pads -inf
+    const int WP2 = (W + 1) & ~1;
+    double* const xrows = reinterpret_cast<double*>(
+        reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) +
+        (MODE == MT ? kWarpsPerBlock * S * (kMtWords + kMtSideWords) : 0)) + warp * 2 * K * kXSlot;
+    for (int i = lane; i < 2 * K * kXSlot; i += kWarp) xrows[i] = -CUDART_INF;
+    const int xseg = lane_on ? seg * WP2 : 0;
+    double* const xw = xrows + (lane_on ? seg * WP2 + l : kXSlot - 1);
     __syncthreads();
 
     // ---- per-slot constants (the lane->competitor map is fixed for the kernel) ----
@@ -405,6 +413,7 @@ exact_kernel(const LaunchArgs a) {
         if (!__any_sync(0xffffffffu, running)) break;
 
         // ---------------- 4 synchronous ticks -------------------------------------------------------
+        __syncwarp();  // position rows: the previous block's reads precede this block's writes
         for (int tj = 0; tj < kTicksPerBlock; ++tj) {
             bool any_racing = false;
 #pragma unroll
@@ -421,25 +430,37 @@ exact_kernel(const LaunchArgs a) {
             }
 
             // ---- front runner (race.py:244-264): gap = p_i - p_c, strict compares in index order ----
+            // Rounding is monotonic, so the reference's smallest gap min_i fl(p_i - p_c) over rivals
+            // strictly ahead equals fl(min_i p_i - p_c): a positional min over the segment's start-of-tick
+            // positions (published to shared memory, finished rivals as -inf) gives the exact gap.
+            // Which rival holds it matters only for a blocked step; that index is found below with the
+            // reference's own gap arithmetic (equal gaps -> lowest index).
             double gap[K];
             int bi[K];
 #pragma unroll
             for (int k = 0; k < K; ++k) { gap[k] = CUDART_INF; bi[k] = 0; }
+            double* const prow = xrows + (tj & 1) * K * kXSlot;
             if (a.scan) {
 #pragma unroll
+                for (int k = 0; k < K; ++k) xw[(tj & 1) * K * kXSlot + k * kXSlot] = pv[k];
+                __syncwarp();
+                double best[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) best[k] = CUDART_INF;
+#pragma unroll
                 for (int kk = 0; kk < K; ++kk) {
-#pragma unroll 2
-                    for (int j = 0; j < W; ++j) {
-                        const double pr = shfl(pv[kk], base + j);
+                    const double2* r2 = reinterpret_cast<const double2*>(prow + kk * kXSlot + xseg);
+                    for (int j = 0; j < WP2 / 2; ++j) {
+                        const double2 v = r2[j];
 #pragma unroll
                         for (int k = 0; k < K; ++k) {
-                            const double g = __dsub_rn(pr, pos[k]);
-                            const bool t = (g > 0.0) & (g < gap[k]);
-                            gap[k] = t ? g : gap[k];
-                            bi[k] = t ? (kk << 5) | j : bi[k];
+                            best[k] = fmin(best[k], v.x > pos[k] ? v.x : CUDART_INF);
+                            best[k] = fmin(best[k], v.y > pos[k] ? v.y : CUDART_INF);
                         }
                     }
                 }
+#pragma unroll
+                for (int k = 0; k < K; ++k) gap[k] = best[k] < CUDART_INF ? __dsub_rn(best[k], pos[k]) : CUDART_INF;
             }
 
             // ---- step resolution (race.py:267-274) ----
@@ -455,6 +476,18 @@ exact_kernel(const LaunchArgs a) {
 #pragma unroll
             for (int k = 0; k < K; ++k) pf[k] = 0.0;
             if (__any_sync(0xffffffffu, any_blocked)) {
+                // the front: lowest index i (slot-major, then lane) with p_i > p_c and
+                // fl(p_i - p_c) == gap -- race.py:244-264 verbatim, scanned from the top index down
+#pragma unroll
+                for (int kk = K - 1; kk >= 0; --kk) {
+                    const double* r = prow + kk * kXSlot + xseg;
+                    for (int j = W - 1; j >= 0; --j) {
+                        const double pr = r[j];
+#pragma unroll
+                        for (int k = 0; k < K; ++k)
+                            if (pr > pos[k] && __dsub_rn(pr, pos[k]) == gap[k]) bi[k] = (kk << 5) | j;
+                    }
+                }
 #pragma unroll
                 for (int kk = 0; kk < K; ++kk) {
 #pragma unroll
