@@ -16,15 +16,20 @@
 //
 // Mapping: one sim per SEGMENT of W consecutive lanes, competitor c = k*W + l in lane l, slot k;
 // S = 32/W sims per warp; persistent grid, a finished segment takes its next sim at a 4-tick block
-// boundary.  Rival positions are read with __shfl_sync; the front-runner scan is the reference's
-// gap arithmetic with strict compares in index order (lowest-index tie rule).
+// boundary.  Front runner: rounding is monotonic, so the reference's smallest gap
+// min_i fl(p_i - p_c) equals fl(min_i p_i - p_c); each lane takes a positional min over its
+// segment's start-of-tick positions (a shared-memory row per tick parity, 128-bit loads).  The
+// index of the rival holding that gap -- needed only for a blocked step -- is found with the
+// reference's own gap arithmetic and lowest-index rule.
 //
 // Draw sources:
 //   INJECT  recorded reference draws (CSR per sim); a free slot's offset in the tick = popc of free
 //           slots of lower competitor index in its segment -- the reference's consumption order.
-//   MT      per-sim CPython MT19937 (mt_stream.cuh) in shared memory: uniform draws of a run of free
-//           competitors are taken in parallel (2 words each, offsets by popc); a lognormal competitor
-//           runs the Kinderman-Monahan loop of random.normalvariate alone, in index order.
+//   MT      per-sim CPython MT19937 (mt_stream.cuh) in shared memory.  Speculative rounds: every
+//           pending competitor reads its words at the offset it would have if each pending lognormal
+//           draw accepted its next Kinderman-Monahan trial; draws before the first rejection are
+//           final.  The whole warp twists a segment's block when its unread window runs low (the
+//           unread tail moves to a side buffer first, so early twists leave the stream unchanged).
 #pragma once
 
 #include <type_traits>
@@ -121,10 +126,9 @@ exact_kernel(const LaunchArgs a) {
     int64_t first_div = INT64_MAX, first_bad = INT64_MAX;
 
     // ---- MT19937 stream helpers (warp-uniform calls) ----
-    // Regenerate this segment's block in place (MT19937 twist), W lanes per chunk; segments that do
-    // not need it idle through the loop.  W <= 32 < 227 keeps every "new" dependency in an earlier chunk.
-    // All 32 lanes of the warp twist one needing segment at a time (20 chunks of 32 words), so a
-    // segment's twist costs the same whether or not its warp-mates need one.
+    // Regenerate a segment's block in place (MT19937 twist): all 32 lanes of the warp twist one
+    // needing segment at a time, 20 chunks of 32 words (32 < 227 keeps every "new" dependency in an
+    // earlier chunk), so a segment's twist costs the same whether or not its warp-mates need one.
     uint32_t* const warp_mt = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) +
                               warp * S * (kMtWords + kMtSideWords);
     auto mt_twist = [&](bool need) {
