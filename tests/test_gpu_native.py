@@ -208,3 +208,37 @@ def test_simulate_sharded_single_rank_matches_batch():
     r = sim.simulate_batch(st, cfg, 50_000, 3)
     assert (t.wins == r.wins).all() and (t.ranks == r.ranks).all()
     assert t.competitor_steps == r.competitor_steps and t.first_diverged == -1
+
+
+def test_criterion_10_calibration_gpu_vs_reference():
+    """tests/test_acceptance.py:394-424 with the GPU on one side: the chi-square PMF comparison of a
+    native-mode batch against a reference (oracle) batch of the same config rejects at most 5/100
+    times at alpha = 0.01, and detects the swapped step law at least 95/100 times (R = 300)."""
+    import itertools
+
+    base = tuple(Competitor(f"c{i + 1}", UniformSteps(10.0, 20.0)) for i in range(3))
+    cfg = RaceConfig(150.0, base)
+    swapped = RaceConfig(150.0, base[:2] + (Competitor("c3", UniformSteps(1.0, 25.0)),))
+    keys = list(itertools.permutations(range(3)))
+
+    def ref_counts(seed):
+        counts = np.zeros(6, np.int64)
+        for i in range(300):
+            counts[keys.index(tuple(oracle.run_race(cfg, oracle.derive_seed_run(seed, i)).order.tolist()))] += 1
+        return counts
+
+    def chi2_p(a, b):
+        cols = [i for i in range(6) if a[i] + b[i] > 0]
+        if len(cols) < 2:
+            return 1.0
+        return chi2_contingency([[a[i] for i in cols], [b[i] for i in cols]], correction=False)[1]
+
+    false_rejects = detections = 0
+    for trial in range(100):
+        ref = ref_counts(1000 + trial)
+        same = sim.simulate_batch(None, cfg, 300, 5000 + trial, perms=True).perms.astype(np.int64)
+        other = sim.simulate_batch(None, swapped, 300, 9000 + trial, perms=True).perms.astype(np.int64)
+        false_rejects += chi2_p(ref, same) < ALPHA
+        detections += chi2_p(ref, other) < ALPHA
+    assert false_rejects <= 5, false_rejects
+    assert detections >= 95, detections
