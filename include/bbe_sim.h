@@ -130,6 +130,14 @@ typedef struct {
 int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_state* state,
                  const bbe_request* req, bbe_result* out);
 
+/* bbe_simulate split in two: _begin validates, uploads and enqueues everything and returns at once;
+ * _end waits and fills `out`.  Host work between the two (e.g. advancing the bettor's stream past
+ * the other d-1 dry-run seeds) overlaps the kernel.  One call in flight per device; the host
+ * buffers of `out` (and the request's inputs) must stay valid until _end returns. */
+int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const bbe_state* state,
+                       const bbe_request* req, bbe_result* out);
+int bbe_simulate_end(bbe_result* out);
+
 /* Device-resident variant.  All pointers in req/state are HOST except draws/draw_offsets/seeds,
  * which must be DEVICE pointers; per-sim output pointers in `dev_out` are DEVICE pointers or NULL.
  * Tallies are ADDED into d_tally (device, bbe_tally_len(n) u64, layout below) on `stream`

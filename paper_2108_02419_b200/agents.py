@@ -15,7 +15,7 @@ import random
 
 import numpy as np
 
-from .sim import _P, lib, simulate_batch
+from .sim import _P, lib, simulate_batch, simulate_batch_begin
 
 M64 = (1 << 64) - 1
 
@@ -99,7 +99,10 @@ def rp_predict(state, config, d: int, rng, *, mode: str = "mt") -> tuple[float, 
     if mode == "mt":
         res = simulate_batch(state, config, d, mode="mt", seeds=dry_run_seeds(rng, d), ranks=False)
     else:
-        # the first dry-run seed keys the Philox stream; the other d-1 draws only advance the stream
-        key = int(dry_run_seeds(rng, d, first_only=True)[0])
-        res = simulate_batch(state, config, d, key, mode=mode, ranks=False)
+        # the first dry-run seed keys the Philox stream; the other d-1 draws only advance the
+        # bettor's stream, which the host does while the kernel runs
+        key = int(dry_run_seeds(rng, 1)[0])
+        pending = simulate_batch_begin(state, config, d, key, mode=mode, ranks=False)
+        dry_run_seeds(rng, d - 1, want=False)
+        res = pending.end()
     return tuple((int(w) + 1) / (d + n) for w in res.wins)

@@ -80,6 +80,11 @@ struct DevCtx {
     DevBuf d_seeds, d_mt_states, d_mt_scratch;  // MT mode
     DevBuf d_traj;                               // trajectories (positions, previous steps)
     bool mt_table = false;                       // c_mt_init uploaded on this device
+    // the call in flight between bbe_simulate_begin and bbe_simulate_end
+    bool pending = false;
+    bbe_result* pend_out = nullptr;
+    int pend_n = 0, pend_nperm = 0, pend_K = 0;
+    int64_t pend_ns = 0, pend_limit = 0;
 };
 
 std::mutex g_ctx_mu;
@@ -635,14 +640,15 @@ static int build_args(const Plan& pl, const bbe_race* race, const bbe_state* st,
     return BBE_OK;
 }
 
-int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, const bbe_request* rq,
-                 bbe_result* out) {
+int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, const bbe_request* rq,
+                       bbe_result* out) {
     int rc = validate(race, comps, st, rq);
     if (rc) return rc;
     if (!out || !out->wins) return fail(BBE_EINVAL, "result needs a wins buffer");
     DevCtx* ctx = nullptr;
     if ((rc = get_ctx(&ctx))) return rc;
     std::lock_guard<std::mutex> guard(ctx->mu);
+    if (ctx->pending) return fail(BBE_EINVAL, "a call is already in flight on this device (bbe_simulate_end first)");
     const int n = race->n;
     const int64_t ns = rq->n_sims;
     Plan pl;
@@ -724,8 +730,27 @@ int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_st
         BBE_CK(cudaMemcpyAsync(out->traj_positions, dev.traj_positions, traj_elems * sizeof(double), cudaMemcpyDeviceToHost, s));
         BBE_CK(cudaMemcpyAsync(out->traj_prev_steps, dev.traj_prev_steps, traj_elems * sizeof(double), cudaMemcpyDeviceToHost, s));
     }
-    BBE_CK(cudaStreamSynchronize(s));
+    ctx->pending = true;
+    ctx->pend_out = out;
+    ctx->pend_n = n;
+    ctx->pend_nperm = pl.nperm;
+    ctx->pend_K = pl.K;
+    ctx->pend_ns = ns;
+    ctx->pend_limit = race->tick_limit;
+    return BBE_OK;
+}
 
+int bbe_simulate_end(bbe_result* out) {
+    DevCtx* ctx = nullptr;
+    int rc;
+    if ((rc = get_ctx(&ctx))) return rc;
+    std::lock_guard<std::mutex> guard(ctx->mu);
+    if (!ctx->pending || ctx->pend_out != out) return fail(BBE_EINVAL, "no call in flight for this result");
+    ctx->pending = false;
+    BBE_CK(cudaStreamSynchronize(ctx->stream));
+    const int n = ctx->pend_n;
+    const int64_t ns = ctx->pend_ns;
+    struct { int nperm, K; } pl{ctx->pend_nperm, ctx->pend_K};
     const uint64_t* T = (const uint64_t*)ctx->h_tally.p;
     TallyLayout TL{n, pl.nperm};
     std::memcpy(out->wins, T + TL.wins(), n * sizeof(uint64_t));
@@ -739,11 +764,17 @@ int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_st
     if (ns) cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
     out->kernel_ms = ms;
     out->lanes_per_slot = pl.K;
-    if (T[TL.n_div()]) return fail(BBE_EDIVERGED, "race exceeded tick_limit=" + std::to_string(race->tick_limit) +
+    if (T[TL.n_div()]) return fail(BBE_EDIVERGED, "race exceeded tick_limit=" + std::to_string(ctx->pend_limit) +
                                                       " in sim " + std::to_string(out->first_diverged));
     if (T[TL.n_bad()]) return fail(BBE_EDRAWS, "injected draw stream under/over-consumed in sim " +
                                                    std::to_string(out->first_bad_draws));
     return BBE_OK;
+}
+
+int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, const bbe_request* rq,
+                 bbe_result* out) {
+    const int rc = bbe_simulate_begin(race, comps, st, rq, out);
+    return rc ? rc : bbe_simulate_end(out);
 }
 
 int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, const bbe_request* rq,

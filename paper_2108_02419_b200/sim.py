@@ -38,6 +38,8 @@ M64 = (1 << 64) - 1
 
 EXPORTED_SYMBOLS = (
     "bbe_simulate",
+    "bbe_simulate_begin",
+    "bbe_simulate_end",
     "bbe_simulate_async",
     "bbe_tally_len",
     "bbe_tally_offset",
@@ -126,6 +128,10 @@ def lib():
         L = ctypes.CDLL(LIB_PATH)
         L.bbe_simulate.argtypes = [_P(BbeRace), _P(BbeCompetitor), _P(BbeState), _P(BbeRequest), _P(BbeResult)]
         L.bbe_simulate.restype = ctypes.c_int
+        L.bbe_simulate_begin.argtypes = L.bbe_simulate.argtypes
+        L.bbe_simulate_begin.restype = ctypes.c_int
+        L.bbe_simulate_end.argtypes = [_P(BbeResult)]
+        L.bbe_simulate_end.restype = ctypes.c_int
         L.bbe_simulate_async.argtypes = [_P(BbeRace), _P(BbeCompetitor), _P(BbeState), _P(BbeRequest),
                                          _P(BbeResult), ctypes.c_void_p, ctypes.c_void_p]
         L.bbe_simulate_async.restype = ctypes.c_int
@@ -293,6 +299,7 @@ def simulate_batch(
     winners: bool = False,
     trajectory_ticks: int = 0,
     lanes_per_slot: int = 0,
+    _defer: bool = False,
 ) -> SimResult:
     """Run ``n_sims`` independent continuations of ``state`` (or races from the start line when
     ``state is None``) and return tallies.
@@ -348,15 +355,38 @@ def simulate_batch(
                     _ptr(winner, ctypes.c_int32), _ptr(order, ctypes.c_int32), _ptr(fin, ctypes.c_int64),
                     _ptr(fpos, ctypes.c_double), _ptr(blk, ctypes.c_int64), _ptr(used, ctypes.c_int64),
                     0, 0, -1, -1, 0.0, 0, _ptr(tpos, ctypes.c_double), _ptr(tprev, ctypes.c_double), cap, 0)
-    rc = lib().bbe_simulate(ctypes.byref(pk.race), pk.comps, ctypes.byref(st), ctypes.byref(req), ctypes.byref(res))
-    del keep
+    rc = lib().bbe_simulate_begin(ctypes.byref(pk.race), pk.comps, ctypes.byref(st), ctypes.byref(req),
+                                  ctypes.byref(res))
     if rc != BBE_OK:
         _raise(rc, res)
-    out = SimResult(pk.ids, n_sims, wins, rk, pm, winner, order, fin, fpos, blk, used,
-                    int(res.competitor_steps), int(res.blocked_steps), float(res.kernel_ms),
-                    int(res.lanes_per_slot))
-    out.traj_positions, out.traj_prev_steps = tpos, tprev
-    return out
+    pending = PendingSim(res, (pk, st, keep, req, draws, draw_offsets, seeds),
+                         lambda r: SimResult(pk.ids, n_sims, wins, rk, pm, winner, order, fin, fpos, blk, used,
+                                             int(r.competitor_steps), int(r.blocked_steps), float(r.kernel_ms),
+                                             int(r.lanes_per_slot), tpos, tprev))
+    return pending if _defer else pending.end()
+
+
+class PendingSim:
+    """A batch enqueued on the GPU (``bbe_simulate_begin``); ``end()`` waits and returns the result.
+    Host work done before ``end()`` overlaps the kernel."""
+
+    def __init__(self, res, keep, build):
+        self._res, self._keep, self._build = res, keep, build
+        self._done = None
+
+    def end(self) -> SimResult:
+        if self._done is None:
+            rc = lib().bbe_simulate_end(ctypes.byref(self._res))
+            self._keep = None
+            if rc != BBE_OK:
+                _raise(rc, self._res)
+            self._done = self._build(self._res)
+        return self._done
+
+
+def simulate_batch_begin(*args, **kwargs) -> PendingSim:
+    """``simulate_batch`` that returns as soon as the work is enqueued (see PendingSim)."""
+    return simulate_batch(*args, _defer=True, **kwargs)
 
 
 # -- reference-shaped single-race entry points ---------------------------------------------------
