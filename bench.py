@@ -230,6 +230,18 @@ def sweep_configs(args, torch, sim):
         out[name] = {"sims": n_sims, "ms": ms, "races_per_s": n_sims / (ms / 1e3), "ct_per_s": ct / (ms / 1e3),
                      "ct_per_race": ct / n_sims, "ops_per_ct": ops,
                      "issue_roofline_frac": ct * ops / (ms / 1e3) / 37.22e12, "scan_needed": scan}
+    # C4: 100 RP bettors, every wake (1 s period, 1 s jitter) predicting with d dry runs on the live
+    # race; all wakes that share a race state run as one launch (session dispatch batching).  The
+    # host exchange loop (order book, matching) is not part of this path and is not run.
+    from paper_2108_02419_b200.session import run_dry_run_session
+
+    for mode, d in (("mt", 1000), ("native", 1000), ("native", 10000)):
+        run_dry_run_session(derby5, n_agents=100, d=d, master_seed=20260818, opening_period=5.0, mode=mode)
+        r = run_dry_run_session(derby5, n_agents=100, d=d, master_seed=20260818, opening_period=5.0, mode=mode)
+        out[f"C4_session_100_rp_bettors_d{d}_{mode}"] = {
+            "predictions": len(r.predictions), "launches": r.launches, "sims": r.sims, "seconds": r.seconds,
+            "races_per_s_end_to_end": r.sims_per_second, "race_ticks": r.ticks,
+            "note": "live race + wake schedule + batched predictions; exchange loop not run"}
     return out
 
 
