@@ -271,22 +271,27 @@ void philox_round_keys(uint64_t seed, uint32_t* rk) {
 
 typedef void (*KernelFn)(LaunchArgs);
 
-template <int K>
+template <int K, bool SCAN>
 KernelFn native_for_ch(int ch) {
     switch (ch) {
-        case 1: return native_kernel<K, 1>;
-        case 2: return native_kernel<K, 2>;
-        case 3: return native_kernel<K, 3>;
-        case 4: return native_kernel<K, 4>;
-        case 5: return native_kernel<K, 5>;
-        case 6: return native_kernel<K, 6>;
-        case 7: return native_kernel<K, 7>;
-        case 8: return native_kernel<K, 8>;
+        case 1: return native_kernel<K, 1, SCAN>;
+        case 2: return native_kernel<K, 2, SCAN>;
+        case 3: return native_kernel<K, 3, SCAN>;
+        case 4: return native_kernel<K, 4, SCAN>;
+        case 5: return native_kernel<K, 5, SCAN>;
+        case 6: return native_kernel<K, 6, SCAN>;
+        case 7: return native_kernel<K, 7, SCAN>;
+        case 8: return native_kernel<K, 8, SCAN>;
     }
     return nullptr;
 }
 
-KernelFn pick_kernel(int mode, int k, int ch) {
+template <int K>
+KernelFn native_for(int ch, bool scan) {
+    return scan ? native_for_ch<K, true>(ch) : native_for_ch<K, false>(ch);
+}
+
+KernelFn pick_kernel(int mode, int k, int ch, bool scan) {
     if (mode == BBE_MODE_MT) return k == 1 ? exact_kernel<1, MT> : nullptr;
     if (mode == BBE_MODE_INJECT) {
         switch (k) {
@@ -297,10 +302,10 @@ KernelFn pick_kernel(int mode, int k, int ch) {
         }
     } else {
         switch (k) {
-            case 1: return native_for_ch<1>(ch);
-            case 2: return native_for_ch<2>(ch);
-            case 3: return native_for_ch<3>(ch);
-            case 4: return native_for_ch<4>(ch);
+            case 1: return native_for<1>(ch, scan);
+            case 2: return native_for<2>(ch, scan);
+            case 3: return native_for<3>(ch, scan);
+            case 4: return native_for<4>(ch, scan);
         }
     }
     return nullptr;
@@ -313,7 +318,10 @@ struct Plan {
     int grid;
 };
 
-int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_request* rq, int want_perms, Plan* pl) {
+int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, const bbe_request* rq, int want_perms,
+              Plan* pl) {
+    bool scan = false;  // any theta > 0: the front-runner scan is needed
+    for (int c = 0; c < race->n; ++c) scan = scan || comps[c].theta > 0.0;
     const int n = race->n;
     pl->mode = rq->mode;
     pl->n = n;
@@ -329,7 +337,7 @@ int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_request* rq, int want
     pl->tally_len = TL.len();
     const int kmode = rq->mode == BBE_MODE_NATIVE ? NATIVE : (rq->mode == BBE_MODE_MT ? MT : INJECT);
     pl->smem = smem_bytes(kmode, (TL.hist_len() + 1) & ~1, pl->K, pl->S, pl->WP);
-    pl->fn = pick_kernel(rq->mode, pl->K, pl->CH);
+    pl->fn = pick_kernel(rq->mode, pl->K, pl->CH, scan);
     if (!pl->fn) return fail(BBE_EINVAL, "no kernel for this configuration");
     if (pl->smem > 48 * 1024) {
         BBE_CK(cudaFuncSetAttribute((const void*)pl->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->smem));
@@ -652,7 +660,7 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
     const int n = race->n;
     const int64_t ns = rq->n_sims;
     Plan pl;
-    if ((rc = make_plan(ctx, race, rq, out->perms != nullptr, &pl))) return rc;
+    if ((rc = make_plan(ctx, race, comps, rq, out->perms != nullptr, &pl))) return rc;
     cudaStream_t s = ctx->stream;
 
     // parameters: one pinned staging block, one H2D copy
@@ -787,7 +795,7 @@ int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const 
     std::lock_guard<std::mutex> guard(ctx->mu);
     Plan pl;
     const bool perms = nperm_for(race->n) > 0;
-    if ((rc = make_plan(ctx, race, rq, perms, &pl))) return rc;
+    if ((rc = make_plan(ctx, race, comps, rq, perms, &pl))) return rc;
     cudaStream_t s = (cudaStream_t)stream;  // NULL = legacy default stream (torch's default)
     // parameters: staged through pinned memory; the copy is ordered on `s` before the kernel, and
     // the staging block is not reused until that copy has been consumed (sync on an event).
