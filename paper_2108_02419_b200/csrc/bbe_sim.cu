@@ -149,9 +149,7 @@ int validate(const bbe_race* race, const bbe_competitor* comps, const bbe_state*
     if (rq->n_sims < 0 || rq->sim_offset < 0) return fail(BBE_EINVAL, "n_sims and sim_offset must be >= 0");
     if (rq->mode == BBE_MODE_INJECT) {
         if (!rq->draws || !rq->draw_offsets) return fail(BBE_EINVAL, "inject mode needs draws and draw_offsets");
-    } else if (rq->mode == BBE_MODE_MT) {
-        if (n > kWarp) return fail(BBE_EINVAL, "mode MT supports at most 32 competitors");
-    } else if (rq->mode != BBE_MODE_NATIVE) {
+    } else if (rq->mode != BBE_MODE_MT && rq->mode != BBE_MODE_NATIVE) {
         return fail(BBE_EINVAL, "unknown mode");
     }
     return BBE_OK;
@@ -292,8 +290,14 @@ KernelFn native_for(int ch, bool scan) {
 }
 
 KernelFn pick_kernel(int mode, int k, int ch, bool scan) {
-    if (mode == BBE_MODE_MT) return k == 1 ? exact_kernel<1, MT> : nullptr;
-    if (mode == BBE_MODE_INJECT) {
+    if (mode == BBE_MODE_MT) {
+        switch (k) {
+            case 1: return exact_kernel<1, MT>;
+            case 2: return exact_kernel<2, MT>;
+            case 3: return exact_kernel<3, MT>;
+            case 4: return exact_kernel<4, MT>;
+        }
+    } else if (mode == BBE_MODE_INJECT) {
         switch (k) {
             case 1: return exact_kernel<1, INJECT>;
             case 2: return exact_kernel<2, INJECT>;
@@ -325,7 +329,9 @@ int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, co
     const int n = race->n;
     pl->mode = rq->mode;
     pl->n = n;
-    pl->K = rq->mode == BBE_MODE_MT ? 1 : choose_k(n, rq->lanes_per_slot_hint);
+    // MT: the fewest slots that fit a warp (every slot adds a speculative word window per lane)
+    pl->K = rq->mode == BBE_MODE_MT ? (n + kWarp - 1) / kWarp : choose_k(n, rq->lanes_per_slot_hint);
+    if (pl->K > 4) pl->K = -1;
     if (pl->K < 0) return fail(BBE_EINVAL, "field too large for one warp");
     pl->W = (n + pl->K - 1) / pl->K;
     if (rq->mode == BBE_MODE_MT) pl->W = std::max(pl->W, 8);  // <= 4 MT states (2.5 KB each) per warp

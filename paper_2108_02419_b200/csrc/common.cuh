@@ -91,12 +91,14 @@ __host__ __device__ constexpr int swp_max(int CH) {
 __host__ __device__ constexpr int native_slot_words(int CH) { return swp_max(CH) + 4; }
 __host__ __device__ constexpr int native_warp_words(int K, int CH) { return 2 * K * native_slot_words(CH); }
 constexpr int kMtWords = 624;
-constexpr int kMtSideWords = 128;  // >= 4 words x 32 lanes: one speculative round's reads
+// side buffer: >= one speculative round's reads (4 words x 32 lanes x K slots)
+__host__ __device__ constexpr int mt_side_words(int K) { return 128 * K; }
+__host__ __device__ constexpr int mt_seg_words(int K) { return kMtWords + mt_side_words(K); }
 constexpr int kXSlot = 66;         // exact modes: doubles per position row (S*round_up(W,2) <= 64, + pad)
 __host__ __device__ inline size_t smem_bytes(int mode, int hist_len_even, int K, int S, int WP) {
     size_t b = (size_t)hist_len_even * 8;
     if (mode == NATIVE) b += (size_t)kWarpsPerBlock * native_warp_words(K, (WP + 3) / 4) * 4;
-    if (mode == MT) b += (size_t)kWarpsPerBlock * S * (kMtWords + kMtSideWords) * 4;
+    if (mode == MT) b += (size_t)kWarpsPerBlock * S * mt_seg_words(K) * 4;
     if (mode != NATIVE) b += (size_t)kWarpsPerBlock * 2 * K * kXSlot * 8;
     return b;
 }

@@ -44,10 +44,10 @@ namespace bbe {
 #endif
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(kBlockThreads, MODE == MT ? BBE_MT_MINBLOCKS : 1)
+__global__ void __launch_bounds__(kBlockThreads, MODE == MT ? (K == 1 ? BBE_MT_MINBLOCKS : 2) : 1)
 exact_kernel(const LaunchArgs a) {
     static_assert(MODE == INJECT || MODE == MT, "exact kernel modes");
-    static_assert(MODE != MT || K == 1, "MT mode maps one competitor per lane");
+    constexpr int kSeg = mt_seg_words(K);  // MT: words per segment (block + side buffer)
     extern __shared__ __align__(16) unsigned long long s_dyn[];
     const TallyLayout TL{a.n, a.perms};
     const int hist_len = TL.hist_len();
@@ -64,13 +64,13 @@ exact_kernel(const LaunchArgs a) {
     const unsigned segmask = lane_on ? ((W == 32 ? 0xffffffffu : ((1u << W) - 1u)) << base) : 0u;
     const unsigned lt_mask = (1u << lane) - 1u;
     uint32_t* const mt = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) +
-                         (warp * S + (lane_on ? seg : 0)) * (kMtWords + kMtSideWords);  // MT: segment state
+                         (warp * S + (lane_on ? seg : 0)) * kSeg;  // MT: this segment's state
     uint32_t* const side = mt + kMtWords;  // MT: unread words saved across an early twist
     // start-of-tick positions, per warp: [parity][slot][segment * WP2 + lane-in-segment], pads -inf
     const int WP2 = (W + 1) & ~1;
     double* const xrows = reinterpret_cast<double*>(
         reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) +
-        (MODE == MT ? kWarpsPerBlock * S * (kMtWords + kMtSideWords) : 0)) + warp * 2 * K * kXSlot;
+        (MODE == MT ? kWarpsPerBlock * S * kSeg : 0)) + warp * 2 * K * kXSlot;
     for (int i = lane; i < 2 * K * kXSlot; i += kWarp) xrows[i] = -CUDART_INF;
     const int xseg = lane_on ? seg * WP2 : 0;
     double* const xw = xrows + (lane_on ? seg * WP2 + l : kXSlot - 1);
@@ -130,14 +130,14 @@ exact_kernel(const LaunchArgs a) {
     // needing segment at a time, 20 chunks of 32 words (32 < 227 keeps every "new" dependency in an
     // earlier chunk), so a segment's twist costs the same whether or not its warp-mates need one.
     uint32_t* const warp_mt = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) +
-                              warp * S * (kMtWords + kMtSideWords);
+                              warp * S * kSeg;
     auto mt_twist = [&](bool need) {
         unsigned todo = __ballot_sync(0xffffffffu, need && l == 0);  // one bit per needing segment
         __syncwarp();
         while (todo) {
             const int leader = __ffs(todo) - 1;
             todo &= todo - 1u;
-            uint32_t* const t = warp_mt + (leader / W) * (kMtWords + kMtSideWords);
+            uint32_t* const t = warp_mt + (leader / W) * kSeg;
             for (int c0 = 0; c0 < kMtWords; c0 += kWarp) {
                 const int i = c0 + lane;
                 const bool act = i < kMtWords;
@@ -154,17 +154,17 @@ exact_kernel(const LaunchArgs a) {
         }
     };
     // The segment's unread stream is a window: side[sp, se) (words saved from the previous block)
-    // followed by mt[q, 624).  Before a round that may read up to 4W words, a window shorter than
+    // followed by mt[q, 624).  Before a round that may read up to 4WK words, a window shorter than
     // that is topped up: the unread words of the block move to `side` and the block is twisted in
     // place -- early, but the stream is the same, since the twist reads the whole old block.
     auto mt_window_fill = [&]() {
-        const bool low = running && lane_on && (se - sp) + (kMtWords - q) < 4 * W;
+        const bool low = running && lane_on && (se - sp) + (kMtWords - q) < 4 * W * K;
         if (!__any_sync(0xffffffffu, low)) return;
-        const int keep = se - sp, tail = kMtWords - q;  // keep + tail < 4W: at most 4 words per lane
-        uint32_t carry[4];
+        const int keep = se - sp, tail = kMtWords - q;  // keep + tail < 4WK: at most 4K words per lane
+        uint32_t carry[4 * K];
         int nc = 0;
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
+        for (int t = 0; t < 4 * K; ++t) {
             const int i = l + t * W;  // new side index
             carry[t] = 0u;
             if (low && i < keep + tail) {
@@ -174,7 +174,7 @@ exact_kernel(const LaunchArgs a) {
         }
         __syncwarp();
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
+        for (int t = 0; t < 4 * K; ++t)
             if (t < nc) side[l + t * W] = carry[t];
         mt_twist(low);  // starts and ends with __syncwarp
         if (low) {
@@ -192,36 +192,59 @@ exact_kernel(const LaunchArgs a) {
         if (c <= ns) sp += c;
         else { q += c - ns; sp = se = 0; }
     };
-    // One step draw per lane with `want`, in competitor-index order within each segment:
-    // uniform(lo, hi) = lo + (hi - lo) * random(); scale * lognormvariate(mu, sigma) via the
-    // Kinderman-Monahan loop of random.normalvariate (Lib/random.py).  Warp-uniform call.
-    auto mt_draws = [&](bool want) -> double {
-        double d = 1.0;
-        double ln_u1 = 0.0, ln_u2 = 1.0;  // the accepted Kinderman-Monahan pair of a lognormal lane
-        bool ln_draw = false;
-        bool pend = want;
+    // One step draw per (slot, lane) with want[k], in competitor-index order within each segment
+    // (slot-major, then lane): uniform(lo, hi) = lo + (hi - lo) * random(); scale *
+    // lognormvariate(mu, sigma) via the Kinderman-Monahan loop of random.normalvariate
+    // (Lib/random.py).  Warp-uniform call.
+    auto mt_draws = [&](const bool (&want)[K], double (&d)[K]) {
+        double ln_u1[K], ln_u2[K];  // the accepted Kinderman-Monahan pair of a lognormal competitor
+        bool ln_draw[K], pend[K];
+        bool any_pend = false;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            d[k] = 1.0;
+            ln_u1[k] = 0.0;
+            ln_u2[k] = 1.0;
+            ln_draw[k] = false;
+            pend[k] = want[k];
+            any_pend |= want[k];
+        }
         // Speculative rounds: every pending competitor takes its words at the offset it would have if
         // each pending lognormal draw accepted its next Kinderman-Monahan trial (2 words per uniform
         // draw, 4 per trial).  Draws up to the first rejected trial in index order are then final;
         // the rejected one consumed its 4 words and retries first in the next round.
-        while (__any_sync(0xffffffffu, pend)) {
+        while (__any_sync(0xffffffffu, any_pend)) {
             mt_window_fill();
-            const int need = pend ? (lognorm[0] ? 4 : 2) : 0;
-            int incl = need;  // inclusive prefix sum over the segment's lanes, in index order
+            // per-slot word counts (<= 4 per lane, <= 128 per slot and segment) packed 8 bits per
+            // slot: one segmented inclusive scan serves all K slots
+            uint32_t need = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) need |= (uint32_t)(pend[k] ? (lognorm[k] ? 4 : 2) : 0) << (8 * k);
+            uint32_t incl = need;
 #pragma unroll
             for (int o = 1; o < kWarp; o <<= 1) {
-                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
                 if (l >= o) incl += v;
             }
-            const int off = incl - need;
-            uint32_t w[4];
+            const uint32_t tot = __shfl_sync(0xffffffffu, incl, lane_on ? base + W - 1 : lane);
+            int off[K];
+            int slot_base = 0;
 #pragma unroll
-            for (int t = 0; t < 4; ++t) w[t] = mt_temper(mt_word(off + t));
-            bool ok = true;
-            if (pend && lognorm[0]) {
-                {
-                    const double u1 = mt_random53(w[0], w[1]);
-                    const double u2 = __dsub_rn(1.0, mt_random53(w[2], w[3]));
+            for (int k = 0; k < K; ++k) {
+                off[k] = slot_base + (int)(((incl - need) >> (8 * k)) & 0xffu);
+                slot_base += (int)((tot >> (8 * k)) & 0xffu);
+            }
+            const int used_all = slot_base;  // the whole round's words
+            uint32_t w[K][4];
+            bool ok[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) w[k][t] = mt_temper(mt_word(off[k] + t));
+                ok[k] = true;
+                if (pend[k] && lognorm[k]) {
+                    const double u1 = mt_random53(w[k][0], w[k][1]);
+                    const double u2 = __dsub_rn(1.0, mt_random53(w[k][2], w[k][3]));
                     // accept iff z*z/4 <= -log(u2) (Lib/random.py normalvariate).  Decide in FP32 when
                     // the two sides are far apart (relative 1e-4, absolute 1e-5: >25x the FP32 error of
                     // either side), else in FP64 exactly as CPython does -- the same decision either way.
@@ -236,32 +259,45 @@ exact_kernel(const LaunchArgs a) {
                         const double zx = __ddiv_rn(__dmul_rn(a.nv_magic, __dsub_rn(u1, 0.5)), u2);
                         acc = __dmul_rn(__dmul_rn(zx, zx), 0.25) <= -log(u2);  // z*z/4.0 (exact scaling)
                     }
-                    ok = acc;
-                    ln_u1 = u1;
-                    ln_u2 = u2;
+                    ok[k] = acc;
+                    ln_u1[k] = u1;
+                    ln_u2[k] = u2;
                 }
             }
-            const unsigned bad = __ballot_sync(0xffffffffu, pend && !ok) & segmask;
-            const unsigned first_bad = bad & (0u - bad);
-            const bool done = pend && (first_bad == 0u || (1u << lane) < first_bad);
-            // words consumed this round: up to and including the rejected trial, or all of them
-            const int last = lane_on ? base + W - 1 : lane;
-            const int used_all = __shfl_sync(0xffffffffu, incl, last);
-            const int used_bad = __shfl_sync(0xffffffffu, off, first_bad ? __ffs(first_bad) - 1 : lane) + 4;
-            if (done) {
-                if (lognorm[0]) ln_draw = true;
-                else d = __dadd_rn(lo[0], __dmul_rn(span[0], mt_random53(w[0], w[1])));
-                pend = false;
+            // first rejected trial in index order: lowest slot with a rejection, lowest lane in it
+            int kb = K;
+            unsigned first_bad = 0u;
+#pragma unroll
+            for (int k = K - 1; k >= 0; --k) {
+                const unsigned bad_k = __ballot_sync(0xffffffffu, pend[k] && !ok[k]) & segmask;
+                if (bad_k) { kb = k; first_bad = bad_k & (0u - bad_k); }
+            }
+            int off_kb = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) off_kb = (k == kb) ? off[k] : off_kb;
+            const int used_bad = __shfl_sync(0xffffffffu, off_kb, first_bad ? __ffs(first_bad) - 1 : lane) + 4;
+            any_pend = false;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const bool done = pend[k] && (k < kb || (k == kb && (1u << lane) < first_bad));
+                if (done) {
+                    if (lognorm[k]) ln_draw[k] = true;
+                    else d[k] = __dadd_rn(lo[k], __dmul_rn(span[k], mt_random53(w[k][0], w[k][1])));
+                    pend[k] = false;
+                }
+                any_pend |= pend[k];
             }
             if (lane_on && running) mt_consume(first_bad ? used_bad : used_all);
         }
         // lognormvariate's value for every accepted pair at once (the stream order is already fixed):
         // z = NV*(u1-0.5)/u2, scale * exp(mu + z*sigma) with the host libm's exp
-        if (ln_draw) {
-            const double z = __ddiv_rn(__dmul_rn(a.nv_magic, __dsub_rn(ln_u1, 0.5)), ln_u2);
-            d = __dmul_rn(scale[0], libm_exp(__dadd_rn(mu[0], __dmul_rn(z, sigma[0]))));
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (ln_draw[k]) {
+                const double z = __ddiv_rn(__dmul_rn(a.nv_magic, __dsub_rn(ln_u1[k], 0.5)), ln_u2[k]);
+                d[k] = __dmul_rn(scale[k], libm_exp(__dadd_rn(mu[k], __dmul_rn(z, sigma[k]))));
+            }
         }
-        return d;
     };
 
     // trajectory snapshot after tick t of the current sim (t = 0: the state the sim starts from)
@@ -305,7 +341,10 @@ exact_kernel(const LaunchArgs a) {
             // race.py:233-241: one free draw per competitor, in index order, resp at position 0
             double d[K];
             if constexpr (MODE == MT) {
-                d[0] = mt_draws(do_it && running && has[0]);
+                bool want[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) want[k] = do_it && running && has[k];
+                mt_draws(want, d);
             } else {
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
@@ -523,7 +562,7 @@ exact_kernel(const LaunchArgs a) {
                     for (int k = 0; k < K; ++k) { racing[k] = false; fr[k] = bl[k] = false; }
                 }
             } else {
-                draw[0] = mt_draws(fr[0]);
+                mt_draws(fr, draw);
             }
 
             // ---- synchronous update (race.py:299-320) ----

@@ -91,9 +91,39 @@ def test_large_fields_native_layouts(n):
     assert abs(r.competitor_steps / 20_000 - ref["ct"] / 4000) / (ref["ct"] / 4000) < 0.01
 
 
-def test_mt_rejects_fields_over_32():
-    with pytest.raises(RaceConfigError):
-        sim.simulate_batch(None, _field(33), 10, mode="mt", seed_master=1)
+def _mixed_field(n, L=60.0):
+    """Uniform and lognormal competitors with alternating theta: blocked steps and rejections in
+    every slot of a multi-slot lane layout."""
+    comps = []
+    for i in range(n):
+        steps = LogNormalSteps(0.4 + 0.01 * (i % 7), 0.35, 2.0) if i % 3 == 0 else UniformSteps(2.0 + i % 3, 5.0 + i % 4)
+        comps.append(Competitor(f"c{i}", steps, theta=1.2 * (i % 2)))
+    return RaceConfig(L, tuple(comps))
+
+
+@pytest.mark.parametrize("n", [33, 40, 64, 65, 97, 128])
+def test_mt_multi_slot_fields_bit_exact(n):
+    """n > 32 puts K = ceil(n/32) competitors in every lane; the speculative MT rounds then span
+    the slots in index order (slot-major) -- positions, ticks and orders must stay bit-exact."""
+    cfg = _mixed_field(n)
+    seeds = oracle.rp_seeds(11, 300)
+    r = sim.simulate_batch(None, cfg, 300, mode="mt", seeds=seeds, records=True)
+    assert int(r.wins.sum()) == 300
+    for i in (0, 1, 2, 150, 299):
+        o = oracle.run_race(cfg, int(seeds[i]))
+        assert r.final_positions[i].tolist() == o.final_positions.tolist()
+        assert r.finish_ticks[i].tolist() == o.finish_ticks.tolist()
+        assert r.order[i].tolist() == o.order.tolist()
+        assert int(r.blocked[i]) == o.blocked
+    # a continuation state (simulate_from) with finished and racing competitors
+    st = RaceState(6, [3.0 + 0.5 * (i % 11) for i in range(n)], [2.5] * n,
+                   [5 if i == 4 else None for i in range(n)])
+    st.positions[4] = 61.0
+    r = sim.simulate_batch(st, cfg, 100, mode="mt", seeds=seeds[:100], records=True)
+    for i in (0, 57, 99):
+        o = oracle.simulate_from(st, cfg, int(seeds[i]))
+        assert r.final_positions[i].tolist() == o.final_positions.tolist()
+        assert r.order[i].tolist() == o.order.tolist()
 
 
 def test_lognormal_zero_sigma_and_responsiveness_edges():

@@ -27,8 +27,6 @@ def test_golden_corpus_from_seeds():
     exact_pos = total = pos_ulp_mismatch = 0
     for case in race_corpus():
         cfg = config_from_dict(case["config"])
-        if cfg.n_competitors > 32:
-            continue
         for path in ("run_race", "simulate_from"):
             exp = case[path]
             st = None if path == "run_race" else state_from_dict(exp["state"])
