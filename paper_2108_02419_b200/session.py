@@ -24,7 +24,7 @@ import numpy as np
 from .agents import dry_run_seeds
 from .race import RaceState
 from .seeding import derive_seed, spawn_rng
-from .sim import run_race, simulate_batch
+from .sim import run_race, simulate_batch_begin
 
 
 @dataclass
@@ -36,43 +36,69 @@ class DryRunRequest:
 
 
 class DryRunDispatcher:
-    """Batch the dry runs of every bettor that predicts from the same race state into one launch."""
+    """Batch the dry runs of every bettor that predicts from the same race state into one launch.
+
+    ``predict_many`` = ``prepare`` (host: advance every bettor's stream, collect the seeds) ->
+    ``launch`` (enqueue one batch) -> ``finish`` (wait, split the winners per bettor).  A caller
+    with a queue of batches prepares batch i+1 while batch i runs on the GPU
+    (``run_dry_run_session`` does).
+    """
 
     def __init__(self, config, mode: str = "mt"):
         self.config = config
         self.mode = mode
         self.launches = 0
         self.sims = 0
+        self._n = len(config.competitors)
+
+    def prepare(self, requests: list[DryRunRequest]) -> dict:
+        """Advance each bettor's stream exactly as its own ``rp_predict`` call would, in request
+        order (bettors own disjoint streams, so the order across bettors does not matter)."""
+        ds = [max(int(r.d), 0) for r in requests]
+        total = sum(ds)
+        prep = {"ds": ds, "total": total, "seeds": None, "key": 0}
+        if self.mode == "mt":
+            seeds = [dry_run_seeds(r.rng, r.d) for r in requests]
+            if total:
+                prep["seeds"] = np.concatenate([s for s in seeds if len(s)])
+        else:
+            # native: the batch's Philox stream is keyed by the first dry-run seed; every other draw
+            # only advances its bettor's stream
+            first = True
+            for r in requests:
+                if r.d > 0 and first:
+                    prep["key"] = int(dry_run_seeds(r.rng, r.d, first_only=True)[0])
+                    first = False
+                else:
+                    dry_run_seeds(r.rng, r.d, want=False)
+        return prep
+
+    def launch(self, state, prep: dict):
+        """Enqueue one batch for a prepared request list (None if it has no dry runs)."""
+        if prep["total"] == 0:
+            return None
+        self.launches += 1
+        self.sims += prep["total"]
+        if self.mode == "mt":
+            return simulate_batch_begin(state, self.config, prep["total"], mode="mt", seeds=prep["seeds"],
+                                        winners=True, ranks=False)
+        return simulate_batch_begin(state, self.config, prep["total"], prep["key"], mode=self.mode, winners=True,
+                                    ranks=False)
+
+    def finish(self, pending, prep: dict) -> list[tuple[float, ...]]:
+        """Laplace-smoothed win probabilities per request (agents.py:153-166), in request order."""
+        n, ds = self._n, prep["ds"]
+        if pending is None:
+            return [tuple(1 / (d + n) for _ in range(n)) for d in ds]
+        res = pending.end()
+        group = np.repeat(np.arange(len(ds)), ds)
+        wins = np.bincount(group * n + res.winner, minlength=len(ds) * n).reshape(len(ds), n)
+        return [tuple((w + 1) / (d + n) for w in row) for d, row in zip(ds, wins.tolist())]
 
     def predict_many(self, state, requests: list[DryRunRequest]) -> list[tuple[float, ...]]:
-        """Laplace-smoothed win probabilities per request (agents.py:153-166), in request order.
-
-        Each bettor's stream is advanced exactly as its own ``rp_predict`` call would, in request
-        order (bettors own disjoint streams, so the order across bettors does not matter).
-        """
-        n = len(self.config.competitors)
-        seeds = [dry_run_seeds(r.rng, r.d) for r in requests]
-        total = int(sum(r.d for r in requests if r.d > 0))
-        out: list[tuple[float, ...]] = []
-        if total == 0:
-            return [tuple(1 / (r.d + n) for _ in range(n)) for r in requests]
-        all_seeds = np.concatenate([s for s in seeds if len(s)])
-        if self.mode == "mt":
-            res = simulate_batch(state, self.config, total, mode="mt", seeds=all_seeds, winners=True, ranks=False)
-        else:
-            res = simulate_batch(state, self.config, total, int(all_seeds[0]), mode=self.mode, winners=True,
-                                 ranks=False)
-        self.launches += 1
-        self.sims += total
-        at = 0
-        for r in requests:
-            if r.d <= 0:
-                out.append(tuple(1 / (r.d + n) for _ in range(n)))
-                continue
-            wins = np.bincount(res.winner[at:at + r.d], minlength=n)
-            at += r.d
-            out.append(tuple((int(w) + 1) / (r.d + n) for w in wins))
-        return out
+        """One batched prediction for every request, in request order."""
+        prep = self.prepare(requests)
+        return self.finish(self.launch(state, prep), prep)
 
 
 def wake_schedule(reevaluate_every: list[float], wake_jitter: list[float], horizon: float, master_seed: int):
@@ -133,15 +159,13 @@ def run_dry_run_session(config, n_agents: int, d: int, master_seed: int, *, open
     disp = DryRunDispatcher(config, mode)
     preds = []
 
-    def process(until: float, state):
+    def batches(until: float, state):
         due = []
         for i in range(n_agents):
             while next_wake[i] <= until:
                 due.append((next_wake[i], i))
                 next_wake[i] += reevaluate_every
         due.sort()
-        if not due:
-            return
         # a bettor waking k times in one batch needs its k-th prediction after its (k-1)-th decision;
         # RP decisions draw from the stream only on ties (agents.py:304-310), which this driver does
         # not model, so rounds are batched: round r = every bettor's r-th due wake.
@@ -153,15 +177,24 @@ def run_dry_run_session(config, n_agents: int, d: int, master_seed: int, *, open
             if r == len(rounds):
                 rounds.append([])
             rounds[r].append((t, i))
-        for rnd in rounds:
-            probs = disp.predict_many(state, [DryRunRequest(rngs[i], d) for _, i in rnd])
-            preds.extend((t, i, p) for (t, i), p in zip(rnd, probs))
+        return [(state, rnd) for rnd in rounds]
 
-    t0 = time.perf_counter()
-    process(opening_period, states[0])
+    # the live race is fixed in advance (session.py:282 uses only rng_race), so the whole sequence of
+    # (race state, wake round) batches is known: prepare batch i+1 on the host while batch i runs
+    work = batches(opening_period, states[0])
     for tick in range(1, n_ticks + 1):
         if all(f is not None for f in states[tick].finish_ticks):
             break  # betting closes when the last runner finishes (BettingClose.last, session.py:294-311)
-        process(opening_period + tick * config.dt, states[tick])
+        work.extend(batches(opening_period + tick * config.dt, states[tick]))
+
+    t0 = time.perf_counter()
+    prev = None  # (batch, prepared, pending) in flight
+    for state, rnd in work:
+        prep = disp.prepare([DryRunRequest(rngs[i], d) for _, i in rnd])
+        if prev is not None:
+            preds.extend((t, i, p) for (t, i), p in zip(prev[0], disp.finish(prev[2], prev[1])))
+        prev = (rnd, prep, disp.launch(state, prep))
+    if prev is not None:
+        preds.extend((t, i, p) for (t, i), p in zip(prev[0], disp.finish(prev[2], prev[1])))
     seconds = time.perf_counter() - t0
     return DryRunSessionResult(preds, disp.launches, disp.sims, seconds, n_ticks)

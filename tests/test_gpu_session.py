@@ -32,6 +32,23 @@ def test_dispatcher_equals_per_bettor_rp_predict():
     assert DryRunDispatcher(cfg, "mt").predict_many(st, [DryRunRequest(r, g["d"])])[0] == tuple(g["probs"])
 
 
+def test_native_dispatcher_advances_streams_like_rp_predict():
+    g = c2()
+    cfg, st = config_from_dict(g["config"]), state_from_dict(g["state"])
+    ds = [0, 5, 1000, 3, 20000]
+    a = [random.Random(50 + i) for i in range(len(ds))]
+    b = [random.Random(50 + i) for i in range(len(ds))]
+    got = DryRunDispatcher(cfg, "native").predict_many(st, [DryRunRequest(r, d) for r, d in zip(a, ds)])
+    for r, d in zip(b, ds):
+        rp_predict(st, cfg, d, r, mode="native")
+    assert all(x.getstate() == y.getstate() for x, y in zip(a, b))
+    assert got[0] == tuple(1 / cfg.n_competitors for _ in range(cfg.n_competitors))
+    assert all(abs(sum(p) - 1.0) < 1e-9 for p in got)
+    # the 20000-run bettor's probabilities agree with the reference's golden rp_predict within binomial noise
+    ref = np.array(g["probs"])
+    assert np.abs(np.array(got[4]) - ref).max() < 5 * np.sqrt(0.25 / 20000) + 5 * np.sqrt(0.25 / g["d"])
+
+
 def test_run_race_record_trajectory_matches_reference_stream():
     """race.py:373-390 with record=True; tests/test_race.py:226-242 trajectory properties."""
     case = next(c for c in race_corpus() if c["name"] == "derby5_0")
