@@ -146,6 +146,12 @@ int validate(const bbe_race* race, const bbe_competitor* comps, const bbe_state*
     }
     if (!st->from_start && (!st->positions || !st->prev_steps || !st->finish_ticks))
         return fail(BBE_EINVAL, "continuation state needs positions, prev_steps and finish_ticks");
+    if (rq->mode == BBE_MODE_NATIVE) {
+        // the FP32 front-runner frame (native_frame) needs finite positions and track length
+        if (!std::isfinite(race->track_length)) return fail(BBE_EINVAL, "mode native needs a finite track_length");
+        for (int c = 0; !st->from_start && c < n; ++c)
+            if (!std::isfinite(st->positions[c])) return fail(BBE_EINVAL, "mode native needs finite positions");
+    }
     if (rq->n_sims < 0 || rq->sim_offset < 0) return fail(BBE_EINVAL, "n_sims and sim_offset must be >= 0");
     if (rq->mode == BBE_MODE_INJECT) {
         if (!rq->draws || !rq->draw_offsets) return fail(BBE_EINVAL, "inject mode needs draws and draw_offsets");
@@ -228,15 +234,67 @@ void pack_params(const bbe_race* race, const bbe_competitor* comps, const bbe_st
 
 size_t param_bytes(int n) { return (size_t)F_COUNT * n * sizeof(double) + (size_t)NF_COUNT * n * sizeof(float); }
 
-// NATIVE FP32 block, appended after the double block.  Returns the position offset that makes every
-// position >= +0.0 (the kernel's float-bits ordering needs it; gaps and L - pos are unchanged).
-float pack_params_f32(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, double* P) {
+// NATIVE front-runner frame (native_kernel.cuh): an offset of positions, L and breakpoints, and the
+// key base, such that every racing position p satisfies 1 <= bits(p) - key_base < 2^(31 - key_bits)
+// for the whole race (racing positions only grow and stay below L, or start at their initial value).
+// The offset is 0 whenever the state already fits (C2: positions ~900..2000, 4 index bits).
+struct NativeFrame {
+    float shift;
+    uint32_t key_base;
+    int key_bits;
+};
+
+uint32_t f32_bits(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, sizeof u);
+    return u;
+}
+
+NativeFrame native_frame(const bbe_race* race, const bbe_state* st, int W) {
+    NativeFrame fr{0.0f, f32_bits(1.0f) - 1u, 1};
+    while ((1 << fr.key_bits) < W) ++fr.key_bits;
+    const uint64_t R = 1ull << (31 - fr.key_bits);
+    const int n = race->n;
+    auto racing = [&](int c) { return st->from_start || st->finish_ticks[c] < 0; };
+    auto pos_of = [&](int c) { return st->from_start ? 0.0 : st->positions[c]; };
+    double min_pos = INFINITY;
+    for (int c = 0; c < n; ++c)
+        if (racing(c)) min_pos = std::min(min_pos, pos_of(c));
+    if (!(min_pos < INFINITY)) return fr;  // nobody racing: the scan never runs on a live key
+    // whether `shift` is a valid frame; sets key_base
+    auto fits = [&](float shift) {
+        float lo = INFINITY, hi = (float)race->track_length + shift;  // the kernel's L
+        for (int c = 0; c < n; ++c) {
+            if (!racing(c)) continue;
+            const float p = (float)(pos_of(c) + (double)shift);  // as packed below
+            lo = std::min(lo, p);
+            hi = std::max(hi, p);
+        }
+        if (!(lo > 0.0f) || !(hi < INFINITY)) return false;
+        fr.key_base = f32_bits(lo) - 1u;
+        return (uint64_t)(f32_bits(hi) - fr.key_base) < R;
+    };
+    if (min_pos > 0.0 && fits(0.0f)) return fr;
+    for (int e = 0; e < 128; ++e) {
+        const double target = std::ldexp(1.0, e);
+        if (target <= min_pos) continue;
+        for (float shift : {(float)(target - min_pos), std::nextafter((float)(target - min_pos), INFINITY)}) {
+            if (fits(shift)) {
+                fr.shift = shift;
+                return fr;
+            }
+        }
+    }
+    fr.shift = NAN;  // unreachable for finite inputs (validate() rejects non-finite ones)
+    return fr;
+}
+
+// NATIVE FP32 block, appended after the double block, in the frame `fr`.
+void pack_params_f32(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, double* P,
+                     const NativeFrame& fr) {
     const int n = race->n;
     float* F = reinterpret_cast<float*>(P + (size_t)F_COUNT * n);
-    double lo_pos = 0.0;
-    if (!st->from_start)
-        for (int c = 0; c < n; ++c) lo_pos = std::min(lo_pos, st->positions[c]);
-    const double shift = -lo_pos;
+    const double shift = fr.shift;
     const double log2e = 1.4426950408889634;
     for (int c = 0; c < n; ++c) {
         const bbe_competitor& p = comps[c];
@@ -251,10 +309,9 @@ float pack_params_f32(const bbe_race* race, const bbe_competitor* comps, const b
         F[NF_LATE * n + c] = (float)p.late_mult;
         F[NF_BP * n + c] = (float)(p.bp_abs + shift);
         F[NF_THETA * n + c] = (float)p.theta;
-        F[NF_POS0 * n + c] = st->from_start ? 0.0f : (float)(st->positions[c] + shift);
+        F[NF_POS0 * n + c] = (float)((st->from_start ? 0.0 : st->positions[c]) + shift);
         F[NF_PREV0 * n + c] = st->from_start ? 0.0f : (float)st->prev_steps[c];
     }
-    return (float)shift;
 }
 
 void philox_round_keys(uint64_t seed, uint32_t* rk) {
@@ -618,12 +675,14 @@ static int launch_all(DevCtx* ctx, const Plan& pl, LaunchArgs a, const bbe_compe
 
 static int build_args(const Plan& pl, const bbe_race* race, const bbe_state* st, const bbe_request* rq,
                       const double* d_params, const double* d_draws, const int64_t* d_offsets, uint64_t* d_tally,
-                      const bbe_result* dev_out, float shift, LaunchArgs* out) {
+                      const bbe_result* dev_out, const NativeFrame& fr, LaunchArgs* out) {
     LaunchArgs& a = *out;
     a = LaunchArgs{};
     a.P = d_params;
     a.Pf = reinterpret_cast<const float*>(d_params + (size_t)F_COUNT * race->n);
-    a.shift = shift;
+    a.shift = fr.shift;
+    a.key_base = fr.key_base;
+    a.key_bits = fr.key_bits;
     philox_round_keys(rq->seed, a.rk);
     a.n = race->n;
     a.W = pl.W;
@@ -674,7 +733,8 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
     BBE_CK(ctx->h_params.ensure(pbytes));
     BBE_CK(ctx->d_params.ensure(pbytes));
     pack_params(race, comps, st, (double*)ctx->h_params.p);
-    const float shift = pack_params_f32(race, comps, st, (double*)ctx->h_params.p);
+    const NativeFrame fr = native_frame(race, st, pl.W);
+    pack_params_f32(race, comps, st, (double*)ctx->h_params.p, fr);
     BBE_CK(cudaMemcpyAsync(ctx->d_params.p, ctx->h_params.p, pbytes, cudaMemcpyHostToDevice, s));
 
     const double* d_draws = nullptr;
@@ -725,7 +785,7 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
 
     LaunchArgs a;
     build_args(pl, race, st, rq, (const double*)ctx->d_params.p, d_draws, d_offsets, (uint64_t*)ctx->d_tally.p, &dev,
-               shift, &a);
+               fr, &a);
     BBE_CK(cudaEventRecord(ctx->ev0, s));
     if ((rc = launch_all(ctx, pl, a, comps, d_seeds, rq->seed_master, s))) return rc;
     BBE_CK(cudaEventRecord(ctx->ev1, s));
@@ -810,10 +870,11 @@ int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const 
     BBE_CK(ctx->d_params.ensure(pbytes));
     BBE_CK(cudaEventSynchronize(ctx->ev1));  // previous async launch on this ctx has read its params
     pack_params(race, comps, st, (double*)ctx->h_params.p);
-    const float shift = pack_params_f32(race, comps, st, (double*)ctx->h_params.p);
+    const NativeFrame fr = native_frame(race, st, pl.W);
+    pack_params_f32(race, comps, st, (double*)ctx->h_params.p, fr);
     BBE_CK(cudaMemcpyAsync(ctx->d_params.p, ctx->h_params.p, pbytes, cudaMemcpyHostToDevice, s));
     LaunchArgs a;
-    build_args(pl, race, st, rq, (const double*)ctx->d_params.p, rq->draws, rq->draw_offsets, d_tally, dev_out, shift,
+    build_args(pl, race, st, rq, (const double*)ctx->d_params.p, rq->draws, rq->draw_offsets, d_tally, dev_out, fr,
                &a);
     BBE_CK(cudaEventRecord(ctx->ev0, s));
     if ((rc = launch_all(ctx, pl, a, comps, rq->seeds, rq->seed_master, s))) return rc;

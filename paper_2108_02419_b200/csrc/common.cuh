@@ -59,7 +59,9 @@ struct LaunchArgs {
     const double* P;  // [F_COUNT][n] parameter block
     const float* Pf;  // [NF_COUNT][n] (NATIVE)
     uint32_t rk[20];  // Philox4x32-10 round keys of the seed (NATIVE)
-    float shift;      // NATIVE: positions, L and breakpoints are offset by this to keep positions >= 0
+    float shift;      // NATIVE: positions, L and breakpoints are offset by this (the front-runner frame)
+    uint32_t key_base;  // NATIVE: front-runner key = float bits of a position - key_base
+    int key_bits;       // NATIVE: index bits packed under the key
     int n, W, S, WP, from_start, scan, perms;
     double L;
     int64_t tick0;

@@ -7,14 +7,13 @@
 // gap > theta => free draw scaled by (resp * pref), else resp * min(prev_c, prev_front) with no draw,
 // nextafter on a zero-progress step, finish at p >= L, order by (finish tick, L - pos, index).
 //
-// Front runner.  The host offsets positions (and L, breakpoints) so every position is >= +0.0;
-// for such floats the raw IEEE bits order like the values, so a position's u32 bits are its key.
-// Each lane publishes its key (0 once finished: 0.0 is never strictly ahead of anyone) to a per-warp
-// shared-memory row (double-buffered by tick parity, one __syncwarp per tick), reads its segment's
-// row with 128-bit broadcast loads and keeps min((key_r - key_c - 1) mod 2^32): the wrap sends every
-// rival at or behind c above every rival ahead, so the minimum is the nearest key strictly ahead.
-// Compiled, that is one VIADDMNMX per rival (two independent chains for ILP).  The front's index --
-// needed only for a blocked step -- is found by a second pass only when some lane is blocked.
+// Front runner.  The host picks a frame (an offset of positions, L and breakpoints) in which every
+// racing position is >= a floor `lo` > 0 and below L with bits(L) - bits(lo) < 2^(31-b), b = index
+// bits of a segment.  Non-negative floats order like their IEEE bits, so key = bits(pos) - bits(lo) + 1
+// is an order-preserving (31-b)-bit key.  Each lane publishes (key << b) | lane-in-segment (0 once
+// finished) to a per-warp shared-memory row (double-buffered by tick parity, one __syncwarp per tick),
+// reads its segment's row with 128-bit broadcast loads and keeps one wrapped minimum (one VIADDMNMX per
+// rival) that yields the nearest key strictly ahead together with the lowest index holding it.
 //
 // Bookkeeping is kept off the per-tick path: rt (ticks advanced in the sim) is segment-uniform;
 // racing <=> fin == kRacing (int32 finish tick relative to the state's tick); the tick-limit check
@@ -30,9 +29,6 @@ namespace bbe {
 // Build-time variants for A/B measurement (tools/ab_build.sh); the defaults are the measured best
 // (C2 on B200: vote-based front recovery 0.474 ms, split limit check 0.443 ms, neither 0.437 ms;
 // 10 blocks/SM at 51 registers 0.483 ms).
-#ifndef BBE_VOTE_RECOVERY
-#define BBE_VOTE_RECOVERY 0
-#endif
 #ifndef BBE_SPLIT_LIMIT
 #define BBE_SPLIT_LIMIT 0
 #endif
@@ -135,6 +131,12 @@ native_kernel(const LaunchArgs a) {
     any_lognorm = __any_sync(0xffffffffu, any_lognorm);
     const float L = (float)a.L + a.shift;
     constexpr bool scan = SCAN;
+    // front-runner values: key = bits(pos) - key_base in [1, 2^(31-b)) for a racing competitor (the
+    // host picks the frame: bbe_sim.cu native_frame), b = a.key_bits index bits
+    const int kbits = a.key_bits;
+    const uint32_t mulb = 1u << kbits, lowmask = mulb - 1u, nmulb = 0u - mulb;
+    const uint32_t cl = (uint32_t)l - a.key_base * mulb;       // v = bits * 2^b + cl = (key << b) | l
+    const uint32_t cn = a.key_base * mulb - lowmask - 1u;      // ~v' = bits * -2^b + cn, v' = v | lowmask
 
     // ---- segment bookkeeping ----
     const int64_t segs_total = (int64_t)gridDim.x * kWarpsPerBlock * S;
@@ -303,26 +305,32 @@ native_kernel(const LaunchArgs a) {
                 }
             }
 
-            // ---- front runner: nearest key strictly ahead (race.py:244-264) ----
+            // ---- front runner: nearest key strictly ahead, lowest index on ties (race.py:244-264) ----
+            // Published value v = (key << b) | j; lane c keeps min over its segment of
+            // v_r + ~(v_c | lowmask) = ((key_r - key_c) << b) + j_r - 2^b  (mod 2^32), one VIADDMNMX
+            // per rival.  Rivals strictly ahead give ((dkey - 1) << b) + j < 2^31, ordered by (key, j);
+            // equal keys, rivals behind and finished rivals (v = 0) wrap to >= 2^31.  So the minimum
+            // holds the front's key AND its index -- no second pass.
             float gap[K];
-            uint32_t fkey[K], kp[K];
+            int fj[K], fk[K];
 #pragma unroll
-            for (int k = 0; k < K; ++k) { gap[k] = CUDART_INF_F; fkey[k] = 0u; kp[k] = 0u; }
+            for (int k = 0; k < K; ++k) { gap[k] = CUDART_INF_F; fj[k] = 0; fk[k] = 0; }
             if constexpr (scan) {
-                uint32_t nk[K];
+                uint32_t kb[K], nk[K];
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
-                    kp[k] = __float_as_uint(pos[k]);
-                    nk[k] = ~kp[k];
-                    wr[(tj & 1) * PAR + k * SLOT] = racing[k] ? kp[k] : 0u;
+                    kb[k] = __float_as_uint(pos[k]);
+                    nk[k] = kb[k] * nmulb + cn;  // ~((key_c << b) | lowmask)
+                    wr[(tj & 1) * PAR + k * SLOT] = racing[k] ? kb[k] * mulb + cl : 0u;
                 }
                 __syncwarp();
-                uint32_t b0[K], b1[K];
-#pragma unroll
-                for (int k = 0; k < K; ++k) { b0[k] = 0xffffffffu; b1[k] = 0xffffffffu; }
+                uint32_t best[K];
 #pragma unroll
                 for (int kk = 0; kk < K; ++kk) {
                     const uint4* r4 = reinterpret_cast<const uint4*>(rd + (tj & 1) * PAR + kk * SLOT);
+                    uint32_t b0[K], b1[K];
+#pragma unroll
+                    for (int k = 0; k < K; ++k) { b0[k] = 0xffffffffu; b1[k] = 0xffffffffu; }
 #pragma unroll
                     for (int c = 0; c < CH; ++c) {
                         const uint4 v = r4[c];
@@ -334,13 +342,20 @@ native_kernel(const LaunchArgs a) {
                             b1[k] = min(b1[k], v.w + nk[k]);
                         }
                     }
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const uint32_t d = min(b0[k], b1[k]);
+                        // rows in slot order, strictly smaller key distance only: equal keys keep the
+                        // lower slot, i.e. the lower competitor index
+                        if (kk == 0 || (d >> kbits) < (best[k] >> kbits)) { best[k] = d; fk[k] = kk; }
+                    }
                 }
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
-                    const uint32_t fk = min(b0[k], b1[k]) - nk[k];  // = best + key_c + 1 (mod 2^32)
-                    const bool ahead = fk > kp[k];                    // no wrap <=> someone strictly ahead
-                    fkey[k] = fk;
-                    gap[k] = ahead ? __fsub_rn(__uint_as_float(fk), pos[k]) : CUDART_INF_F;
+                    const uint32_t t = best[k] + mulb;  // (dkey << b) | j
+                    fj[k] = (int)(t & lowmask);
+                    const bool ahead = best[k] < 0x80000000u;
+                    gap[k] = ahead ? __fsub_rn(__uint_as_float(kb[k] + (t >> kbits)), pos[k]) : CUDART_INF_F;
                 }
             }
 
@@ -353,48 +368,19 @@ native_kernel(const LaunchArgs a) {
                 any_bl |= bl[k];
             }
             float pf[K];
+            if constexpr (K == 1) {
+                pf[0] = shfl(prev[0], base + fj[0]);
+            } else {
 #pragma unroll
-            for (int k = 0; k < K; ++k) pf[k] = 0.0f;
-            if (BBE_VOTE_RECOVERY && K == 1 && __any_sync(0xffffffffu, any_bl)) {
-                // one competitor per lane: for each blocked lane b (warp-uniform loop), the lanes of b's
-                // segment holding b's front key vote; the lowest such lane is the lowest index
-                unsigned bm = __ballot_sync(0xffffffffu, bl[0]);
-                const uint32_t mine = racing[0] ? kp[0] : 0u;
-                while (bm) {
-                    const int b = __ffs(bm) - 1;
-                    bm &= bm - 1u;
-                    const uint32_t x = __shfl_sync(0xffffffffu, fkey[0], b);
-                    const unsigned sm = __shfl_sync(0xffffffffu, segmask, b);
-                    const unsigned m = __ballot_sync(0xffffffffu, mine == x) & sm;
-                    const float v = __shfl_sync(0xffffffffu, prev[0], __ffs(m) - 1);
-                    if (lane == b) pf[0] = v;
-                }
-            } else if ((K > 1 || !BBE_VOTE_RECOVERY) && __any_sync(0xffffffffu, any_bl)) {
-                // front index: lowest competitor index holding the front key (slot-major, then lane)
-                int bi[K];
+                for (int k = 0; k < K; ++k) pf[k] = 0.0f;
+                if (__any_sync(0xffffffffu, any_bl)) {
 #pragma unroll
-                for (int k = 0; k < K; ++k) bi[k] = 0;
-#pragma unroll
-                for (int kk = K - 1; kk >= 0; --kk) {
-                    const uint4* r4 = reinterpret_cast<const uint4*>(rd + (tj & 1) * PAR + kk * SLOT);
-#pragma unroll
-                    for (int c = CH - 1; c >= 0; --c) {
-                        const uint4 v = r4[c];
+                    for (int kk = 0; kk < K; ++kk) {
 #pragma unroll
                         for (int k = 0; k < K; ++k) {
-                            bi[k] = (v.w == fkey[k]) ? (kk << 5) | (4 * c + 3) : bi[k];
-                            bi[k] = (v.z == fkey[k]) ? (kk << 5) | (4 * c + 2) : bi[k];
-                            bi[k] = (v.y == fkey[k]) ? (kk << 5) | (4 * c + 1) : bi[k];
-                            bi[k] = (v.x == fkey[k]) ? (kk << 5) | (4 * c + 0) : bi[k];
+                            const float v = shfl(prev[kk], base + fj[k]);
+                            pf[k] = (fk[k] == kk) ? v : pf[k];
                         }
-                    }
-                }
-#pragma unroll
-                for (int kk = 0; kk < K; ++kk) {
-#pragma unroll
-                    for (int k = 0; k < K; ++k) {
-                        const float v = shfl(prev[kk], base + (bi[k] & 31));
-                        pf[k] = ((bi[k] >> 5) == kk) ? v : pf[k];
                     }
                 }
             }

@@ -136,3 +136,32 @@ def test_lognormal_zero_sigma_and_responsiveness_edges():
     for i in (0, 1, 499):
         o = oracle.run_race(cfg, int(seeds[i]))
         assert r.final_positions[i].tolist() == o.final_positions.tolist()
+
+
+@pytest.mark.parametrize("n", [3, 12, 31, 40, 100])
+def test_native_front_runner_ties_are_exact(n):
+    """Degenerate U(v, v) steps on a half-integer grid make every FP32 operation exact, so native
+    mode must reproduce the reference race bit for bit -- including rivals on identical positions,
+    where the front runner is the lowest index (race.py:244-264), within a slot and across slots."""
+    rng = np.random.default_rng(n)
+    comps = tuple(Competitor(f"c{i}", UniformSteps(v, v), theta=float(th))
+                  for i, (v, th) in enumerate(zip(rng.integers(1, 9, n) * 0.5, rng.choice([0.0, 1.0, 2.5], n))))
+    cfg = RaceConfig(60.0, comps)
+    pos = rng.integers(0, 12, n) * 0.5  # many shared positions
+    prev = rng.integers(1, 9, n) * 0.5
+    st = RaceState(3, pos.tolist(), prev.tolist(), [None] * n)
+    r = sim.simulate_batch(st, cfg, 8, 1, records=True)
+    o = oracle.simulate_from(st, cfg, 1)
+    assert o.blocked > 0
+    for i in range(8):
+        assert r.final_positions[i].tolist() == o.final_positions.tolist()
+        assert r.finish_ticks[i].tolist() == o.finish_ticks.tolist()
+        assert r.order[i].tolist() == o.order.tolist()
+        assert int(r.blocked[i]) == o.blocked
+    # from the start line (run_race: priming draws, everyone level at 0.0)
+    r = sim.simulate_batch(None, cfg, 4, 1, records=True)
+    o = oracle.run_race(cfg, 1)
+    for i in range(4):
+        assert r.final_positions[i].tolist() == o.final_positions.tolist()
+        assert r.order[i].tolist() == o.order.tolist()
+        assert int(r.blocked[i]) == o.blocked
