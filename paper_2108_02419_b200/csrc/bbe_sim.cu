@@ -79,6 +79,8 @@ struct DevCtx {
     DevBuf d_params, d_tally, d_draws, d_offsets, d_winner, d_order, d_fin, d_fpos, d_blocked, d_dused;
     DevBuf d_seeds, d_mt_states, d_mt_scratch;  // MT mode
     DevBuf d_traj;                               // trajectories (positions, previous steps)
+    DevBuf d_work;                               // NATIVE work counters, a ring of kWorkSlots pairs
+    int work_slot = 0;
     bool mt_table = false;                       // c_mt_init uploaded on this device
     // the call in flight between bbe_simulate_begin and bbe_simulate_end
     bool pending = false;
@@ -527,8 +529,21 @@ int bbe_derive_seeds(uint64_t master, int64_t first, int64_t count, uint64_t* ou
     return BBE_OK;
 }
 
-static int launch_one(const Plan& pl, const LaunchArgs& a, cudaStream_t stream) {
-    if (a.n_sims == 0) return BBE_OK;
+constexpr int kWorkSlots = 64;  // concurrent native launches per device with their own work counters
+
+static int launch_one(DevCtx* ctx, const Plan& pl, const LaunchArgs& a0, cudaStream_t stream) {
+    if (a0.n_sims == 0) return BBE_OK;
+    LaunchArgs a = a0;
+    if (pl.mode == BBE_MODE_NATIVE) {
+        // the kernel leaves its counter pair zeroed; consecutive launches rotate through the ring
+        if (!ctx->d_work.p) {
+            BBE_CK(ctx->d_work.ensure(kWorkSlots * 2 * sizeof(unsigned long long)));
+            BBE_CK(cudaMemsetAsync(ctx->d_work.p, 0, kWorkSlots * 2 * sizeof(unsigned long long), stream));
+            BBE_CK(cudaStreamSynchronize(stream));
+        }
+        a.work = (unsigned long long*)ctx->d_work.p + 2 * ctx->work_slot;
+        ctx->work_slot = (ctx->work_slot + 1) % kWorkSlots;
+    }
     // persistent grid: never more blocks than this launch's sims need
     const int64_t sims_per_block = (int64_t)kWarpsPerBlock * pl.S;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pl.grid, (a.n_sims + sims_per_block - 1) / sims_per_block));
@@ -624,7 +639,7 @@ static int launch_all(DevCtx* ctx, const Plan& pl, LaunchArgs a, const bbe_compe
     a.scan = 0;
     for (int c = 0; c < a.n; ++c)
         if (comps[c].theta > 0.0) a.scan = 1;
-    if (pl.mode != BBE_MODE_MT) return launch_one(pl, a, stream);
+    if (pl.mode != BBE_MODE_MT) return launch_one(ctx, pl, a, stream);
 
     if (!ctx->mt_table) {
         uint32_t t[kMtWords];
@@ -667,7 +682,7 @@ static int launch_all(DevCtx* ctx, const Plan& pl, LaunchArgs a, const bbe_compe
             b.traj_pos += c0 * ((int64_t)b.traj_cap + 1) * n;
             b.traj_prev += c0 * ((int64_t)b.traj_cap + 1) * n;
         }
-        int rc = launch_one(pl, b, stream);
+        int rc = launch_one(ctx, pl, b, stream);
         if (rc) return rc;
     }
     return BBE_OK;

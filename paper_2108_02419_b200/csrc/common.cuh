@@ -76,6 +76,7 @@ struct LaunchArgs {
     double* traj_prev;            //   and previous steps (run_race(record=True), race.py:378-389)
     int32_t traj_cap;             //   ticks recorded per sim (longer sims are reported via n_ticks)
     uint64_t* tally;              // device, TallyLayout
+    unsigned long long* work;     // NATIVE: [0] sims claimed after the first round, [1] blocks done (zeroed)
     int32_t* winner;              // optional per-sim outputs
     int32_t* order;
     int64_t* finish_ticks;
