@@ -534,7 +534,7 @@ constexpr int kWorkSlots = 64;  // concurrent native launches per device with th
 static int launch_one(DevCtx* ctx, const Plan& pl, const LaunchArgs& a0, cudaStream_t stream) {
     if (a0.n_sims == 0) return BBE_OK;
     LaunchArgs a = a0;
-    if (pl.mode == BBE_MODE_NATIVE) {
+    {
         // the kernel leaves its counter pair zeroed; consecutive launches rotate through the ring
         if (!ctx->d_work.p) {
             BBE_CK(ctx->d_work.ensure(kWorkSlots * 2 * sizeof(unsigned long long)));

@@ -76,7 +76,7 @@ struct LaunchArgs {
     double* traj_prev;            //   and previous steps (run_race(record=True), race.py:378-389)
     int32_t traj_cap;             //   ticks recorded per sim (longer sims are reported via n_ticks)
     uint64_t* tally;              // device, TallyLayout
-    unsigned long long* work;     // NATIVE: [0] sims claimed after the first round, [1] blocks done (zeroed)
+    unsigned long long* work;     // [0] sims claimed after the first round, [1] blocks done (zeroed)
     int32_t* winner;              // optional per-sim outputs
     int32_t* order;
     int64_t* finish_ticks;
@@ -121,5 +121,28 @@ __device__ __forceinline__ U4 philox_rk(U4 c, const uint32_t* rk) {
 
 template <typename T>
 __device__ __forceinline__ T shfl(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+
+// ---- dynamic sim assignment (persistent kernels) ----
+// Every segment starts on sim `slot` (< segs_total); later sims are claimed from work[0], so a
+// segment that drew short races takes more of them.  Warp-uniform call: one atomic per warp for all
+// its finishing segments (leader lane = the segment's first lane, `base`).
+__device__ __forceinline__ int64_t claim_next_sim(bool seg_done, bool leader, int base, int64_t segs_total,
+                                                  unsigned long long* work) {
+    const unsigned lead = __ballot_sync(0xffffffffu, seg_done && leader);
+    const int first = __ffs(lead) - 1;
+    unsigned long long got = 0;
+    if ((int)(threadIdx.x & 31) == first) got = atomicAdd(work, (unsigned long long)__popc(lead));
+    got = __shfl_sync(0xffffffffu, got, first < 0 ? 0 : first);
+    return segs_total + (int64_t)got + __popc(lead & ((1u << base) - 1u));
+}
+// After the block's last claim (call from thread 0 after a __syncthreads): the last block to finish
+// re-zeroes the counters for the next launch that uses this pair.
+__device__ __forceinline__ void release_work(unsigned long long* work) {
+    __threadfence();
+    if (atomicAdd(work + 1, 1ull) == gridDim.x - 1) {
+        work[0] = 0ull;
+        work[1] = 0ull;
+    }
+}
 
 }  // namespace bbe

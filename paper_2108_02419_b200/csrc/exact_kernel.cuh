@@ -453,8 +453,9 @@ exact_kernel(const LaunchArgs a) {
                 }
                 ct_tot += ct_sim;
                 blk_tot += blk_sim;
-                s += segs_total;
             }
+            const int64_t next = claim_next_sim(seg_done, l == 0, base, segs_total, a.work);
+            if (seg_done) s = next;
             load_sim(seg_done);
         }
         if (!__any_sync(0xffffffffu, running)) break;
@@ -615,6 +616,7 @@ exact_kernel(const LaunchArgs a) {
         if (first_bad != INT64_MAX) atomicMax((unsigned long long*)&a.tally[ct_at + 5], encode_first(first_bad));
     }
     __syncthreads();
+    if (threadIdx.x == 0) release_work(a.work);
     for (int i = threadIdx.x; i < hist_len; i += blockDim.x) {
         const unsigned long long v = s_hist[i];
         if (v) atomicAdd((unsigned long long*)&a.tally[i], v);

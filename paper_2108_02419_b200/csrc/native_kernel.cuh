@@ -268,12 +268,8 @@ native_kernel(const LaunchArgs a) {
             }
             // next sim: claimed from a global counter (dynamic balance -- a segment that drew short
             // races takes more of them), one atomic per warp for all its finishing segments
-            const unsigned lead = __ballot_sync(0xffffffffu, seg_done && l == 0);
-            const int first = __ffs(lead) - 1;
-            unsigned long long got = 0;
-            if (lane == first) got = atomicAdd(a.work, (unsigned long long)__popc(lead));
-            got = __shfl_sync(0xffffffffu, got, first);
-            if (seg_done) s = segs_total + (int64_t)got + __popc(lead & ((1u << base) - 1u));
+            const int64_t next = claim_next_sim(seg_done, l == 0, base, segs_total, a.work);
+            if (seg_done) s = next;
             load_sim(seg_done);
         }
         if (!__any_sync(0xffffffffu, running)) break;
@@ -438,14 +434,7 @@ native_kernel(const LaunchArgs a) {
             atomicMax((unsigned long long*)&a.tally[ct_at + 4], encode_first(first_div));
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        // every claim of this block precedes this point; the last block out re-zeroes the counters
-        __threadfence();
-        if (atomicAdd(a.work + 1, 1ull) == gridDim.x - 1) {
-            a.work[0] = 0ull;
-            a.work[1] = 0ull;
-        }
-    }
+    if (threadIdx.x == 0) release_work(a.work);
     for (int i = threadIdx.x; i < hist_len; i += blockDim.x) {
         const unsigned long long v = s_hist[i];
         if (v) atomicAdd((unsigned long long*)&a.tally[i], v);
