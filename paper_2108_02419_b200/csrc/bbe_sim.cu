@@ -698,6 +698,8 @@ static int build_args(const Plan& pl, const bbe_race* race, const bbe_state* st,
     a.shift = fr.shift;
     a.key_base = fr.key_base;
     a.key_bits = fr.key_bits;
+    a.key_mul = 1u << fr.key_bits;
+    a.key_nmul = 0u - a.key_mul;
     philox_round_keys(rq->seed, a.rk);
     a.n = race->n;
     a.W = pl.W;

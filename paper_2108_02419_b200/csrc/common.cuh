@@ -62,6 +62,7 @@ struct LaunchArgs {
     float shift;      // NATIVE: positions, L and breakpoints are offset by this (the front-runner frame)
     uint32_t key_base;  // NATIVE: front-runner key = float bits of a position - key_base
     int key_bits;       // NATIVE: index bits packed under the key
+    uint32_t key_mul, key_nmul;  // NATIVE: 2^key_bits and -2^key_bits (runtime values: IMAD, not shifts)
     int n, W, S, WP, from_start, scan, perms;
     double L;
     int64_t tick0;

@@ -27,11 +27,7 @@
 namespace bbe {
 
 // Build-time variants for A/B measurement (tools/ab_build.sh); the defaults are the measured best
-// (C2 on B200: vote-based front recovery 0.474 ms, split limit check 0.443 ms, neither 0.437 ms;
-// 10 blocks/SM at 51 registers 0.483 ms).
-#ifndef BBE_SPLIT_LIMIT
-#define BBE_SPLIT_LIMIT 0
-#endif
+// (C2 on B200, round-1 kernel: 10 blocks/SM at 51 registers 0.483 ms vs 0.437 ms).
 #ifndef BBE_SPREAD_TAIL
 #define BBE_SPREAD_TAIL 1
 #endif
@@ -134,7 +130,7 @@ native_kernel(const LaunchArgs a) {
     // front-runner values: key = bits(pos) - key_base in [1, 2^(31-b)) for a racing competitor (the
     // host picks the frame: bbe_sim.cu native_frame), b = a.key_bits index bits
     const int kbits = a.key_bits;
-    const uint32_t mulb = 1u << kbits, lowmask = mulb - 1u, nmulb = 0u - mulb;
+    const uint32_t mulb = a.key_mul, lowmask = mulb - 1u, nmulb = a.key_nmul;  // 2^b, -2^b: one IMAD each
     const uint32_t cl = (uint32_t)l - a.key_base * mulb;       // v = bits * 2^b + cl = (key << b) | l
     const uint32_t cn = a.key_base * mulb - lowmask - 1u;      // ~v' = bits * -2^b + cn, v' = v | lowmask
 
@@ -185,6 +181,14 @@ native_kernel(const LaunchArgs a) {
 
     while (true) {
         // ---------------- block boundary ----------------
+        // Tick limit (race.py:381-386 / 402-404): the reference refuses the tick after `limit`.  Blocks
+        // run whole, so a sim is diverged iff, once rt >= limit, a competitor racing at its start is
+        // still racing or finished after tick `limit` -- exactly the sims the reference rejects.
+        if (rt >= a.limit) {
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                if (started[k] && fin[k] > a.limit) fin[k] = kDiverged;
+        }
         bool live = false, dv = false;
 #pragma unroll
         for (int k = 0; k < K; ++k) { live |= fin[k] == kRacing; dv |= fin[k] == kDiverged; }
@@ -295,18 +299,10 @@ native_kernel(const LaunchArgs a) {
         }
 
         // ---------------- 4 synchronous ticks ----------------
-        // The tick-limit check (race.py:381-386 / 402-404) can only fire in a block that reaches the
-        // limit; every other block runs the tick without it.
-        auto tick = [&](const int tj, auto check_limit) {
+        auto tick = [&](const int tj) {
             bool racing[K];
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                racing[k] = fin[k] == kRacing;
-                if (decltype(check_limit)::value && racing[k] && rt >= a.limit) {
-                    fin[k] = kDiverged;
-                    racing[k] = false;
-                }
-            }
+            for (int k = 0; k < K; ++k) racing[k] = fin[k] == kRacing;
 
             // ---- front runner: nearest key strictly ahead, lowest index on ties (race.py:244-264) ----
             // Published value v = (key << b) | j; lane c keeps min over its segment of
@@ -392,28 +388,24 @@ native_kernel(const LaunchArgs a) {
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 const bool early = pos[k] < bp[k];
-                const float m = (pf[k] < prev[k]) ? pf[k] : prev[k];  // Python min(prev_c, prev_front)
+                // Python min(prev_c, prev_front): steps are positive, so fminf returns the same value
+                const float m = fminf(prev[k], pf[k]);
                 const float step = __fmul_rn(fr[k] ? (early ? rpE[k] : rpL[k]) : (early ? eE[k] : eL[k]),
                                              fr[k] ? rawd[k][tj] : m);
                 float p = __fadd_rn(pos[k], step);
                 // positions are >= +0.0, so the next float up is the next bit pattern (race.py:310-313)
                 p = (p == pos[k]) ? __uint_as_float(__float_as_uint(p) + 1u) : p;
-                if (racing[k]) {
-                    pos[k] = p;
-                    prev[k] = step;
-                    blk_sim += bl[k] ? 1u : 0u;
-                    if (p >= L) fin[k] = rt + 1;
-                }
+                // branch-free: only racing competitors move
+                const bool done = racing[k] && p >= L;
+                pos[k] = racing[k] ? p : pos[k];
+                prev[k] = racing[k] ? step : prev[k];
+                blk_sim += bl[k] ? 1u : 0u;
+                fin[k] = done ? rt + 1 : fin[k];
             }
             rt += 1;
         };
-        if (!BBE_SPLIT_LIMIT || __any_sync(0xffffffffu, running && rt + kTicksPerBlock > a.limit)) {
 #pragma unroll
-            for (int tj = 0; tj < kTicksPerBlock; ++tj) tick(tj, std::true_type{});
-        } else {
-#pragma unroll
-            for (int tj = 0; tj < kTicksPerBlock; ++tj) tick(tj, std::false_type{});
-        }
+        for (int tj = 0; tj < kTicksPerBlock; ++tj) tick(tj);
     }
 
     // ---------------- flush ----------------
