@@ -29,7 +29,8 @@
 //           pending competitor reads its words at the offset it would have if each pending lognormal
 //           draw accepted its next Kinderman-Monahan trial; draws before the first rejection are
 //           final.  The whole warp twists a segment's block when its unread window runs low (the
-//           unread tail moves to a side buffer first, so early twists leave the stream unchanged).
+//           unread words move to a side buffer just below the block first, so the window stays
+//           contiguous and early twists leave the stream unchanged).
 #pragma once
 
 #include <type_traits>
@@ -63,9 +64,12 @@ exact_kernel(const LaunchArgs a) {
     const int l = lane - seg * W;
     const unsigned segmask = lane_on ? ((W == 32 ? 0xffffffffu : ((1u << W) - 1u)) << base) : 0u;
     const unsigned lt_mask = (1u << lane) - 1u;
-    uint32_t* const mt = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) +
-                         (warp * S + (lane_on ? seg : 0)) * kSeg;  // MT: this segment's state
-    uint32_t* const side = mt + kMtWords;  // MT: unread words saved across an early twist
+    // MT: this segment's words: [side buffer: kSide][current block: 624]; the unread stream is the
+    // contiguous window seg_mt[wp, kSeg)
+    constexpr int kSide = mt_side_words(K);
+    uint32_t* const seg_mt = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) +
+                             (warp * S + (lane_on ? seg : 0)) * kSeg;
+    uint32_t* const mt = seg_mt + kSide;  // the 624-word MT19937 block
     // start-of-tick positions, per warp: [parity][slot][segment * WP2 + lane-in-segment], pads -inf
     const int WP2 = (W + 1) & ~1;
     double* const xrows = reinterpret_cast<double*>(
@@ -114,8 +118,7 @@ exact_kernel(const LaunchArgs a) {
     const int64_t start = a.tick0;
     int32_t rt = 0;
     int64_t cursor = 0, cursor_end = 0;  // INJECT
-    int q = kMtWords;                    // MT: CPython's position in the current 624-word block
-    int sp = 0, se = 0;                  // MT: unread words side[sp, se) precede mt[q, 624)
+    int wp = kSeg;                       // MT: start of the unread window seg_mt[wp, kSeg)
     bool running = false, diverged = false, bad = false;
 
     double pos[K], prev[K], pv[K];
@@ -137,7 +140,7 @@ exact_kernel(const LaunchArgs a) {
         while (todo) {
             const int leader = __ffs(todo) - 1;
             todo &= todo - 1u;
-            uint32_t* const t = warp_mt + (leader / W) * kSeg;
+            uint32_t* const t = warp_mt + (leader / W) * kSeg + kSide;
             for (int c0 = 0; c0 < kMtWords; c0 += kWarp) {
                 const int i = c0 + lane;
                 const bool act = i < kMtWords;
@@ -153,45 +156,32 @@ exact_kernel(const LaunchArgs a) {
             }
         }
     };
-    // The segment's unread stream is a window: side[sp, se) (words saved from the previous block)
-    // followed by mt[q, 624).  Before a round that may read up to 4WK words, a window shorter than
-    // that is topped up: the unread words of the block move to `side` and the block is twisted in
-    // place -- early, but the stream is the same, since the twist reads the whole old block.
+    // The segment's unread stream is the window seg_mt[wp, kSeg): words saved from earlier blocks
+    // followed by the rest of the current block.  Before a round that may read up to 4WK words, a
+    // shorter window is topped up: its words move to the end of the side buffer, just below the
+    // block, and the block is twisted in place -- early, but the stream is the same, since the
+    // twist reads the whole old block.
     auto mt_window_fill = [&]() {
-        const bool low = running && lane_on && (se - sp) + (kMtWords - q) < 4 * W * K;
+        const bool low = running && lane_on && kSeg - wp < 4 * W * K;
         if (!__any_sync(0xffffffffu, low)) return;
-        const int keep = se - sp, tail = kMtWords - q;  // keep + tail < 4WK: at most 4K words per lane
+        const int keep = kSeg - wp;  // < 4WK: at most 4K words per lane
         uint32_t carry[4 * K];
-        int nc = 0;
 #pragma unroll
         for (int t = 0; t < 4 * K; ++t) {
-            const int i = l + t * W;  // new side index
-            carry[t] = 0u;
-            if (low && i < keep + tail) {
-                carry[t] = i < keep ? side[sp + i] : mt[q + i - keep];
-                nc = t + 1;
-            }
+            const int i = l + t * W;
+            carry[t] = (low && i < keep) ? seg_mt[wp + i] : 0u;
         }
         __syncwarp();
 #pragma unroll
-        for (int t = 0; t < 4 * K; ++t)
-            if (t < nc) side[l + t * W] = carry[t];
-        mt_twist(low);  // starts and ends with __syncwarp
-        if (low) {
-            sp = 0;
-            se = keep + tail;
-            q = 0;
+        for (int t = 0; t < 4 * K; ++t) {
+            const int i = l + t * W;
+            if (low && i < keep) seg_mt[kSide - keep + i] = carry[t];
         }
+        mt_twist(low);  // starts and ends with __syncwarp
+        if (low) wp = kSide - keep;
     };
-    auto mt_word = [&](int k) -> uint32_t {  // window offset k -> raw word
-        const int ns = se - sp;
-        return k < ns ? side[sp + k] : mt[min(q + k - ns, kMtWords - 1)];
-    };
-    auto mt_consume = [&](int c) {
-        const int ns = se - sp;
-        if (c <= ns) sp += c;
-        else { q += c - ns; sp = se = 0; }
-    };
+    auto mt_word = [&](int k) -> uint32_t { return seg_mt[min(wp + k, kSeg - 1)]; };  // window offset k
+    auto mt_consume = [&](int c) { wp += c; };
     // One step draw per (slot, lane) with want[k], in competitor-index order within each segment
     // (slot-major, then lane): uniform(lo, hi) = lo + (hi - lo) * random(); scale *
     // lognormvariate(mu, sigma) via the Kinderman-Monahan loop of random.normalvariate
@@ -332,8 +322,7 @@ exact_kernel(const LaunchArgs a) {
             }
             if (MODE == MT && running) {
                 for (int i = l; i < kMtWords; i += W) mt[i] = a.mt_states[s * kMtWords + i];
-                q = kMtWords;  // random.Random(seed): the first draw twists
-                sp = se = 0;
+                wp = kSeg;  // random.Random(seed): the first draw twists
             }
         }
         if (MODE == MT) __syncwarp();
