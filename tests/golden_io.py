@@ -54,3 +54,17 @@ def race_corpus() -> list:
 def c2() -> dict:
     with open(os.path.join(GOLDEN, "c2.json")) as fh:
         return json.load(fh)
+
+
+@functools.lru_cache(None)
+def acceptance() -> dict:
+    """tests/golden/acceptance.json.gz (make_acceptance_golden.py): reference criteria 7 and 8."""
+    with gzip.open(os.path.join(GOLDEN, "acceptance.json.gz"), "rt") as fh:
+        return json.load(fh)
+
+
+def plain_race(spec: dict) -> RaceConfig:
+    """The reference tests' make_race (tests/conftest.py:6-8): n identical U(lo, hi) runners c1..cn."""
+    return RaceConfig(track_length=spec["length"],
+                      competitors=tuple(Competitor(f"c{i + 1}", UniformSteps(spec["lo"], spec["hi"]))
+                                        for i in range(spec["n"])))

@@ -129,3 +129,29 @@ def test_batch_threads_do_not_change_tallies():
     assert (a["wins"] == b["wins"]).all() and (a["ranks"] == b["ranks"]).all()
     assert a["ct"] == b["ct"] and a["blocked"] == b["blocked"]
     assert a["wins"].sum() == 300 and (a["ranks"].sum(axis=0) == 300).all()
+
+
+def test_oracle_reproduces_reference_dry_run_criteria():
+    """Criteria 7 and 8 of the reference's acceptance suite (tests/test_acceptance.py:301-355): the
+    oracle rebuilds the mid-race states and the reference's rp_predict probabilities exactly."""
+    from golden_io import acceptance, plain_race
+
+    g = acceptance()
+    cfg = plain_race(g["c07"]["race"])
+    for case in g["c07"]["cases"]:
+        st = state_from_dict(case["state"])
+        seeds = oracle.rp_seeds(case["agent_seed"], case["d"])
+        out = oracle.batch(cfg, case["d"], state=st, seeds=seeds)
+        assert [(int(w) + 1) / (case["d"] + 2) for w in out["wins"]] == case["probs"]
+    cfg = plain_race(g["c08"]["race"])
+    from paper_2108_02419_b200.seeding import derive_seed
+
+    for r, case in enumerate(g["c08"]["cases"][:150]):
+        tick, pos, prev, fin, _ = oracle.advance_from_start(cfg, derive_seed(8, "run", r), 3)
+        assert tick == case["state"]["tick"] and pos.tolist() == case["state"]["positions"]
+        assert prev.tolist() == case["state"]["prev_steps"]
+        st = state_from_dict(case["state"])
+        for d in (5, 50):
+            seeds = oracle.rp_seeds(derive_seed(8, "agent", r, d), d)
+            out = oracle.batch(cfg, d, state=st, seeds=seeds)
+            assert [(int(w) + 1) / (d + 3) for w in out["wins"]] == case["probs"][str(d)]
