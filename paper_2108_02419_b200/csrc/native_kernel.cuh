@@ -286,14 +286,18 @@ native_kernel(const LaunchArgs a) {
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 const U4 w = philox_rk(U4{blk, (uint32_t)cidx[k], (uint32_t)gs, (uint32_t)(gs >> 32)}, a.rk);
-                if (any_lognorm && lognorm[k]) {
-                    lognormal_pair(w.x, w.y, sg2[k], lmu2[k], rawd[k][0], rawd[k][1]);
-                    lognormal_pair(w.z, w.w, sg2[k], lmu2[k], rawd[k][2], rawd[k][3]);
-                } else {
-                    rawd[k][0] = fmaf(span[k], one_plus_u(w.x), lms[k]);
-                    rawd[k][1] = fmaf(span[k], one_plus_u(w.y), lms[k]);
-                    rawd[k][2] = fmaf(span[k], one_plus_u(w.z), lms[k]);
-                    rawd[k][3] = fmaf(span[k], one_plus_u(w.w), lms[k]);
+                rawd[k][0] = fmaf(span[k], one_plus_u(w.x), lms[k]);
+                rawd[k][1] = fmaf(span[k], one_plus_u(w.y), lms[k]);
+                rawd[k][2] = fmaf(span[k], one_plus_u(w.z), lms[k]);
+                rawd[k][3] = fmaf(span[k], one_plus_u(w.w), lms[k]);
+                if (any_lognorm) {  // warp-uniform: no divergent second copy of the Philox rounds
+                    float l0, l1, l2, l3;
+                    lognormal_pair(w.x, w.y, sg2[k], lmu2[k], l0, l1);
+                    lognormal_pair(w.z, w.w, sg2[k], lmu2[k], l2, l3);
+                    rawd[k][0] = lognorm[k] ? l0 : rawd[k][0];
+                    rawd[k][1] = lognorm[k] ? l1 : rawd[k][1];
+                    rawd[k][2] = lognorm[k] ? l2 : rawd[k][2];
+                    rawd[k][3] = lognorm[k] ? l3 : rawd[k][3];
                 }
             }
         }
