@@ -315,9 +315,10 @@ native_kernel(const LaunchArgs a) {
             // equal keys, rivals behind and finished rivals (v = 0) wrap to >= 2^31.  So the minimum
             // holds the front's key AND its index -- no second pass.
             float gap[K];
+            bool ahead[K];
             int fj[K], fk[K];
 #pragma unroll
-            for (int k = 0; k < K; ++k) { gap[k] = CUDART_INF_F; fj[k] = 0; fk[k] = 0; }
+            for (int k = 0; k < K; ++k) { gap[k] = CUDART_INF_F; ahead[k] = false; fj[k] = 0; fk[k] = 0; }
             if constexpr (scan) {
                 uint32_t kb[K], nk[K];
 #pragma unroll
@@ -357,8 +358,8 @@ native_kernel(const LaunchArgs a) {
                 for (int k = 0; k < K; ++k) {
                     const uint32_t t = best[k] + mulb;  // (dkey << b) | j
                     fj[k] = (int)(t & lowmask);
-                    const bool ahead = best[k] < 0x80000000u;
-                    gap[k] = ahead ? __fsub_rn(__uint_as_float(kb[k] + (t >> kbits)), pos[k]) : CUDART_INF_F;
+                    ahead[k] = best[k] < 0x80000000u;
+                    gap[k] = __fsub_rn(__uint_as_float(kb[k] + (t >> kbits)), pos[k]);  // used only if ahead
                 }
             }
 
@@ -366,7 +367,7 @@ native_kernel(const LaunchArgs a) {
             bool fr[K], bl[K], any_bl = false;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                fr[k] = gap[k] > th[k];
+                fr[k] = !ahead[k] || gap[k] > th[k];
                 bl[k] = racing[k] && !fr[k];
                 any_bl |= bl[k];
             }
