@@ -10,6 +10,8 @@
  *                         agents.py:153-166 rp_predict(state, config, d, rng)      (wins -> (w+1)/(d+n))
  *                         batch.py:110-124 run_batch(BatchConfig)                  (per-sim outputs)
  *                         batch.py:149-170 estimate_pmf / pmf_from_results         (perms tally, n <= 6)
+ *   bbe_simulate_multi    the same over several GPUs (one host thread per device, host-merged
+ *                         tallies): run_batch(BatchConfig(workers=N)), batch.py:120-124.
  *   bbe_simulate_async    the same, device-resident: tallies accumulate into a device buffer on a
  *                         caller stream (used by the multi-GPU path before one NCCL all-reduce).
  *   bbe_derive_seeds      seeding.py:50-59 derive_seed(master, "run", i) for a range of i.
@@ -129,6 +131,16 @@ typedef struct {
 
 int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_state* state,
                  const bbe_request* req, bbe_result* out);
+
+/* bbe_simulate over several GPUs from one host thread -- the run_batch(workers=N) analogue
+ * (batch.py:110-124): the sims are split into `n_parts` contiguous shards (shard_range), part p runs
+ * on device p % bbe_device_count() in its own host thread (parts on one device run in turn), and
+ * the tallies are merged on the host (SUM; first_diverged / first_bad_draws keep the smallest
+ * index).  Per-sim outputs land at their global positions in `out`.  Every per-sim stream is a pure
+ * function of the global sim index, so results are identical for any n_parts.  n_parts <= 0 -> one
+ * part per visible device.  kernel_ms = the slowest part. */
+int bbe_simulate_multi(int32_t n_parts, const bbe_race* race, const bbe_competitor* comps, const bbe_state* state,
+                       const bbe_request* req, bbe_result* out);
 
 /* bbe_simulate split in two: _begin validates, uploads and enqueues everything and returns at once;
  * _end waits and fills `out`.  Host work between the two (e.g. advancing the bettor's stream past

@@ -13,6 +13,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <dlfcn.h>
@@ -866,6 +867,117 @@ int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_st
                  bbe_result* out) {
     const int rc = bbe_simulate_begin(race, comps, st, rq, out);
     return rc ? rc : bbe_simulate_end(out);
+}
+
+int bbe_simulate_multi(int32_t n_parts, const bbe_race* race, const bbe_competitor* comps, const bbe_state* st,
+                       const bbe_request* rq, bbe_result* out) {
+    int rc = validate(race, comps, st, rq);
+    if (rc) return rc;
+    if (!out || !out->wins) return fail(BBE_EINVAL, "result needs a wins buffer");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(BBE_ENODEV, "no CUDA device");
+    }
+    if (n_parts <= 0) n_parts = ndev;
+    const int n = race->n;
+    const int64_t N = rq->n_sims;
+    const int nperm = out->perms ? nperm_for(n) : 0;
+    if (rq->mode == BBE_MODE_INJECT && (!rq->draw_offsets || rq->draw_offsets[0] != 0))
+        return fail(BBE_EINVAL, "draw_offsets must start at 0 and be non-decreasing");
+    struct Part {
+        bbe_request rq;
+        bbe_result res;
+        std::vector<uint64_t> wins, ranks, perms;
+        std::vector<int64_t> offsets;  // INJECT: rebased CSR offsets of the shard
+        int rc = BBE_OK;
+        std::string err;
+    };
+    std::vector<Part> parts(n_parts);
+    const int traj_stride = out->traj_cap > 0 ? (out->traj_cap + 1) * n : 0;
+    for (int p = 0; p < n_parts; ++p) {
+        Part& P = parts[p];
+        const int64_t a = N * p / n_parts, b = N * (p + 1) / n_parts;  // shard_range (parallel.py)
+        P.rq = *rq;
+        P.rq.n_sims = b - a;
+        P.rq.sim_offset = rq->sim_offset + a;
+        if (rq->seeds) P.rq.seeds = rq->seeds + a;
+        if (rq->mode == BBE_MODE_INJECT) {
+            const int64_t base = rq->draw_offsets[a];
+            P.offsets.resize(b - a + 1);
+            for (int64_t i = 0; i <= b - a; ++i) P.offsets[i] = rq->draw_offsets[a + i] - base;
+            P.rq.draws = rq->draws + base;
+            P.rq.draw_offsets = P.offsets.data();
+        }
+        P.wins.assign(n, 0);
+        if (out->ranks) P.ranks.assign((size_t)n * n, 0);
+        if (nperm) P.perms.assign(nperm, 0);
+        P.res = *out;
+        P.res.wins = P.wins.data();
+        P.res.ranks = out->ranks ? P.ranks.data() : nullptr;
+        P.res.perms = nperm ? P.perms.data() : nullptr;
+        if (out->winner) P.res.winner = out->winner + a;
+        if (out->order) P.res.order = out->order + a * n;
+        if (out->finish_ticks) P.res.finish_ticks = out->finish_ticks + a * n;
+        if (out->final_positions) P.res.final_positions = out->final_positions + a * n;
+        if (out->blocked) P.res.blocked = out->blocked + a;
+        if (out->draws_used) P.res.draws_used = out->draws_used + a;
+        if (traj_stride) {
+            P.res.traj_positions = out->traj_positions + a * traj_stride;
+            P.res.traj_prev_steps = out->traj_prev_steps + a * traj_stride;
+        }
+    }
+    // one host thread per device; a device's parts run in order on that thread
+    auto run_device = [&](int d) {
+        if (cudaSetDevice(d) != cudaSuccess) {
+            cudaGetLastError();
+            for (int p = d; p < n_parts; p += ndev) { parts[p].rc = BBE_ECUDA; parts[p].err = "cudaSetDevice failed"; }
+            return;
+        }
+        for (int p = d; p < n_parts; p += ndev) {
+            parts[p].rc = bbe_simulate(race, comps, st, &parts[p].rq, &parts[p].res);
+            if (parts[p].rc != BBE_OK) parts[p].err = bbe_last_error();
+        }
+    };
+    int caller_dev = 0;
+    cudaGetDevice(&caller_dev);
+    std::vector<std::thread> threads;
+    for (int d = 1; d < std::min(ndev, n_parts); ++d) threads.emplace_back(run_device, d);
+    run_device(0);
+    for (auto& t : threads) t.join();
+    cudaSetDevice(caller_dev);
+    // merge (parallel.py reduce_tally on the host)
+    std::fill(out->wins, out->wins + n, 0ull);
+    if (out->ranks) std::fill(out->ranks, out->ranks + (size_t)n * n, 0ull);
+    if (nperm) std::fill(out->perms, out->perms + nperm, 0ull);
+    out->competitor_steps = out->blocked_steps = 0;
+    out->first_diverged = out->first_bad_draws = -1;
+    out->kernel_ms = 0.f;
+    int worst = BBE_OK;
+    std::string worst_err;
+    for (const Part& P : parts) {
+        if (P.rc != BBE_OK && P.rc != BBE_EDIVERGED && P.rc != BBE_EDRAWS) {
+            if (worst == BBE_OK || worst == BBE_EDIVERGED || worst == BBE_EDRAWS) { worst = P.rc; worst_err = P.err; }
+            continue;
+        }
+        for (int c = 0; c < n; ++c) out->wins[c] += P.wins[c];
+        if (out->ranks) for (size_t i = 0; i < (size_t)n * n; ++i) out->ranks[i] += P.ranks[i];
+        if (nperm) for (int i = 0; i < nperm; ++i) out->perms[i] += P.perms[i];
+        out->competitor_steps += P.res.competitor_steps;
+        out->blocked_steps += P.res.blocked_steps;
+        auto keep_min = [](int64_t& acc, int64_t v) { if (v >= 0 && (acc < 0 || v < acc)) acc = v; };
+        keep_min(out->first_diverged, P.res.first_diverged);
+        keep_min(out->first_bad_draws, P.res.first_bad_draws);
+        out->kernel_ms = std::max(out->kernel_ms, P.res.kernel_ms);
+        out->lanes_per_slot = P.res.lanes_per_slot;
+    }
+    if (worst != BBE_OK) return fail(worst, worst_err);
+    if (out->first_diverged >= 0)
+        return fail(BBE_EDIVERGED, "race exceeded tick_limit=" + std::to_string(race->tick_limit) + " in sim " +
+                                       std::to_string(out->first_diverged));
+    if (out->first_bad_draws >= 0)
+        return fail(BBE_EDRAWS, "injected draw stream under/over-consumed in sim " + std::to_string(out->first_bad_draws));
+    return BBE_OK;
 }
 
 int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, const bbe_request* rq,

@@ -41,6 +41,7 @@ EXPORTED_SYMBOLS = (
     "bbe_simulate_begin",
     "bbe_simulate_end",
     "bbe_simulate_async",
+    "bbe_simulate_multi",
     "bbe_tally_len",
     "bbe_tally_offset",
     "bbe_derive_seeds",
@@ -130,6 +131,8 @@ def lib():
         L.bbe_simulate.restype = ctypes.c_int
         L.bbe_simulate_begin.argtypes = L.bbe_simulate.argtypes
         L.bbe_simulate_begin.restype = ctypes.c_int
+        L.bbe_simulate_multi.argtypes = [ctypes.c_int32] + L.bbe_simulate.argtypes
+        L.bbe_simulate_multi.restype = ctypes.c_int
         L.bbe_simulate_end.argtypes = [_P(BbeResult)]
         L.bbe_simulate_end.restype = ctypes.c_int
         L.bbe_simulate_async.argtypes = [_P(BbeRace), _P(BbeCompetitor), _P(BbeState), _P(BbeRequest),
@@ -299,6 +302,7 @@ def simulate_batch(
     winners: bool = False,
     trajectory_ticks: int = 0,
     lanes_per_slot: int = 0,
+    parts: int | None = None,
     _defer: bool = False,
 ) -> SimResult:
     """Run ``n_sims`` independent continuations of ``state`` (or races from the start line when
@@ -312,6 +316,8 @@ def simulate_batch(
     records=True also returns per-sim winner, order, finish ticks, final positions, blocked counts;
     winners=True only the per-sim winner; trajectory_ticks=T (exact modes) positions and previous
     steps after each of the first T ticks of every sim.
+    parts=P splits the sims over the visible GPUs (``bbe_simulate_multi``: P contiguous shards, part p
+    on device p % device_count, 0 = one per device) -- run_batch(workers=...) -- with identical results.
     """
     if mode not in MODES:
         raise ValueError(f"unknown mode {mode!r}")
@@ -355,14 +361,22 @@ def simulate_batch(
                     _ptr(winner, ctypes.c_int32), _ptr(order, ctypes.c_int32), _ptr(fin, ctypes.c_int64),
                     _ptr(fpos, ctypes.c_double), _ptr(blk, ctypes.c_int64), _ptr(used, ctypes.c_int64),
                     0, 0, -1, -1, 0.0, 0, _ptr(tpos, ctypes.c_double), _ptr(tprev, ctypes.c_double), cap, 0)
+    build = (lambda r: SimResult(pk.ids, n_sims, wins, rk, pm, winner, order, fin, fpos, blk, used,
+                                 int(r.competitor_steps), int(r.blocked_steps), float(r.kernel_ms),
+                                 int(r.lanes_per_slot), tpos, tprev))
+    if parts is not None:
+        if _defer:
+            raise ValueError("parts= runs synchronously (one host thread per device)")
+        rc = lib().bbe_simulate_multi(int(parts), ctypes.byref(pk.race), pk.comps, ctypes.byref(st),
+                                      ctypes.byref(req), ctypes.byref(res))
+        if rc != BBE_OK:
+            _raise(rc, res)
+        return build(res)
     rc = lib().bbe_simulate_begin(ctypes.byref(pk.race), pk.comps, ctypes.byref(st), ctypes.byref(req),
                                   ctypes.byref(res))
     if rc != BBE_OK:
         _raise(rc, res)
-    pending = PendingSim(res, (pk, st, keep, req, draws, draw_offsets, seeds),
-                         lambda r: SimResult(pk.ids, n_sims, wins, rk, pm, winner, order, fin, fpos, blk, used,
-                                             int(r.competitor_steps), int(r.blocked_steps), float(r.kernel_ms),
-                                             int(r.lanes_per_slot), tpos, tprev))
+    pending = PendingSim(res, (pk, st, keep, req, draws, draw_offsets, seeds), build)
     return pending if _defer else pending.end()
 
 

@@ -165,3 +165,33 @@ def test_native_front_runner_ties_are_exact(n):
         assert r.final_positions[i].tolist() == o.final_positions.tolist()
         assert r.order[i].tolist() == o.order.tolist()
         assert int(r.blocked[i]) == o.blocked
+
+
+@pytest.mark.parametrize("mode", ["native", "mt", "inject"])
+def test_multi_part_split_is_invisible(mode):
+    """bbe_simulate_multi: any number of parts (mapped round-robin onto the visible GPUs) gives the
+    single-launch tallies and per-sim outputs bit for bit; errors keep the smallest failing index."""
+    cfg = _mixed_field(7)
+    n_sims = 1001
+    kw = {}
+    if mode == "mt":
+        kw = dict(seeds=oracle.rp_seeds(5, n_sims))
+    if mode == "inject":
+        seeds = oracle.rp_seeds(6, n_sims)
+        recs = [oracle.run_race(cfg, int(s), record=True) for s in seeds]
+        offs = np.zeros(n_sims + 1, np.int64)
+        offs[1:] = np.cumsum([r.draws_used for r in recs])
+        kw = dict(draws=np.concatenate([r.draws[: r.draws_used] for r in recs]), draw_offsets=offs)
+    one = sim.simulate_batch(None, cfg, n_sims, 3, mode=mode, records=True, perms=False, **kw)
+    for parts in (1, 3, 8):
+        r = sim.simulate_batch(None, cfg, n_sims, 3, mode=mode, records=True, parts=parts, **kw)
+        assert (r.wins == one.wins).all() and (r.ranks == one.ranks).all()
+        assert r.competitor_steps == one.competitor_steps and r.blocked_steps == one.blocked_steps
+        assert (r.order == one.order).all() and (r.finish_ticks == one.finish_ticks).all()
+        assert (r.final_positions == one.final_positions).all() and (r.blocked == one.blocked).all()
+    # divergence in a later part is reported with its global index
+    slow = RaceConfig(100.0, (Competitor("a", UniformSteps(1.0, 1.0)), Competitor("b", UniformSteps(1.0, 1.0))),
+                      tick_limit=10)
+    with pytest.raises(sim.SimDivergedError) as e:
+        sim.simulate_batch(None, slow, 300, 1, mode="native", sim_offset=40, parts=4)
+    assert e.value.sim_index == 40
