@@ -15,6 +15,7 @@ import random
 
 import numpy as np
 
+from .race import RaceState
 from .sim import _P, lib, simulate_batch, simulate_batch_begin
 
 M64 = (1 << 64) - 1
@@ -106,3 +107,40 @@ def rp_predict(state, config, d: int, rng, *, mode: str = "mt") -> tuple[float, 
         dry_run_seeds(rng, d - 1, want=False)
         res = pending.end()
     return tuple((int(w) + 1) / (d + n) for w in res.wins)
+
+
+# -- the RP / RB bettors' prediction step (agents.py:345-362, 399-404) ----------------------------
+
+
+def reconstruct_state(obs) -> RaceState:
+    """RPBettor._reconstruct_state (agents.py:348-358): the bettor's view of the race from an
+    observation -- previous steps are the last entry of each step history (0.0 before the race)."""
+    prev = [h[-1] if h else 0.0 for h in obs.step_history]
+    return RaceState(obs.race_tick, list(obs.positions), prev, list(obs.finish_ticks))
+
+
+def rb_weight(p: float, gamma: float) -> float:
+    """Inverse-S probability weighting p^g / (p^g + (1-p)^g)^(1/g) (agents.py:234-245)."""
+    if not 0.0 <= p <= 1.0:
+        raise ValueError(f"probability must be in [0, 1], got {p}")
+    if p in (0.0, 1.0) or gamma == 1.0:
+        return p
+    num = p**gamma
+    return num / (num + (1.0 - p) ** gamma) ** (1.0 / gamma)
+
+
+def rb_weighted(probs, gamma: float) -> tuple[float, ...]:
+    """Elementwise rb_weight, renormalised to sum to 1 (agents.py:248-252)."""
+    w = [rb_weight(p, gamma) for p in probs]
+    total = sum(w)
+    return tuple(x / total for x in w)
+
+
+def rp_bettor_predict(obs, config, d: int, rng, *, mode: str = "mt") -> tuple[float, ...]:
+    """RPBettor.predict (agents.py:360-362) with the dry runs on the GPU."""
+    return rp_predict(reconstruct_state(obs), config, d, rng, mode=mode)
+
+
+def rb_bettor_predict(obs, config, d: int, gamma: float, rng, *, mode: str = "mt") -> tuple[float, ...]:
+    """RBBettor.predict (agents.py:402-404): the RP estimate through the inverse-S weighting."""
+    return rb_weighted(rp_bettor_predict(obs, config, d, rng, mode=mode), gamma)

@@ -80,3 +80,26 @@ def test_criterion_01_fuzz_races_terminate_with_monotone_trajectories():
         if checked == 300:
             break
     assert checked == 300
+
+
+@pytest.mark.parametrize("mode", ["mt", "native"])
+def test_rp_and_rb_bettor_predictions(mode):
+    """RPBettor / RBBettor.predict from session observations: MT equals the reference bit for bit
+    and leaves the bettor's stream where the reference leaves it."""
+    from types import SimpleNamespace
+
+    from paper_2108_02419_b200.agents import rb_bettor_predict, rp_bettor_predict
+
+    g = acceptance()["bettors"]
+    cfg = config_from_dict(g["race"])
+    for case in g["cases"]:
+        obs = SimpleNamespace(**case["obs"])
+        rng = make_rng(case["agent_seed"])
+        if case["strategy"] == "rp":
+            p = rp_bettor_predict(obs, cfg, case["d"], rng, mode=mode)
+        else:
+            p = rb_bettor_predict(obs, cfg, case["d"], case["gamma"], rng, mode=mode)
+        assert rng.random() == case["next_random"]
+        assert abs(sum(p) - 1.0) < 1e-12
+        if mode == "mt":
+            assert list(p) == case["probs"]

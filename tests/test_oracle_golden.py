@@ -155,3 +155,30 @@ def test_oracle_reproduces_reference_dry_run_criteria():
             seeds = oracle.rp_seeds(derive_seed(8, "agent", r, d), d)
             out = oracle.batch(cfg, d, state=st, seeds=seeds)
             assert [(int(w) + 1) / (d + 3) for w in out["wins"]] == case["probs"][str(d)]
+
+
+def test_bettor_predictions_via_oracle_match_reference():
+    """RPBettor / RBBettor.predict (agents.py:345-362, 399-404): state reconstruction from the
+    observation + dry runs (oracle) + rb weighting reproduce the reference's probabilities."""
+    import random as _random
+    from types import SimpleNamespace
+
+    from golden_io import acceptance
+    from paper_2108_02419_b200.agents import rb_weighted, reconstruct_state
+
+    g = acceptance()["bettors"]
+    cfg = config_from_dict(g["race"])
+    n = cfg.n_competitors
+    for case in g["cases"]:
+        obs = SimpleNamespace(**case["obs"])
+        st = reconstruct_state(obs)
+        seeds = oracle.rp_seeds(case["agent_seed"], case["d"])
+        out = oracle.batch(cfg, case["d"], state=st, seeds=seeds)
+        probs = tuple((int(w) + 1) / (case["d"] + n) for w in out["wins"])
+        if case["strategy"] == "rb":
+            probs = rb_weighted(probs, case["gamma"])
+        assert list(probs) == case["probs"]
+        rng = _random.Random(case["agent_seed"])
+        for _ in range(case["d"]):
+            rng.getrandbits(64)
+        assert rng.random() == case["next_random"]
