@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -77,10 +78,12 @@ struct DevCtx {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     HostBuf h_params, h_tally;
-    DevBuf d_params, d_tally, d_draws, d_offsets, d_winner, d_order, d_fin, d_fpos, d_blocked, d_dused;
+    DevBuf d_params, d_draws, d_offsets, d_winner, d_order, d_fin, d_fpos, d_blocked, d_dused;
     DevBuf d_seeds, d_mt_states, d_mt_scratch;  // MT mode
     DevBuf d_traj;                               // trajectories (positions, previous steps)
-    DevBuf d_work;                               // NATIVE work counters, a ring of kWorkSlots pairs
+    DevBuf d_work;                               // work counters, a ring of kWorkSlots pairs
+    std::map<std::pair<const void*, size_t>, int> occupancy;  // blocks per SM by (kernel, smem)
+    std::map<const void*, size_t> smem_limit;                // dynamic-smem limit set per kernel
     int work_slot = 0;
     bool mt_table = false;                       // c_mt_init uploaded on this device
     // the call in flight between bbe_simulate_begin and bbe_simulate_end
@@ -405,11 +408,22 @@ int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, co
     pl->smem = smem_bytes(kmode, (TL.hist_len() + 1) & ~1, pl->K, pl->S, pl->WP);
     pl->fn = pick_kernel(rq->mode, pl->K, pl->CH, scan);
     if (!pl->fn) return fail(BBE_EINVAL, "no kernel for this configuration");
-    if (pl->smem > 48 * 1024) {
+    // the kernel's dynamic-smem limit only ever grows (a smaller later request keeps the larger
+    // limit valid); residency per (kernel, dynamic smem) is queried once per device
+    size_t& limit = ctx->smem_limit[(const void*)pl->fn];
+    if (pl->smem > 48 * 1024 && pl->smem > limit) {
         BBE_CK(cudaFuncSetAttribute((const void*)pl->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->smem));
+        limit = pl->smem;
     }
     int per_sm = 0;
-    BBE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl->fn, kBlockThreads, pl->smem));
+    const auto key = std::make_pair((const void*)pl->fn, pl->smem);
+    auto it = ctx->occupancy.find(key);
+    if (it != ctx->occupancy.end()) {
+        per_sm = it->second;
+    } else {
+        BBE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl->fn, kBlockThreads, pl->smem));
+        ctx->occupancy[key] = per_sm;
+    }
     if (per_sm < 1) per_sm = 1;
     const int64_t sims_per_block = (int64_t)(kBlockThreads / kWarp) * pl->S;
     const int64_t need = (rq->n_sims + sims_per_block - 1) / sims_per_block;
@@ -746,14 +760,19 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
     if ((rc = make_plan(ctx, race, comps, rq, out->perms != nullptr, &pl))) return rc;
     cudaStream_t s = ctx->stream;
 
-    // parameters: one pinned staging block, one H2D copy
-    const size_t pbytes = param_bytes(n);
-    BBE_CK(ctx->h_params.ensure(pbytes));
-    BBE_CK(ctx->d_params.ensure(pbytes));
+    // parameters and the zeroed tally: one pinned staging block, one H2D copy
+    const size_t pbytes = (param_bytes(n) + 63) & ~(size_t)63;
+    const size_t tbytes = (size_t)pl.tally_len * sizeof(uint64_t);
+    BBE_CK(cudaEventSynchronize(ctx->ev1));  // a previous async launch on this ctx has read its params
+    BBE_CK(ctx->h_params.ensure(pbytes + tbytes));
+    BBE_CK(ctx->d_params.ensure(pbytes + tbytes));
+    BBE_CK(ctx->h_tally.ensure(tbytes));
     pack_params(race, comps, st, (double*)ctx->h_params.p);
     const NativeFrame fr = native_frame(race, st, pl.W);
     pack_params_f32(race, comps, st, (double*)ctx->h_params.p, fr);
-    BBE_CK(cudaMemcpyAsync(ctx->d_params.p, ctx->h_params.p, pbytes, cudaMemcpyHostToDevice, s));
+    std::memset((char*)ctx->h_params.p + pbytes, 0, tbytes);
+    uint64_t* const d_tally = (uint64_t*)((char*)ctx->d_params.p + pbytes);
+    BBE_CK(cudaMemcpyAsync(ctx->d_params.p, ctx->h_params.p, pbytes + tbytes, cudaMemcpyHostToDevice, s));
 
     const double* d_draws = nullptr;
     const int64_t* d_offsets = nullptr;
@@ -775,10 +794,6 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
         d_seeds = (const uint64_t*)ctx->d_seeds.p;
     }
 
-    const size_t tbytes = (size_t)pl.tally_len * sizeof(uint64_t);
-    BBE_CK(ctx->d_tally.ensure(tbytes));
-    BBE_CK(ctx->h_tally.ensure(tbytes));
-    BBE_CK(cudaMemsetAsync(ctx->d_tally.p, 0, tbytes, s));
 
     bbe_result dev{};
     const size_t nsn = (size_t)ns * n;
@@ -802,13 +817,12 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
     }
 
     LaunchArgs a;
-    build_args(pl, race, st, rq, (const double*)ctx->d_params.p, d_draws, d_offsets, (uint64_t*)ctx->d_tally.p, &dev,
-               fr, &a);
+    build_args(pl, race, st, rq, (const double*)ctx->d_params.p, d_draws, d_offsets, d_tally, &dev, fr, &a);
     BBE_CK(cudaEventRecord(ctx->ev0, s));
     if ((rc = launch_all(ctx, pl, a, comps, d_seeds, rq->seed_master, s))) return rc;
     BBE_CK(cudaEventRecord(ctx->ev1, s));
 
-    BBE_CK(cudaMemcpyAsync(ctx->h_tally.p, ctx->d_tally.p, tbytes, cudaMemcpyDeviceToHost, s));
+    BBE_CK(cudaMemcpyAsync(ctx->h_tally.p, d_tally, tbytes, cudaMemcpyDeviceToHost, s));
     if (out->winner && ns) BBE_CK(cudaMemcpyAsync(out->winner, dev.winner, ns * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     if (out->order && ns) BBE_CK(cudaMemcpyAsync(out->order, dev.order, nsn * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     if (out->finish_ticks && ns)
@@ -988,6 +1002,7 @@ int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const 
     DevCtx* ctx = nullptr;
     if ((rc = get_ctx(&ctx))) return rc;
     std::lock_guard<std::mutex> guard(ctx->mu);
+    if (ctx->pending) return fail(BBE_EINVAL, "a call is already in flight on this device (bbe_simulate_end first)");
     Plan pl;
     const bool perms = nperm_for(race->n) > 0;
     if ((rc = make_plan(ctx, race, comps, rq, perms, &pl))) return rc;

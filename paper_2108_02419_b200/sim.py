@@ -93,27 +93,29 @@ class BbeCompetitor(ctypes.Structure):
 _P = ctypes.POINTER
 
 
+# Pointer members are declared c_void_p (ABI-identical to the header's typed pointers) and set from
+# integer addresses: ndarray.ctypes.data is about half the cost of ctypes.data_as per call.
+_VP = ctypes.c_void_p
+
+
 class BbeState(ctypes.Structure):
-    _fields_ = [("tick", ctypes.c_int64), ("positions", _P(ctypes.c_double)), ("prev_steps", _P(ctypes.c_double)),
-                ("finish_ticks", _P(ctypes.c_int64)), ("from_start", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+    _fields_ = [("tick", ctypes.c_int64), ("positions", _VP), ("prev_steps", _VP),
+                ("finish_ticks", _VP), ("from_start", ctypes.c_int32), ("_pad", ctypes.c_int32)]
 
 
 class BbeRequest(ctypes.Structure):
     _fields_ = [("n_sims", ctypes.c_int64), ("sim_offset", ctypes.c_int64), ("seed", ctypes.c_uint64),
                 ("mode", ctypes.c_int32), ("lanes_per_slot_hint", ctypes.c_int32),
-                ("draws", _P(ctypes.c_double)), ("draw_offsets", _P(ctypes.c_int64)),
-                ("seeds", _P(ctypes.c_uint64)), ("seed_master", ctypes.c_uint64)]
+                ("draws", _VP), ("draw_offsets", _VP), ("seeds", _VP), ("seed_master", ctypes.c_uint64)]
 
 
 class BbeResult(ctypes.Structure):
-    _fields_ = [("wins", _P(ctypes.c_uint64)), ("ranks", _P(ctypes.c_uint64)), ("perms", _P(ctypes.c_uint64)),
-                ("winner", _P(ctypes.c_int32)), ("order", _P(ctypes.c_int32)),
-                ("finish_ticks", _P(ctypes.c_int64)), ("final_positions", _P(ctypes.c_double)),
-                ("blocked", _P(ctypes.c_int64)), ("draws_used", _P(ctypes.c_int64)),
+    _fields_ = [("wins", _VP), ("ranks", _VP), ("perms", _VP), ("winner", _VP), ("order", _VP),
+                ("finish_ticks", _VP), ("final_positions", _VP), ("blocked", _VP), ("draws_used", _VP),
                 ("competitor_steps", ctypes.c_uint64), ("blocked_steps", ctypes.c_uint64),
                 ("first_diverged", ctypes.c_int64), ("first_bad_draws", ctypes.c_int64),
                 ("kernel_ms", ctypes.c_float), ("lanes_per_slot", ctypes.c_int32),
-                ("traj_positions", _P(ctypes.c_double)), ("traj_prev_steps", _P(ctypes.c_double)),
+                ("traj_positions", _VP), ("traj_prev_steps", _VP),
                 ("traj_cap", ctypes.c_int32), ("_pad", ctypes.c_int32)]
 
 
@@ -221,20 +223,28 @@ def _pack_config(config) -> Packed:
     return Packed(race, comps, n, tuple(c.cid for c in config.competitors))
 
 
-def _ptr(a, ct):
-    return None if a is None else a.ctypes.data_as(_P(ct))
+def _ptr(a, ct=None):
+    """Address of an ndarray's data for a c_void_p member (None stays NULL)."""
+    return None if a is None else a.ctypes.data
+
+
+_last_state = (None, None, None)  # (key, BbeState, arrays): a session predicts many times per state
 
 
 def pack_state(state, n: int):
+    global _last_state
     if state is None:
         return BbeState(0, None, None, None, 1, 0), ()
     if len(state.positions) != n or len(state.prev_steps) != n or len(state.finish_ticks) != n:
         raise RaceConfigError("state vectors must have one entry per competitor")
+    key = (state.tick, tuple(state.positions), tuple(state.prev_steps), tuple(state.finish_ticks))
+    if _last_state[0] == key:
+        return _last_state[1], _last_state[2]
     pos = np.ascontiguousarray(state.positions, np.float64)
     prev = np.ascontiguousarray(state.prev_steps, np.float64)
     fin = np.array([-1 if t is None else int(t) for t in state.finish_ticks], np.int64)
-    st = BbeState(int(state.tick), _ptr(pos, ctypes.c_double), _ptr(prev, ctypes.c_double),
-                  _ptr(fin, ctypes.c_int64), 0, 0)
+    st = BbeState(int(state.tick), pos.ctypes.data, prev.ctypes.data, fin.ctypes.data, 0, 0)
+    _last_state = (key, st, (pos, prev, fin))
     return st, (pos, prev, fin)  # keep arrays alive
 
 
