@@ -352,13 +352,13 @@ KernelFn native_for(int ch, bool scan) {
     return scan ? native_for_ch<K, true>(ch) : native_for_ch<K, false>(ch);
 }
 
-KernelFn pick_kernel(int mode, int k, int ch, bool scan) {
+KernelFn pick_kernel(int mode, int k, int ch, bool scan, bool ln) {
     if (mode == BBE_MODE_MT) {
         switch (k) {
-            case 1: return exact_kernel<1, MT>;
-            case 2: return exact_kernel<2, MT>;
-            case 3: return exact_kernel<3, MT>;
-            case 4: return exact_kernel<4, MT>;
+            case 1: return ln ? exact_kernel<1, MT, true> : exact_kernel<1, MT, false>;
+            case 2: return ln ? exact_kernel<2, MT, true> : exact_kernel<2, MT, false>;
+            case 3: return ln ? exact_kernel<3, MT, true> : exact_kernel<3, MT, false>;
+            case 4: return ln ? exact_kernel<4, MT, true> : exact_kernel<4, MT, false>;
         }
     } else if (mode == BBE_MODE_INJECT) {
         switch (k) {
@@ -388,7 +388,11 @@ struct Plan {
 int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, const bbe_request* rq, int want_perms,
               Plan* pl) {
     bool scan = false;  // any theta > 0: the front-runner scan is needed
-    for (int c = 0; c < race->n; ++c) scan = scan || comps[c].theta > 0.0;
+    bool ln = false;    // any lognormal competitor (MT: speculative draw rounds)
+    for (int c = 0; c < race->n; ++c) {
+        scan = scan || comps[c].theta > 0.0;
+        ln = ln || comps[c].family == BBE_FAMILY_LOGNORMAL;
+    }
     const int n = race->n;
     pl->mode = rq->mode;
     pl->n = n;
@@ -406,7 +410,7 @@ int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, co
     pl->tally_len = TL.len();
     const int kmode = rq->mode == BBE_MODE_NATIVE ? NATIVE : (rq->mode == BBE_MODE_MT ? MT : INJECT);
     pl->smem = smem_bytes(kmode, (TL.hist_len() + 1) & ~1, pl->K, pl->S, pl->WP);
-    pl->fn = pick_kernel(rq->mode, pl->K, pl->CH, scan);
+    pl->fn = pick_kernel(rq->mode, pl->K, pl->CH, scan, ln);
     if (!pl->fn) return fail(BBE_EINVAL, "no kernel for this configuration");
     // the kernel's dynamic-smem limit only ever grows (a smaller later request keeps the larger
     // limit valid); residency per (kernel, dynamic smem) is queried once per device

@@ -44,7 +44,9 @@ namespace bbe {
 #define BBE_MT_MINBLOCKS 5  // measured: 1 -> 3.82 ms, 5 -> 3.67 ms, 6 -> 4.41 ms (C2, 100k sims)
 #endif
 
-template <int K, int MODE>
+// LN = false (MT): the field has no lognormal competitor, so every draw takes exactly two words and a
+// tick's offsets follow from one ballot per slot -- no speculative rounds.
+template <int K, int MODE, bool LN = true>
 __global__ void __launch_bounds__(kBlockThreads, MODE == MT ? (K == 1 ? BBE_MT_MINBLOCKS : 2) : 1)
 exact_kernel(const LaunchArgs a) {
     static_assert(MODE == INJECT || MODE == MT, "exact kernel modes");
@@ -187,6 +189,21 @@ exact_kernel(const LaunchArgs a) {
     // lognormvariate(mu, sigma) via the Kinderman-Monahan loop of random.normalvariate
     // (Lib/random.py).  Warp-uniform call.
     auto mt_draws = [&](const bool (&want)[K], double (&d)[K]) {
+        if constexpr (!LN) {
+            // uniform(lo, hi) only: 2 words per draw in competitor-index order (slot-major, then lane)
+            mt_window_fill();
+            int slot_base = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const unsigned m = __ballot_sync(0xffffffffu, want[k]) & segmask;
+                const int off = slot_base + 2 * __popc(m & lt_mask);
+                slot_base += 2 * __popc(m);
+                const uint32_t w0 = mt_temper(mt_word(off)), w1 = mt_temper(mt_word(off + 1));
+                d[k] = want[k] ? __dadd_rn(lo[k], __dmul_rn(span[k], mt_random53(w0, w1))) : 1.0;
+            }
+            if (lane_on && running) mt_consume(slot_base);
+            return;
+        }
         double ln_u1[K], ln_u2[K];  // the accepted Kinderman-Monahan pair of a lognormal competitor
         bool ln_draw[K], pend[K];
         bool any_pend = false;
