@@ -177,6 +177,12 @@ int bbe_mt_getrandbits64(uint32_t* state625, int64_t count, uint64_t* out);
  * `int index; uint32_t state[624]`), writing only the first out_len values (out may be NULL). */
 int bbe_mt_advance64(uint32_t* state624, int32_t* pos, int64_t count, uint64_t* out, int64_t out_len);
 
+/* bbe_mt_advance64 for n_gen independent generators at once (a tick's batch of bettors, each with
+ * its own d), spread over `threads` host threads (<= 0: all cores).  outs / out_lens may be NULL, or
+ * hold per-generator output arrays (NULL entries allowed) and the number of values to store. */
+int bbe_mt_advance64_many(int64_t n_gen, uint32_t* const* states, int32_t* const* pos, const int64_t* counts,
+                          uint64_t* const* outs, const int64_t* out_lens, int32_t threads);
+
 /* 1 if MT mode reproduces the host libm's exp() (used by random.lognormvariate) bit for bit: the
  * library found glibc's exp table in the loaded libm and verified its evaluation against exp().
  * 0 -> lognormal steps in MT mode may differ from the reference in the last bit. */

@@ -85,6 +85,39 @@ def dry_run_seeds(rng, d: int, *, want: bool = True, first_only: bool = False) -
     return np.frombuffer(bits.to_bytes(8 * d, "little"), dtype="<u8").astype(np.uint64) if want else None
 
 
+def dry_run_seeds_many(rngs, ds, out_lens) -> list:
+    """dry_run_seeds for many bettors in one C call (threads over generators): advance rngs[i] by
+    ds[i] getrandbits(64) and return its first out_lens[i] values (None where out_lens[i] == 0).
+
+    Falls back to per-generator calls unless every generator is a plain random.Random with the
+    verified in-place layout."""
+    outs = [np.zeros(int(k), np.uint64) if k else None for k in out_lens]
+    if not all(type(r) is random.Random for r in rngs) or not _inplace_ok():
+        res = []
+        for r, d, k in zip(rngs, ds, out_lens):
+            if k:
+                v = dry_run_seeds(r, d, first_only=(k == 1 and d > 1))
+                res.append(v[:k])
+            else:
+                dry_run_seeds(r, d, want=False)
+                res.append(None)
+        return res
+    m = len(rngs)
+    if m == 0:
+        return []
+    base = np.array([id(r) for r in rngs], np.uint64)
+    states = base + np.uint64(_STATE_OFF)
+    pos = base + np.uint64(_IDX_OFF)
+    counts = np.array([max(int(d), 0) for d in ds], np.int64)
+    optr = np.array([o.ctypes.data if o is not None else 0 for o in outs], np.uint64)
+    olen = np.array([int(k) for k in out_lens], np.int64)
+    rc = lib().bbe_mt_advance64_many(m, states.ctypes.data, pos.ctypes.data, counts.ctypes.data,
+                                     optr.ctypes.data, olen.ctypes.data, 0)
+    if rc != 0:
+        raise RuntimeError("bbe_mt_advance64_many failed")
+    return outs
+
+
 def rp_predict(state, config, d: int, rng, *, mode: str = "mt") -> tuple[float, ...]:
     """Laplace-smoothed win probabilities from d dry-run continuations, computed on the GPU.
 

@@ -91,6 +91,9 @@ struct DevCtx {
     bbe_result* pend_out = nullptr;
     int pend_n = 0, pend_nperm = 0, pend_K = 0;
     int64_t pend_ns = 0, pend_limit = 0;
+    struct Copy { void* dst; const void* src; size_t bytes; };
+    std::vector<Copy> pend_copies;  // pinned staging -> caller buffers, done in _end
+    HostBuf h_out;                  // pinned staging of per-sim outputs
 };
 
 std::mutex g_ctx_mu;
@@ -495,6 +498,31 @@ int bbe_mt_advance64(uint32_t* state624, int32_t* pos, int64_t count, uint64_t* 
     return BBE_OK;
 }
 
+int bbe_mt_advance64_many(int64_t n_gen, uint32_t* const* states, int32_t* const* pos, const int64_t* counts,
+                          uint64_t* const* outs, const int64_t* out_lens, int32_t threads) {
+    if (n_gen < 0 || (n_gen && (!states || !pos || !counts))) return fail(BBE_EINVAL, "bad arguments");
+    for (int64_t g = 0; g < n_gen; ++g)
+        if (!states[g] || !pos[g] || counts[g] < 0 || *pos[g] < 0 || *pos[g] > 624)
+            return fail(BBE_EINVAL, "bad generator " + std::to_string(g));
+    if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+    int64_t words = 0;
+    for (int64_t g = 0; g < n_gen; ++g) words += counts[g];
+    // below ~64k draws the thread start-up costs more than it saves
+    threads = (int)std::min<int64_t>(threads, std::max<int64_t>(1, std::min<int64_t>(n_gen, words / 65536 + 1)));
+    auto work = [&](int t) {
+        for (int64_t g = t; g < n_gen; g += threads) {
+            uint64_t* o = outs ? outs[g] : nullptr;
+            const int64_t ol = (o && out_lens) ? out_lens[g] : 0;
+            *pos[g] = (int32_t)bbe_host_mt_getrandbits64(states[g], (uint32_t)*pos[g], counts[g], o, o ? ol : 0);
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+    return BBE_OK;
+}
+
 int64_t bbe_param_bytes(int32_t n) {
     if (n < 1 || n > BBE_MAX_COMPETITORS) return -1;
     return (int64_t)param_bytes(n);
@@ -549,6 +577,7 @@ int bbe_derive_seeds(uint64_t master, int64_t first, int64_t count, uint64_t* ou
 }
 
 constexpr int kWorkSlots = 64;  // concurrent native launches per device with their own work counters
+constexpr size_t kMaxStagedBytes = 256ull << 20;  // per-sim outputs staged through pinned memory up to this
 
 static int launch_one(DevCtx* ctx, const Plan& pl, const LaunchArgs& a0, cudaStream_t stream) {
     if (a0.n_sims == 0) return BBE_OK;
@@ -827,18 +856,37 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
     BBE_CK(cudaEventRecord(ctx->ev1, s));
 
     BBE_CK(cudaMemcpyAsync(ctx->h_tally.p, d_tally, tbytes, cudaMemcpyDeviceToHost, s));
-    if (out->winner && ns) BBE_CK(cudaMemcpyAsync(out->winner, dev.winner, ns * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    if (out->order && ns) BBE_CK(cudaMemcpyAsync(out->order, dev.order, nsn * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    if (out->finish_ticks && ns)
-        BBE_CK(cudaMemcpyAsync(out->finish_ticks, dev.finish_ticks, nsn * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    if (out->final_positions && ns)
-        BBE_CK(cudaMemcpyAsync(out->final_positions, dev.final_positions, nsn * sizeof(double), cudaMemcpyDeviceToHost, s));
-    if (out->blocked && ns) BBE_CK(cudaMemcpyAsync(out->blocked, dev.blocked, ns * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    if (dev.draws_used && ns)
-        BBE_CK(cudaMemcpyAsync(out->draws_used, dev.draws_used, ns * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    if (traj_elems) {
-        BBE_CK(cudaMemcpyAsync(out->traj_positions, dev.traj_positions, traj_elems * sizeof(double), cudaMemcpyDeviceToHost, s));
-        BBE_CK(cudaMemcpyAsync(out->traj_prev_steps, dev.traj_prev_steps, traj_elems * sizeof(double), cudaMemcpyDeviceToHost, s));
+    // Per-sim outputs go device -> pinned staging asynchronously (a copy into pageable memory would
+    // block this call until the kernel ends); _end copies them into the caller's buffers.  Very
+    // large outputs (trajectories) are copied directly.
+    struct Out { void* dst; const void* src; size_t bytes; };
+    std::vector<Out> outs;
+    if (ns) {
+        if (out->winner) outs.push_back({out->winner, dev.winner, ns * sizeof(int32_t)});
+        if (out->order) outs.push_back({out->order, dev.order, nsn * sizeof(int32_t)});
+        if (out->finish_ticks) outs.push_back({out->finish_ticks, dev.finish_ticks, nsn * sizeof(int64_t)});
+        if (out->final_positions) outs.push_back({out->final_positions, dev.final_positions, nsn * sizeof(double)});
+        if (out->blocked) outs.push_back({out->blocked, dev.blocked, ns * sizeof(int64_t)});
+        if (dev.draws_used) outs.push_back({out->draws_used, dev.draws_used, ns * sizeof(int64_t)});
+        if (traj_elems) {
+            outs.push_back({out->traj_positions, dev.traj_positions, traj_elems * sizeof(double)});
+            outs.push_back({out->traj_prev_steps, dev.traj_prev_steps, traj_elems * sizeof(double)});
+        }
+    }
+    size_t staged = 0;
+    for (const Out& o : outs) staged += (o.bytes + 255) & ~(size_t)255;
+    ctx->pend_copies.clear();
+    if (staged && staged <= kMaxStagedBytes) {
+        BBE_CK(ctx->h_out.ensure(staged));
+        size_t at = 0;
+        for (const Out& o : outs) {
+            char* h = (char*)ctx->h_out.p + at;
+            BBE_CK(cudaMemcpyAsync(h, o.src, o.bytes, cudaMemcpyDeviceToHost, s));
+            ctx->pend_copies.push_back({o.dst, h, o.bytes});
+            at += (o.bytes + 255) & ~(size_t)255;
+        }
+    } else {
+        for (const Out& o : outs) BBE_CK(cudaMemcpyAsync(o.dst, o.src, o.bytes, cudaMemcpyDeviceToHost, s));
     }
     ctx->pending = true;
     ctx->pend_out = out;
@@ -858,6 +906,8 @@ int bbe_simulate_end(bbe_result* out) {
     if (!ctx->pending || ctx->pend_out != out) return fail(BBE_EINVAL, "no call in flight for this result");
     ctx->pending = false;
     BBE_CK(cudaStreamSynchronize(ctx->stream));
+    for (const auto& c : ctx->pend_copies) std::memcpy(c.dst, c.src, c.bytes);
+    ctx->pend_copies.clear();
     const int n = ctx->pend_n;
     const int64_t ns = ctx->pend_ns;
     struct { int nperm, K; } pl{ctx->pend_nperm, ctx->pend_K};

@@ -21,7 +21,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .agents import dry_run_seeds
+from .agents import dry_run_seeds_many
 from .race import RaceState
 from .seeding import derive_seed, spawn_rng
 from .sim import run_race, simulate_batch_begin
@@ -57,20 +57,18 @@ class DryRunDispatcher:
         ds = [max(int(r.d), 0) for r in requests]
         total = sum(ds)
         prep = {"ds": ds, "total": total, "seeds": None, "key": 0}
+        rngs = [r.rng for r in requests]
         if self.mode == "mt":
-            seeds = [dry_run_seeds(r.rng, r.d) for r in requests]
+            seeds = dry_run_seeds_many(rngs, ds, ds)
             if total:
-                prep["seeds"] = np.concatenate([s for s in seeds if len(s)])
+                prep["seeds"] = np.concatenate([s for s in seeds if s is not None and len(s)])
         else:
             # native: the batch's Philox stream is keyed by the first dry-run seed; every other draw
             # only advances its bettor's stream
-            first = True
-            for r in requests:
-                if r.d > 0 and first:
-                    prep["key"] = int(dry_run_seeds(r.rng, r.d, first_only=True)[0])
-                    first = False
-                else:
-                    dry_run_seeds(r.rng, r.d, want=False)
+            first = next((i for i, d in enumerate(ds) if d > 0), None)
+            seeds = dry_run_seeds_many(rngs, ds, [1 if i == first else 0 for i in range(len(ds))])
+            if first is not None:
+                prep["key"] = int(seeds[first][0])
         return prep
 
     def launch(self, state, prep: dict):

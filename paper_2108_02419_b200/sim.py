@@ -54,6 +54,7 @@ EXPORTED_SYMBOLS = (
     "bbe_mt_getrandbits64",
     "bbe_mt_exp_exact",
     "bbe_mt_advance64",
+    "bbe_mt_advance64_many",
 )
 
 
@@ -150,6 +151,9 @@ def lib():
         L.bbe_mt_getrandbits64.argtypes = [_P(ctypes.c_uint32), ctypes.c_int64, _P(ctypes.c_uint64)]
         L.bbe_mt_getrandbits64.restype = ctypes.c_int
         L.bbe_mt_exp_exact.restype = ctypes.c_int
+        L.bbe_mt_advance64_many.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32]
+        L.bbe_mt_advance64_many.restype = ctypes.c_int
         L.bbe_mt_advance64.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, _P(ctypes.c_uint64),
                                        ctypes.c_int64]
         L.bbe_mt_advance64.restype = ctypes.c_int

@@ -109,3 +109,24 @@ def test_no_cpu_fallback_without_gpu():
     cfg = RaceConfig(100.0, (Competitor("a", UniformSteps(1, 2)), Competitor("b", UniformSteps(1, 2))))
     with pytest.raises(sim.BackendUnavailable):
         sim.simulate_batch(None, cfg, 10, 1)
+
+
+def test_batched_stream_advance_matches_sequential_getrandbits():
+    """bbe_mt_advance64_many (a tick's bettors in one call, threads over generators) leaves every
+    generator exactly where d sequential getrandbits(64) calls leave it and returns the values."""
+    import random
+
+    from paper_2108_02419_b200.agents import dry_run_seeds_many
+
+    ds = [0, 1, 7, 311, 1000, 20000] * 6
+    out_lens = [d if i % 3 else min(d, 1) for i, d in enumerate(ds)]
+    a = [random.Random(1000 + i) for i in range(len(ds))]
+    b = [random.Random(1000 + i) for i in range(len(ds))]
+    outs = dry_run_seeds_many(a, ds, out_lens)
+    for r, d, k, o in zip(b, ds, out_lens, outs):
+        vals = [r.getrandbits(64) for _ in range(d)]
+        if k:
+            assert [int(x) for x in o] == vals[:k]
+        else:
+            assert o is None
+    assert all(x.getstate() == y.getstate() for x, y in zip(a, b))
