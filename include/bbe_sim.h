@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define BBE_ABI_VERSION 1
+#define BBE_ABI_VERSION 2
 #define BBE_MAX_COMPETITORS 128
 #define BBE_MAX_PERM_COMPETITORS 6 /* batch.py:27 MAX_FULL_OUTCOME_COMPETITORS */
 
@@ -101,6 +101,9 @@ typedef struct {
      * seed_master, "run", sim_offset + s) as run_batch does */
     const uint64_t* seeds;
     uint64_t seed_master;
+    /* > 0: also count winners per group of group_size consecutive sims (the dry runs of one bettor
+     * in a batched dispatch) into bbe_result.group_wins */
+    int64_t group_size;
 } bbe_request;
 
 /* Outputs.  Tally pointers (host for bbe_simulate) may be NULL except wins. */
@@ -127,6 +130,8 @@ typedef struct {
     double* traj_prev_steps;
     int32_t traj_cap;
     int32_t _pad;
+    /* [ceil(n_sims / group_size) * n] winner counts per group (req.group_size > 0), or NULL */
+    uint64_t* group_wins;
 } bbe_result;
 
 int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_state* state,

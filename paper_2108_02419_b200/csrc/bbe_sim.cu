@@ -162,6 +162,7 @@ int validate(const bbe_race* race, const bbe_competitor* comps, const bbe_state*
             if (!std::isfinite(st->positions[c])) return fail(BBE_EINVAL, "mode native needs finite positions");
     }
     if (rq->n_sims < 0 || rq->sim_offset < 0) return fail(BBE_EINVAL, "n_sims and sim_offset must be >= 0");
+    if (rq->group_size < 0) return fail(BBE_EINVAL, "group_size must be >= 0");
     if (rq->mode == BBE_MODE_INJECT) {
         if (!rq->draws || !rq->draw_offsets) return fail(BBE_EINVAL, "inject mode needs draws and draw_offsets");
     } else if (rq->mode != BBE_MODE_MT && rq->mode != BBE_MODE_NATIVE) {
@@ -722,6 +723,7 @@ static int launch_all(DevCtx* ctx, const Plan& pl, LaunchArgs a, const bbe_compe
         b.sim_offset = off0 + c0;
         b.mt_states = (const uint32_t*)ctx->d_mt_states.p;
         if (b.winner) b.winner += c0;
+        b.group_base = c0;
         if (b.order) b.order += c0 * n;
         if (b.finish_ticks) b.finish_ticks += c0 * n;
         if (b.final_pos) b.final_pos += c0 * n;
@@ -771,6 +773,10 @@ static int build_args(const Plan& pl, const bbe_race* race, const bbe_state* st,
         a.final_pos = dev_out->final_positions;
         a.blocked = dev_out->blocked;
         a.draws_used = dev_out->draws_used;
+        if (rq->group_size > 0 && dev_out->group_wins) {
+            a.group_wins = (unsigned long long*)dev_out->group_wins;
+            a.group_size = rq->group_size;
+        }
         a.traj_pos = dev_out->traj_cap > 0 ? dev_out->traj_positions : nullptr;
         a.traj_prev = dev_out->traj_cap > 0 ? dev_out->traj_prev_steps : nullptr;
         a.traj_cap = dev_out->traj_cap;
@@ -796,16 +802,20 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
     // parameters and the zeroed tally: one pinned staging block, one H2D copy
     const size_t pbytes = (param_bytes(n) + 63) & ~(size_t)63;
     const size_t tbytes = (size_t)pl.tally_len * sizeof(uint64_t);
+    // per-group winner counts (zeroed with the tally)
+    const bool groups = rq->group_size > 0 && out->group_wins && ns > 0;
+    const size_t gbytes = groups ? (size_t)((ns + rq->group_size - 1) / rq->group_size) * n * sizeof(uint64_t) : 0;
     BBE_CK(cudaEventSynchronize(ctx->ev1));  // a previous async launch on this ctx has read its params
-    BBE_CK(ctx->h_params.ensure(pbytes + tbytes));
-    BBE_CK(ctx->d_params.ensure(pbytes + tbytes));
+    BBE_CK(ctx->h_params.ensure(pbytes + tbytes + gbytes));
+    BBE_CK(ctx->d_params.ensure(pbytes + tbytes + gbytes));
     BBE_CK(ctx->h_tally.ensure(tbytes));
     pack_params(race, comps, st, (double*)ctx->h_params.p);
     const NativeFrame fr = native_frame(race, st, pl.W);
     pack_params_f32(race, comps, st, (double*)ctx->h_params.p, fr);
-    std::memset((char*)ctx->h_params.p + pbytes, 0, tbytes);
+    std::memset((char*)ctx->h_params.p + pbytes, 0, tbytes + gbytes);
     uint64_t* const d_tally = (uint64_t*)((char*)ctx->d_params.p + pbytes);
-    BBE_CK(cudaMemcpyAsync(ctx->d_params.p, ctx->h_params.p, pbytes + tbytes, cudaMemcpyHostToDevice, s));
+    uint64_t* const d_groups = groups ? d_tally + pl.tally_len : nullptr;
+    BBE_CK(cudaMemcpyAsync(ctx->d_params.p, ctx->h_params.p, pbytes + tbytes + gbytes, cudaMemcpyHostToDevice, s));
 
     const double* d_draws = nullptr;
     const int64_t* d_offsets = nullptr;
@@ -849,6 +859,7 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
         dev.traj_cap = out->traj_cap;
     }
 
+    dev.group_wins = d_groups;
     LaunchArgs a;
     build_args(pl, race, st, rq, (const double*)ctx->d_params.p, d_draws, d_offsets, d_tally, &dev, fr, &a);
     BBE_CK(cudaEventRecord(ctx->ev0, s));
@@ -868,6 +879,7 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
         if (out->final_positions) outs.push_back({out->final_positions, dev.final_positions, nsn * sizeof(double)});
         if (out->blocked) outs.push_back({out->blocked, dev.blocked, ns * sizeof(int64_t)});
         if (dev.draws_used) outs.push_back({out->draws_used, dev.draws_used, ns * sizeof(int64_t)});
+        if (groups) outs.push_back({out->group_wins, d_groups, gbytes});
         if (traj_elems) {
             outs.push_back({out->traj_positions, dev.traj_positions, traj_elems * sizeof(double)});
             outs.push_back({out->traj_prev_steps, dev.traj_prev_steps, traj_elems * sizeof(double)});
@@ -965,7 +977,10 @@ int bbe_simulate_multi(int32_t n_parts, const bbe_race* race, const bbe_competit
     const int traj_stride = out->traj_cap > 0 ? (out->traj_cap + 1) * n : 0;
     for (int p = 0; p < n_parts; ++p) {
         Part& P = parts[p];
-        const int64_t a = N * p / n_parts, b = N * (p + 1) / n_parts;  // shard_range (parallel.py)
+        // shard_range (parallel.py); with per-group winners, shard edges fall on group edges
+        const int64_t g = (rq->group_size > 0 && out->group_wins) ? rq->group_size : 1;
+        const int64_t ng = (N + g - 1) / g;
+        const int64_t a = std::min(N, ng * p / n_parts * g), b = std::min(N, ng * (p + 1) / n_parts * g);
         P.rq = *rq;
         P.rq.n_sims = b - a;
         P.rq.sim_offset = rq->sim_offset + a;
@@ -984,6 +999,7 @@ int bbe_simulate_multi(int32_t n_parts, const bbe_race* race, const bbe_competit
         P.res.wins = P.wins.data();
         P.res.ranks = out->ranks ? P.ranks.data() : nullptr;
         P.res.perms = nperm ? P.perms.data() : nullptr;
+        if (out->group_wins && rq->group_size > 0) P.res.group_wins = out->group_wins + (a / g) * n;
         if (out->winner) P.res.winner = out->winner + a;
         if (out->order) P.res.order = out->order + a * n;
         if (out->finish_ticks) P.res.finish_ticks = out->finish_ticks + a * n;

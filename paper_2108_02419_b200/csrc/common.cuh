@@ -84,6 +84,8 @@ struct LaunchArgs {
     double* final_pos;
     int64_t* blocked;
     int64_t* draws_used;
+    unsigned long long* group_wins;  // optional [groups][n]: winners of sims (group_base + s) / group_size
+    int64_t group_size, group_base;
 };
 
 // ---- dynamic shared memory ----

@@ -248,6 +248,8 @@ native_kernel(const LaunchArgs a) {
                         if (!has[k]) continue;
                         if (rank[k] == 0) atomicAdd(&s_hist[TL.wins() + cidx[k]], 1ull);
                         atomicAdd(&s_hist[TL.ranks() + cidx[k] * n + rank[k]], 1ull);
+                        if (a.group_wins && rank[k] == 0)
+                            atomicAdd(&a.group_wins[((a.group_base + s) / a.group_size) * n + cidx[k]], 1ull);
                     }
                     if (a.perms && l == 0) atomicAdd(&s_hist[TL.perms() + lehmer], 1ull);
                 }

@@ -77,11 +77,15 @@ class DryRunDispatcher:
             return None
         self.launches += 1
         self.sims += prep["total"]
+        # equal d for every bettor (the session's case): per-bettor winner counts come from the
+        # kernel (group_size = d); otherwise the per-sim winners are split on the host
+        ds = [d for d in prep["ds"] if d > 0]
+        g = ds[0] if len(set(ds)) == 1 else 0
+        kw = dict(group_size=g) if g else dict(winners=True)
         if self.mode == "mt":
             return simulate_batch_begin(state, self.config, prep["total"], mode="mt", seeds=prep["seeds"],
-                                        winners=True, ranks=False)
-        return simulate_batch_begin(state, self.config, prep["total"], prep["key"], mode=self.mode, winners=True,
-                                    ranks=False)
+                                        ranks=False, **kw)
+        return simulate_batch_begin(state, self.config, prep["total"], prep["key"], mode=self.mode, ranks=False, **kw)
 
     def finish(self, pending, prep: dict) -> list[tuple[float, ...]]:
         """Laplace-smoothed win probabilities per request (agents.py:153-166), in request order."""
@@ -89,9 +93,13 @@ class DryRunDispatcher:
         if pending is None:
             return [tuple(1 / (d + n) for _ in range(n)) for d in ds]
         res = pending.end()
-        group = np.repeat(np.arange(len(ds)), ds)
-        wins = np.bincount(group * n + res.winner, minlength=len(ds) * n).reshape(len(ds), n)
-        return [tuple((w + 1) / (d + n) for w in row) for d, row in zip(ds, wins.tolist())]
+        if res.group_wins is not None:
+            rows = iter(res.group_wins.tolist())
+            wins = [next(rows) if d > 0 else [0] * n for d in ds]
+        else:
+            group = np.repeat(np.arange(len(ds)), ds)
+            wins = np.bincount(group * n + res.winner, minlength=len(ds) * n).reshape(len(ds), n).tolist()
+        return [tuple((w + 1) / (d + n) for w in row) for d, row in zip(ds, wins)]
 
     def predict_many(self, state, requests: list[DryRunRequest]) -> list[tuple[float, ...]]:
         """One batched prediction for every request, in request order."""

@@ -36,6 +36,8 @@ MAX_COMPETITORS = 128
 MAX_PERM_COMPETITORS = 6
 M64 = (1 << 64) - 1
 
+ABI_VERSION = 2  # include/bbe_sim.h BBE_ABI_VERSION
+
 EXPORTED_SYMBOLS = (
     "bbe_simulate",
     "bbe_simulate_begin",
@@ -107,7 +109,8 @@ class BbeState(ctypes.Structure):
 class BbeRequest(ctypes.Structure):
     _fields_ = [("n_sims", ctypes.c_int64), ("sim_offset", ctypes.c_int64), ("seed", ctypes.c_uint64),
                 ("mode", ctypes.c_int32), ("lanes_per_slot_hint", ctypes.c_int32),
-                ("draws", _VP), ("draw_offsets", _VP), ("seeds", _VP), ("seed_master", ctypes.c_uint64)]
+                ("draws", _VP), ("draw_offsets", _VP), ("seeds", _VP), ("seed_master", ctypes.c_uint64),
+                ("group_size", ctypes.c_int64)]
 
 
 class BbeResult(ctypes.Structure):
@@ -117,7 +120,7 @@ class BbeResult(ctypes.Structure):
                 ("first_diverged", ctypes.c_int64), ("first_bad_draws", ctypes.c_int64),
                 ("kernel_ms", ctypes.c_float), ("lanes_per_slot", ctypes.c_int32),
                 ("traj_positions", _VP), ("traj_prev_steps", _VP),
-                ("traj_cap", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+                ("traj_cap", ctypes.c_int32), ("_pad", ctypes.c_int32), ("group_wins", _VP)]
 
 
 _lib = None
@@ -164,6 +167,8 @@ def lib():
         L.bbe_device_count.restype = ctypes.c_int
         L.bbe_device_info.argtypes = [ctypes.c_int, ctypes.c_char_p, _P(ctypes.c_int32), _P(ctypes.c_int32)]
         L.bbe_device_info.restype = ctypes.c_int
+        if L.bbe_version() != ABI_VERSION:
+            raise BackendUnavailable(f"{LIB_PATH} has ABI {L.bbe_version()}, expected {ABI_VERSION}: rebuild (make)")
         _lib = L
     return _lib
 
@@ -276,6 +281,7 @@ class SimResult:
     lanes_per_slot: int
     traj_positions: np.ndarray | None = None
     traj_prev_steps: np.ndarray | None = None
+    group_wins: np.ndarray | None = None  # [groups, n] winner counts per group_size consecutive sims
 
     def win_probabilities(self, laplace: bool = True) -> tuple[float, ...]:
         """(w + 1) / (d + n) as agents.py:166, or plain frequencies."""
@@ -317,6 +323,7 @@ def simulate_batch(
     trajectory_ticks: int = 0,
     lanes_per_slot: int = 0,
     parts: int | None = None,
+    group_size: int = 0,
     _defer: bool = False,
 ) -> SimResult:
     """Run ``n_sims`` independent continuations of ``state`` (or races from the start line when
@@ -330,6 +337,8 @@ def simulate_batch(
     records=True also returns per-sim winner, order, finish ticks, final positions, blocked counts;
     winners=True only the per-sim winner; trajectory_ticks=T (exact modes) positions and previous
     steps after each of the first T ticks of every sim.
+    group_size=g also counts winners per group of g consecutive sims (``group_wins``, [groups, n]):
+    one bettor's dry runs in a batched dispatch.
     parts=P splits the sims over the visible GPUs (``bbe_simulate_multi``: P contiguous shards, part p
     on device p % device_count, 0 = one per device) -- run_batch(workers=...) -- with identical results.
     """
@@ -340,7 +349,7 @@ def simulate_batch(
     st, keep = pack_state(state, n)
     n_sims = int(n_sims)
     req = BbeRequest(n_sims, int(sim_offset), int(seed) & M64, MODES[mode], int(lanes_per_slot), None, None, None,
-                     int(seed_master) & M64)
+                     int(seed_master) & M64, int(group_size))
     if mode == "inject":
         draws = np.ascontiguousarray(draws, np.float64)
         draw_offsets = np.ascontiguousarray(draw_offsets, np.int64)
@@ -367,6 +376,9 @@ def simulate_batch(
         fpos = np.zeros((n_sims, n), np.float64)
         blk = np.zeros(n_sims, np.int64)
         used = np.zeros(n_sims, np.int64) if mode == "inject" else None
+    gw = None
+    if group_size > 0:
+        gw = np.zeros(((n_sims + int(group_size) - 1) // int(group_size), n), np.uint64)
     cap = int(trajectory_ticks)
     if cap > 0:
         tpos = np.zeros((n_sims, cap + 1, n), np.float64)
@@ -374,10 +386,11 @@ def simulate_batch(
     res = BbeResult(_ptr(wins, ctypes.c_uint64), _ptr(rk, ctypes.c_uint64), _ptr(pm, ctypes.c_uint64),
                     _ptr(winner, ctypes.c_int32), _ptr(order, ctypes.c_int32), _ptr(fin, ctypes.c_int64),
                     _ptr(fpos, ctypes.c_double), _ptr(blk, ctypes.c_int64), _ptr(used, ctypes.c_int64),
-                    0, 0, -1, -1, 0.0, 0, _ptr(tpos, ctypes.c_double), _ptr(tprev, ctypes.c_double), cap, 0)
+                    0, 0, -1, -1, 0.0, 0, _ptr(tpos, ctypes.c_double), _ptr(tprev, ctypes.c_double), cap, 0,
+                    _ptr(gw))
     build = (lambda r: SimResult(pk.ids, n_sims, wins, rk, pm, winner, order, fin, fpos, blk, used,
                                  int(r.competitor_steps), int(r.blocked_steps), float(r.kernel_ms),
-                                 int(r.lanes_per_slot), tpos, tprev))
+                                 int(r.lanes_per_slot), tpos, tprev, gw))
     if parts is not None:
         if _defer:
             raise ValueError("parts= runs synchronously (one host thread per device)")

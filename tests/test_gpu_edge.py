@@ -195,3 +195,21 @@ def test_multi_part_split_is_invisible(mode):
     with pytest.raises(sim.SimDivergedError) as e:
         sim.simulate_batch(None, slow, 300, 1, mode="native", sim_offset=40, parts=4)
     assert e.value.sim_index == 40
+
+
+@pytest.mark.parametrize("mode", ["native", "mt"])
+def test_group_wins_equal_per_group_winner_counts(mode):
+    """req.group_size: per-group winner counts from the kernel equal the host split of the per-sim
+    winners (ragged last group, MT seeding chunks, multi-part shards on group edges)."""
+    cfg = _mixed_field(6)
+    n_sims, g = 140_000, 1000  # > one MT seeding chunk (131072)
+    kw = dict(seeds=oracle.rp_seeds(9, n_sims)) if mode == "mt" else {}
+    ref = sim.simulate_batch(None, cfg, n_sims, 5, mode=mode, winners=True, ranks=False, **kw)
+    want = np.bincount((np.arange(n_sims) // g) * 6 + ref.winner, minlength=((n_sims + g - 1) // g) * 6)
+    r = sim.simulate_batch(None, cfg, n_sims, 5, mode=mode, ranks=False, group_size=g, **kw)
+    assert r.group_wins.reshape(-1).tolist() == want.tolist()
+    r = sim.simulate_batch(None, cfg, 2500, 5, mode=mode, ranks=False, group_size=300, parts=3,
+                           **({"seeds": kw["seeds"][:2500]} if kw else {}))
+    w = sim.simulate_batch(None, cfg, 2500, 5, mode=mode, winners=True, ranks=False,
+                           **({"seeds": kw["seeds"][:2500]} if kw else {})).winner
+    assert r.group_wins.reshape(-1).tolist() == np.bincount((np.arange(2500) // 300) * 6 + w, minlength=9 * 6).tolist()
