@@ -182,7 +182,10 @@ exact_kernel(const LaunchArgs a) {
         mt_twist(low);  // starts and ends with __syncwarp
         if (low) wp = kSide - keep;
     };
-    auto mt_word = [&](int k) -> uint32_t { return seg_mt[min(wp + k, kSeg - 1)]; };  // window offset k
+    // window offset k -> raw word.  No clamp: after mt_window_fill the window holds >= 4WK words and
+    // a round reads below offset 4WK + 4, so an idle lane's read lands at most 3 words past the
+    // segment, inside the block's dynamic shared memory (the next segment or the position rows).
+    auto mt_word = [&](int k) -> uint32_t { return seg_mt[wp + k]; };
     auto mt_consume = [&](int c) { wp += c; };
     // One step draw per (slot, lane) with want[k], in competitor-index order within each segment
     // (slot-major, then lane): uniform(lo, hi) = lo + (hi - lo) * random(); scale *
@@ -222,24 +225,16 @@ exact_kernel(const LaunchArgs a) {
         // the rejected one consumed its 4 words and retries first in the next round.
         while (__any_sync(0xffffffffu, any_pend)) {
             mt_window_fill();
-            // per-slot word counts (<= 4 per lane, <= 128 per slot and segment) packed 8 bits per
-            // slot: one segmented inclusive scan serves all K slots
-            uint32_t need = 0;
-#pragma unroll
-            for (int k = 0; k < K; ++k) need |= (uint32_t)(pend[k] ? (lognorm[k] ? 4 : 2) : 0) << (8 * k);
-            uint32_t incl = need;
-#pragma unroll
-            for (int o = 1; o < kWarp; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (l >= o) incl += v;
-            }
-            const uint32_t tot = __shfl_sync(0xffffffffu, incl, lane_on ? base + W - 1 : lane);
+            // offsets: a pending competitor takes 2 words, +2 more if lognormal -- two ballots per
+            // slot give every lane its segment-local prefix
             int off[K];
             int slot_base = 0;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                off[k] = slot_base + (int)(((incl - need) >> (8 * k)) & 0xffu);
-                slot_base += (int)((tot >> (8 * k)) & 0xffu);
+                const unsigned pm = __ballot_sync(0xffffffffu, pend[k]) & segmask;
+                const unsigned lm = __ballot_sync(0xffffffffu, pend[k] && lognorm[k]) & segmask;
+                off[k] = slot_base + 2 * (__popc(pm & lt_mask) + __popc(lm & lt_mask));
+                slot_base += 2 * (__popc(pm) + __popc(lm));
             }
             const int used_all = slot_base;  // the whole round's words
             uint32_t w[K][4];
