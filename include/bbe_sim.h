@@ -18,7 +18,8 @@
  *   bbe_last_error        -- (error text for the Python exceptions of race.py:27-32, batch.py:30-38)
  *
  * All types are plain C; no torch or CUDA types appear.  Host pointers are caller-owned and only
- * touched during the call.  Calls on one device are serialised by the library.
+ * touched during the call.  Calls are thread-safe: concurrent calls on one device each lease their
+ * own context (stream + staging buffers) from a per-device pool.
  *
  * Return codes: BBE_OK, BBE_EINVAL (-> RaceConfigError), BBE_EDIVERGED (-> RaceDivergedError /
  * BatchRunError(first_diverged)), BBE_EDRAWS (inject stream under/over-consumed), BBE_ECUDA,
@@ -149,8 +150,9 @@ int bbe_simulate_multi(int32_t n_parts, const bbe_race* race, const bbe_competit
 
 /* bbe_simulate split in two: _begin validates, uploads and enqueues everything and returns at once;
  * _end waits and fills `out`.  Host work between the two (e.g. advancing the bettor's stream past
- * the other d-1 dry-run seeds) overlaps the kernel.  One call in flight per device; the host
- * buffers of `out` (and the request's inputs) must stay valid until _end returns. */
+ * the other d-1 dry-run seeds) overlaps the kernel.  Any number of calls may be in flight (each holds
+ * its own stream and staging buffers; `out` identifies the call); the host buffers of `out` (and the
+ * request's inputs) must stay valid until _end returns. */
 int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const bbe_state* state,
                        const bbe_request* req, bbe_result* out);
 int bbe_simulate_end(bbe_result* out);

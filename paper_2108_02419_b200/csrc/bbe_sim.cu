@@ -71,7 +71,7 @@ struct HostBuf {
 };
 
 struct DevCtx {
-    std::mutex mu;
+    bool busy = false;  // leased to one call (bbe_simulate_begin .. _end, or one async launch)
     int dev = -1;
     bool ready = false;
     int sm_count = 0;
@@ -96,10 +96,26 @@ struct DevCtx {
     HostBuf h_out;                  // pinned staging of per-sim outputs
 };
 
+// Contexts (stream, events, staging buffers) are pooled per device and leased to one call at a
+// time, so host threads can call concurrently: each call takes an idle context or creates one.
 std::mutex g_ctx_mu;
-std::vector<DevCtx*> g_ctx;
+std::vector<std::vector<DevCtx*>> g_pool;  // per device
+thread_local DevCtx* tl_last = nullptr;    // the context of this thread's most recent launch
 
-int get_ctx(DevCtx** out) {
+void release_ctx(DevCtx* c) {
+    std::lock_guard<std::mutex> g(g_ctx_mu);
+    c->busy = false;
+}
+
+struct Lease {  // releases the context unless the call keeps it (a call left in flight)
+    DevCtx* c = nullptr;
+    bool keep = false;
+    ~Lease() {
+        if (c && !keep) release_ctx(c);
+    }
+};
+
+int acquire_ctx(Lease& lease) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
         cudaGetLastError();
@@ -107,10 +123,22 @@ int get_ctx(DevCtx** out) {
     }
     int dev = 0;
     BBE_CK(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> g(g_ctx_mu);
-    if ((int)g_ctx.size() < ndev) g_ctx.resize(ndev, nullptr);
-    if (!g_ctx[dev]) g_ctx[dev] = new DevCtx();
-    DevCtx* c = g_ctx[dev];
+    DevCtx* c = nullptr;
+    {
+        std::lock_guard<std::mutex> g(g_ctx_mu);
+        if ((int)g_pool.size() < ndev) g_pool.resize(ndev);
+        for (DevCtx* p : g_pool[dev])
+            if (!p->busy) {
+                c = p;
+                break;
+            }
+        if (!c) {
+            c = new DevCtx();
+            g_pool[dev].push_back(c);
+        }
+        c->busy = true;
+    }
+    lease.c = c;
     if (!c->ready) {
         c->dev = dev;
         BBE_CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, dev));
@@ -119,7 +147,7 @@ int get_ctx(DevCtx** out) {
         BBE_CK(cudaEventCreate(&c->ev1));
         c->ready = true;
     }
-    *out = c;
+    tl_last = c;
     return BBE_OK;
 }
 
@@ -449,9 +477,8 @@ uint32_t bbe_host_mt_getrandbits64(uint32_t* mt, uint32_t idx, int64_t count, ui
 int bbe_version(void) { return BBE_ABI_VERSION; }
 
 float bbe_last_kernel_ms(void) {
-    DevCtx* ctx = nullptr;
-    if (get_ctx(&ctx)) return -1.f;
-    std::lock_guard<std::mutex> guard(ctx->mu);
+    DevCtx* ctx = tl_last;
+    if (!ctx) return -1.f;
     if (cudaEventSynchronize(ctx->ev1) != cudaSuccess) return -1.f;
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) != cudaSuccess) {
@@ -789,10 +816,9 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
     int rc = validate(race, comps, st, rq);
     if (rc) return rc;
     if (!out || !out->wins) return fail(BBE_EINVAL, "result needs a wins buffer");
-    DevCtx* ctx = nullptr;
-    if ((rc = get_ctx(&ctx))) return rc;
-    std::lock_guard<std::mutex> guard(ctx->mu);
-    if (ctx->pending) return fail(BBE_EINVAL, "a call is already in flight on this device (bbe_simulate_end first)");
+    Lease lease;
+    if ((rc = acquire_ctx(lease))) return rc;
+    DevCtx* const ctx = lease.c;
     const int n = race->n;
     const int64_t ns = rq->n_sims;
     Plan pl;
@@ -907,15 +933,20 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
     ctx->pend_K = pl.K;
     ctx->pend_ns = ns;
     ctx->pend_limit = race->tick_limit;
+    lease.keep = true;  // in flight until bbe_simulate_end(out)
     return BBE_OK;
 }
 
 int bbe_simulate_end(bbe_result* out) {
-    DevCtx* ctx = nullptr;
-    int rc;
-    if ((rc = get_ctx(&ctx))) return rc;
-    std::lock_guard<std::mutex> guard(ctx->mu);
-    if (!ctx->pending || ctx->pend_out != out) return fail(BBE_EINVAL, "no call in flight for this result");
+    Lease lease;
+    {
+        std::lock_guard<std::mutex> g(g_ctx_mu);
+        for (auto& dev_pool : g_pool)
+            for (DevCtx* p : dev_pool)
+                if (p->busy && p->pending && p->pend_out == out) lease.c = p;
+    }
+    if (!lease.c) return fail(BBE_EINVAL, "no call in flight for this result");
+    DevCtx* const ctx = lease.c;
     ctx->pending = false;
     BBE_CK(cudaStreamSynchronize(ctx->stream));
     for (const auto& c : ctx->pend_copies) std::memcpy(c.dst, c.src, c.bytes);
@@ -1069,10 +1100,9 @@ int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const 
     int rc = validate(race, comps, st, rq);
     if (rc) return rc;
     if (!d_tally) return fail(BBE_EINVAL, "d_tally is required");
-    DevCtx* ctx = nullptr;
-    if ((rc = get_ctx(&ctx))) return rc;
-    std::lock_guard<std::mutex> guard(ctx->mu);
-    if (ctx->pending) return fail(BBE_EINVAL, "a call is already in flight on this device (bbe_simulate_end first)");
+    Lease lease;
+    if ((rc = acquire_ctx(lease))) return rc;
+    DevCtx* const ctx = lease.c;
     Plan pl;
     const bool perms = nperm_for(race->n) > 0;
     if ((rc = make_plan(ctx, race, comps, rq, perms, &pl))) return rc;

@@ -201,8 +201,9 @@ def pack_config(config) -> Packed:
     Race configs are frozen dataclasses, so the last packed config is reused when the same object
     comes back (every bettor of a session predicts on the session's one config)."""
     global _last_packed
-    if _last_packed[0] is config:
-        return _last_packed[1]
+    cached = _last_packed  # one read: another thread may replace the cache meanwhile
+    if cached[0] is config:
+        return cached[1]
     pk = _pack_config(config)
     _last_packed = (config, pk)
     return pk
@@ -247,8 +248,9 @@ def pack_state(state, n: int):
     if len(state.positions) != n or len(state.prev_steps) != n or len(state.finish_ticks) != n:
         raise RaceConfigError("state vectors must have one entry per competitor")
     key = (state.tick, tuple(state.positions), tuple(state.prev_steps), tuple(state.finish_ticks))
-    if _last_state[0] == key:
-        return _last_state[1], _last_state[2]
+    cached = _last_state
+    if cached[0] == key:
+        return cached[1], cached[2]
     pos = np.ascontiguousarray(state.positions, np.float64)
     prev = np.ascontiguousarray(state.prev_steps, np.float64)
     fin = np.array([-1 if t is None else int(t) for t in state.finish_ticks], np.int64)

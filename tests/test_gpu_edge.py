@@ -213,3 +213,26 @@ def test_group_wins_equal_per_group_winner_counts(mode):
     w = sim.simulate_batch(None, cfg, 2500, 5, mode=mode, winners=True, ranks=False,
                            **({"seeds": kw["seeds"][:2500]} if kw else {})).winner
     assert r.group_wins.reshape(-1).tolist() == np.bincount((np.arange(2500) // 300) * 6 + w, minlength=9 * 6).tolist()
+
+
+def test_concurrent_host_threads_and_overlapping_calls():
+    """Calls from several host threads (and several begin/end calls in flight from one thread) each
+    lease their own context: results equal the sequential ones."""
+    import threading
+
+    cfg = _mixed_field(8)
+    want = {seed: sim.simulate_batch(None, cfg, 20_000, seed, ranks=True).ranks.copy() for seed in range(8)}
+    got = {}
+
+    def work(seed):
+        got[seed] = sim.simulate_batch(None, cfg, 20_000, seed, ranks=True).ranks
+
+    threads = [threading.Thread(target=work, args=(seed,)) for seed in range(8)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert all((got[s] == want[s]).all() for s in range(8))
+    pend = [sim.simulate_batch_begin(None, cfg, 20_000, seed, ranks=True) for seed in range(3)]
+    for seed, p in reversed(list(enumerate(pend))):
+        assert (p.end().ranks == want[seed]).all()
