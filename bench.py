@@ -191,7 +191,8 @@ def run_reference(args):
 def sweep_configs(args, torch, sim):
     """The other BASELINE.json configs, device-resident NATIVE launches (one warm-up + one timed each):
     C1 = 5 x U(10,20), L=2000 from the start line (1,000 sims, the reference's CPU case, and 10^6);
-    C3 = 20 x U(10,20), L=2000, 10^7 sims; derby20 = derby.json resized to 20, 10^6 sims."""
+    C3 = 20 x U(10,20), L=2000, 10^7 sims; derby20 = derby.json resized to 20, 10^6 sims; C5 = the C3
+    field at 10^9 sims in one launch (the per-GPU shard of the scaling config)."""
     from golden_io import c2, config_from_dict
     from paper_2108_02419_b200.batch import resize_race
     from paper_2108_02419_b200.race import Competitor, RaceConfig, UniformSteps
@@ -204,7 +205,8 @@ def sweep_configs(args, torch, sim):
     runs = [("C1_5x_U10_20_from_start_1e3", uniform_field(5), 1_000),
             ("C1_5x_U10_20_from_start_1e6", uniform_field(5), 1_000_000),
             ("C3_20x_U10_20_from_start_1e7", uniform_field(20), args.c3_sims),
-            ("derby20_from_start_1e6", resize_race(derby5, 20), 1_000_000)]
+            ("derby20_from_start_1e6", resize_race(derby5, 20), 1_000_000),
+            ("C5_20x_U10_20_from_start_1e9", uniform_field(20), args.c5_sims)]
     out = {}
     stream = torch.cuda.current_stream()
     for name, cfg, n_sims in runs:
@@ -410,6 +412,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=2000, help="sims per --impl reference step")
     ap.add_argument("--sweep", type=int, default=1, help="also time the other BASELINE configs (0 = skip)")
     ap.add_argument("--c3-sims", type=int, default=10_000_000)
+    ap.add_argument("--c5-sims", type=int, default=1_000_000_000, help="C5 on this GPU (the per-GPU shard)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup < 3 requested; timing rules want >= 3", file=sys.stderr)

@@ -199,23 +199,28 @@ int validate(const bbe_race* race, const bbe_competitor* comps, const bbe_state*
     return BBE_OK;
 }
 
-// Choose competitors-per-lane K: maximise occupied slots (n * sims-per-warp) / (32 * K); ties -> smaller K.
-int choose_k(int n, int hint) {
-    static const int ks[] = {1, 2, 3, 4};
-    if (hint > 0) {
-        for (int k : ks)
-            if (k == hint && (n + k - 1) / k <= kWarp) return k;
+// Competitors per lane K for the NATIVE kernel (profiles/r1_k_sweep.md: every K timed for n = 1..128,
+// with and without blocking competitors).  util(K) = occupied slots / (32 K) with S = 32 / ceil(n/K)
+// races per warp.  n > 32: the smallest K that fits.  With a front-runner scan (some theta > 0):
+// K = 1, or K = 2 when that fills >= 20 % more slots.  Without: K = 2 (more independent work per
+// lane), K = 1 when it fills > 10 % more slots, K = 3 when that fills > 15 % more than K = 2.
+double slot_util(int n, int k) {
+    const int w = (n + k - 1) / k;
+    if (w > kWarp) return 0.0;
+    return (double)n * (kWarp / w) / (kWarp * k);
+}
+
+int choose_k(int n, bool scan, int hint) {
+    if (hint > 0 && hint <= 4 && (n + hint - 1) / hint <= kWarp) return hint;
+    if (n > kWarp) {
+        for (int k = 2; k <= 4; ++k)
+            if ((n + k - 1) / k <= kWarp) return k;
+        return -1;
     }
-    int best = -1;
-    double best_u = -1;
-    for (int k : ks) {
-        const int w = (n + k - 1) / k;
-        if (w > kWarp) continue;
-        const int s = kWarp / w;
-        const double u = (double)n * s / (kWarp * k);
-        if (u > best_u + 1e-9) { best_u = u; best = k; }
-    }
-    return best;
+    const double u1 = slot_util(n, 1), u2 = slot_util(n, 2), u3 = slot_util(n, 3);
+    if (scan) return u2 >= 1.2 * u1 ? 2 : 1;
+    if (u1 > 1.1 * u2) return 1;
+    return u3 > 1.15 * u2 ? 3 : 2;
 }
 
 void pack_params(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, double* P) {
@@ -275,7 +280,7 @@ size_t param_bytes(int n) { return (size_t)F_COUNT * n * sizeof(double) + (size_
 // NATIVE front-runner frame (native_kernel.cuh): an offset of positions, L and breakpoints, and the
 // key base, such that every racing position p satisfies 1 <= bits(p) - key_base < 2^(31 - key_bits)
 // for the whole race (racing positions only grow and stay below L, or start at their initial value).
-// The offset is 0 whenever the state already fits (C2: positions ~900..2000, 4 index bits).
+// The offset is 0 whenever the state already fits (C2: positions ~900..2000).
 struct NativeFrame {
     float shift;
     uint32_t key_base;
@@ -289,8 +294,10 @@ uint32_t f32_bits(float f) {
 }
 
 NativeFrame native_frame(const bbe_race* race, const bbe_state* st, int W) {
-    NativeFrame fr{0.0f, f32_bits(1.0f) - 1u, 1};
-    while ((1 << fr.key_bits) < W) ++fr.key_bits;
+    // 5 index bits for every layout (W <= 32): the frame, and so every FP32 operation of a sim, is
+    // then the same whatever competitors-per-lane layout runs it
+    (void)W;
+    NativeFrame fr{0.0f, f32_bits(1.0f) - 1u, 5};
     const uint64_t R = 1ull << (31 - fr.key_bits);
     const int n = race->n;
     auto racing = [&](int c) { return st->from_start || st->finish_ticks[c] < 0; };
@@ -428,8 +435,11 @@ int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, co
     const int n = race->n;
     pl->mode = rq->mode;
     pl->n = n;
-    // MT: the fewest slots that fit a warp (every slot adds a speculative word window per lane)
-    pl->K = rq->mode == BBE_MODE_MT ? (n + kWarp - 1) / kWarp : choose_k(n, rq->lanes_per_slot_hint);
+    // exact modes: the fewest slots that fit a warp (an MT slot adds a speculative word window per
+    // lane); NATIVE: the measured layout rule
+    const int k_min = (n + kWarp - 1) / kWarp;
+    if (rq->mode == BBE_MODE_NATIVE) pl->K = choose_k(n, scan, rq->lanes_per_slot_hint);
+    else pl->K = (rq->lanes_per_slot_hint >= k_min && rq->lanes_per_slot_hint <= 4) ? rq->lanes_per_slot_hint : k_min;
     if (pl->K > 4) pl->K = -1;
     if (pl->K < 0) return fail(BBE_EINVAL, "field too large for one warp");
     pl->W = (n + pl->K - 1) / pl->K;

@@ -242,3 +242,21 @@ def test_criterion_10_calibration_gpu_vs_reference():
         detections += chi2_p(ref, other) < ALPHA
     assert false_rejects <= 5, false_rejects
     assert detections >= 95, detections
+
+
+def test_layout_rule_and_layout_invariance_from_the_start():
+    """choose_k picks the measured-best layout (profiles/r1_k_sweep.md) and every layout gives the
+    same per-sim results: the FP32 frame does not depend on it (from-start races included)."""
+    for n, scan, want in ((10, True, 1), (12, True, 2), (20, True, 2), (22, True, 1), (10, False, 2),
+                          (5, False, 1), (24, False, 3), (40, True, 2), (96, False, 3), (128, True, 4)):
+        comps = tuple(Competitor(f"c{i + 1}", UniformSteps(10.0, 20.0), theta=8.0 if (scan and i % 4 == 1) else 0.0)
+                      for i in range(n))
+        cfg = RaceConfig(2000.0, comps)
+        r = sim.simulate_batch(None, cfg, 3000, 11, records=True)
+        assert r.lanes_per_slot == want, (n, scan, r.lanes_per_slot)
+        for k in (1, 2, 3, 4):
+            if -(-n // k) > 32 or k == want:
+                continue
+            o = sim.simulate_batch(None, cfg, 3000, 11, records=True, lanes_per_slot=k)
+            assert (o.order == r.order).all() and (o.finish_ticks == r.finish_ticks).all()
+            assert (o.final_positions == r.final_positions).all() and (o.blocked == r.blocked).all()
