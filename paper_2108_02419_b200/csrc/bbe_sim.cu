@@ -2,9 +2,10 @@
 //
 // Host responsibilities: validate (race.py:175-189 errors), pack the race into a small SoA parameter
 // block (one H2D copy), size a persistent grid to residency on this GPU, launch, and bring tallies
-// (and optional per-sim records) back.  One context per device: cached device buffers, a private
-// stream, and a mutex serialising calls on that device.  No CPU fallback exists: every entry point
-// that needs a GPU returns BBE_ENODEV / BBE_ECUDA when there is none.
+// (and optional per-sim records) back.  Each call leases a context (cached device buffers, pinned
+// staging, a private stream) from a per-device pool, so concurrent host threads never share one.
+// No CPU fallback exists: every entry point that needs a GPU returns BBE_ENODEV / BBE_ECUDA when
+// there is none.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -83,7 +84,6 @@ struct DevCtx {
     DevBuf d_traj;                               // trajectories (positions, previous steps)
     DevBuf d_work;                               // work counters, a ring of kWorkSlots pairs
     std::map<std::pair<const void*, size_t>, int> occupancy;  // blocks per SM by (kernel, smem)
-    std::map<const void*, size_t> smem_limit;                // dynamic-smem limit set per kernel
     int work_slot = 0;
     bool mt_table = false;                       // c_mt_init uploaded on this device
     // the call in flight between bbe_simulate_begin and bbe_simulate_end
@@ -101,6 +101,7 @@ struct DevCtx {
 std::mutex g_ctx_mu;
 std::vector<std::vector<DevCtx*>> g_pool;  // per device
 thread_local DevCtx* tl_last = nullptr;    // the context of this thread's most recent launch
+std::map<std::pair<int, const void*>, size_t> g_smem_limit;  // dynamic-smem limit set per (device, kernel)
 
 void release_ctx(DevCtx* c) {
     std::lock_guard<std::mutex> g(g_ctx_mu);
@@ -257,7 +258,8 @@ void pack_params(const bbe_race* race, const bbe_competitor* comps, const bbe_st
     for (int c = 0; c < n; ++c) {
         double rel = 0.0;
         if (!st->from_start && st->finish_ticks[c] > st->tick) {
-            rel = (double)std::min<int64_t>(st->finish_ticks[c] - st->tick, INT32_MAX - 2);
+            rel = (double)std::min<int64_t>(st->finish_ticks[c] - st->tick, INT32_MAX - 8);  // below the
+                                                                                          // kernels' sentinels
         } else if (!st->from_start && st->finish_ticks[c] >= 0) {
             int greater_distinct = 0;
             for (int d = 0; d < n; ++d) {
@@ -456,10 +458,15 @@ int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, co
     if (!pl->fn) return fail(BBE_EINVAL, "no kernel for this configuration");
     // the kernel's dynamic-smem limit only ever grows (a smaller later request keeps the larger
     // limit valid); residency per (kernel, dynamic smem) is queried once per device
-    size_t& limit = ctx->smem_limit[(const void*)pl->fn];
-    if (pl->smem > 48 * 1024 && pl->smem > limit) {
-        BBE_CK(cudaFuncSetAttribute((const void*)pl->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->smem));
-        limit = pl->smem;
+    if (pl->smem > 48 * 1024) {
+        // the limit is a device-wide attribute of the kernel: tracked per (device, kernel) for all
+        // contexts, and only ever raised
+        std::lock_guard<std::mutex> g(g_ctx_mu);
+        size_t& limit = g_smem_limit[std::make_pair(ctx->dev, (const void*)pl->fn)];
+        if (pl->smem > limit) {
+            BBE_CK(cudaFuncSetAttribute((const void*)pl->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->smem));
+            limit = pl->smem;
+        }
     }
     int per_sm = 0;
     const auto key = std::make_pair((const void*)pl->fn, pl->smem);
