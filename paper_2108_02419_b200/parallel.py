@@ -99,11 +99,14 @@ def encode_first(index: int) -> int:
     return 0 if index < 0 else (2**63 - 1) - index
 
 
-def simulate_sharded(state, config, n_sims: int, seed: int = 0, *, group=None, lanes_per_slot: int = 0) -> Tally:
-    """NATIVE-mode batch over all ranks of ``group`` (one GPU per rank, NCCL).
+def simulate_sharded(state, config, n_sims: int, seed: int = 0, *, group=None, lanes_per_slot: int = 0,
+                     mode: str = "native") -> Tally:
+    """A batch over all ranks of ``group`` (one GPU per rank, NCCL).
 
     Each rank simulates its contiguous shard of [0, n_sims) with global sim indices, the device
-    tallies are all-reduced, and every rank returns the job total.
+    tallies are all-reduced, and every rank returns the job total.  mode="native": Philox keyed by
+    ``seed``; mode="mt": sim i replays the reference's stream random.Random(derive_seed(seed, "run", i))
+    -- run_batch's seeds (batch.py:117-119), so the total equals the reference's batch tallies.
     """
     import torch
     import torch.distributed as dist
@@ -118,7 +121,7 @@ def simulate_sharded(state, config, n_sims: int, seed: int = 0, *, group=None, l
     assert layout.length == launcher.tally_len
     tally = torch.zeros(layout.length, dtype=torch.int64, device="cuda")
     launcher.launch(tally.data_ptr(), hi - lo, seed, sim_offset=lo,
-                    stream=torch.cuda.current_stream().cuda_stream)
+                    stream=torch.cuda.current_stream().cuda_stream, mode=mode)
     if world > 1:
         reduce_tally(tally, layout, group)
     out = decode_tally(tally.cpu().numpy().view(np.uint64), layout)

@@ -501,8 +501,9 @@ class DeviceLauncher:
 
     def launch(self, d_tally_ptr: int, n_sims: int, seed: int, *, sim_offset: int = 0, stream: int = 0,
                mode: str = "native") -> None:
+        # mode "mt": sim i replays random.Random(derive_seed(seed, "run", sim_offset + i)), derived on the GPU
         req = BbeRequest(int(n_sims), int(sim_offset), int(seed) & M64, MODES[mode], self.lanes_per_slot, None,
-                         None, None, 0)
+                         None, None, int(seed) & M64)
         rc = lib().bbe_simulate_async(ctypes.byref(self.pk.race), self.pk.comps, ctypes.byref(self.st),
                                       ctypes.byref(req), None, ctypes.c_void_p(d_tally_ptr),
                                       ctypes.c_void_p(stream))

@@ -208,6 +208,10 @@ def test_simulate_sharded_single_rank_matches_batch():
     r = sim.simulate_batch(st, cfg, 50_000, 3)
     assert (t.wins == r.wins).all() and (t.ranks == r.ranks).all()
     assert t.competitor_steps == r.competitor_steps and t.first_diverged == -1
+    # MT mode: run_batch's per-run seeds, derived on the device -- the reference's own tallies
+    t = simulate_sharded(None, cfg, 3_000, 9, mode="mt")
+    ob = oracle.batch(cfg, 3_000, master=9, threads=8)
+    assert t.wins.tolist() == ob["wins"].tolist() and t.competitor_steps == ob["ct"]
 
 
 def test_criterion_10_calibration_gpu_vs_reference():
