@@ -151,12 +151,16 @@ def live_states(config, master_seed: int):
 
 def run_dry_run_session(config, n_agents: int, d: int, master_seed: int, *, opening_period: float = 5.0,
                         reevaluate_every: float = 1.0, wake_jitter: float = 1.0, mode: str = "mt",
-                        agent_rngs=None) -> DryRunSessionResult:
+                        agent_rngs=None, on_batch=None) -> DryRunSessionResult:
     """C4 without the exchange: n_agents RP bettors, each predicting with d dry runs at every wake.
 
     Time runs as in session.py:271-311: wakes up to the opening period see the pre-race state; then
     each race tick advances the clock by dt and processes the wakes due by then (one launch per
     batch of wakes that share a race state).  Returns every prediction and the end-to-end rate.
+
+    ``on_batch(predictions)`` -- the host's use of a batch (the exchange loop's decisions and order
+    book in a full session) -- runs while the NEXT batch is already on the GPU: the race never depends
+    on the market (session.py:282), so predictions run one batch ahead of the host.
     """
     states = live_states(config, master_seed)
     n_ticks = len(states) - 1
@@ -197,10 +201,17 @@ def run_dry_run_session(config, n_agents: int, d: int, master_seed: int, *, open
     prev = None  # (batch, prepared, pending) in flight
     for state, rnd in work:
         prep = disp.prepare([DryRunRequest(rngs[i], d) for _, i in rnd])
+        done = None
         if prev is not None:
-            preds.extend((t, i, p) for (t, i), p in zip(prev[0], disp.finish(prev[2], prev[1])))
+            done = [(t, i, p) for (t, i), p in zip(prev[0], disp.finish(prev[2], prev[1]))]
+            preds.extend(done)
         prev = (rnd, prep, disp.launch(state, prep))
+        if done is not None and on_batch is not None:
+            on_batch(done)  # overlaps the batch just launched
     if prev is not None:
-        preds.extend((t, i, p) for (t, i), p in zip(prev[0], disp.finish(prev[2], prev[1])))
+        done = [(t, i, p) for (t, i), p in zip(prev[0], disp.finish(prev[2], prev[1]))]
+        preds.extend(done)
+        if on_batch is not None:
+            on_batch(done)
     seconds = time.perf_counter() - t0
     return DryRunSessionResult(preds, disp.launches, disp.sims, seconds, n_ticks)

@@ -153,3 +153,14 @@ def oracle_seed_race():
     from paper_2108_02419_b200.seeding import derive_seed
 
     return derive_seed(20260818, "race")
+
+
+def test_session_host_work_overlaps_the_next_batch():
+    """on_batch (the exchange loop's share of a tick) runs while the next batch is on the GPU: the
+    predictions are unchanged and each batch reaches the callback exactly once, in order."""
+    base = RaceConfig(300.0, tuple(Competitor(f"c{i + 1}", UniformSteps(10.0, 20.0)) for i in range(5)))
+    ref = run_dry_run_session(base, n_agents=20, d=50, master_seed=7, opening_period=3.0)
+    seen = []
+    out = run_dry_run_session(base, n_agents=20, d=50, master_seed=7, opening_period=3.0,
+                              on_batch=lambda batch: seen.extend(batch))
+    assert out.predictions == ref.predictions == seen
