@@ -357,7 +357,8 @@ def run_ours(args):
             return statistics.mean(ts[args.warmup:])
 
         e2e_s = time_calls("native", args.steps)
-        h2d = int(sim.lib().bbe_param_bytes(n))  # the race-parameter block, the call's only H2D input
+        # one H2D per call: the race-parameter block (64-byte aligned) followed by the zeroed tally
+        h2d = ((int(sim.lib().bbe_param_bytes(n)) + 63) // 64) * 64 + launcher.tally_len * 8
         d2h = launcher.tally_len * 8
         # MT mode: the reference's own MT19937 streams, bit-identical results (seeds are H2D inputs)
         mt_steps = max(3, min(args.steps, 20))
