@@ -482,31 +482,32 @@ exact_kernel(const LaunchArgs a) {
 
             // ---- front runner (race.py:244-264): gap = p_i - p_c, strict compares in index order ----
             // Rounding is monotonic, so the reference's smallest gap min_i fl(p_i - p_c) over rivals
-            // strictly ahead equals fl(min_i p_i - p_c): a positional min over the segment's start-of-tick
-            // positions (published to shared memory, finished rivals as -inf) gives the exact gap.
-            // Which rival holds it matters only for a blocked step; that index is found below with the
-            // reference's own gap arithmetic (equal gaps -> lowest index).
-            double gap[K];
+            // strictly ahead equals fl(p* - p_c), p* = the smallest position strictly ahead: one pass
+            // over the segment's start-of-tick positions (shared memory, finished rivals as -inf) keeps
+            // p* and the lowest index holding it (strict compares in index order).  That index is the
+            // reference's front unless a rival further ahead has a gap that rounds to the same double;
+            // rival positions differ by >= ulp(p*), so that needs ulp(p*) <= ulp(gap), impossible when
+            // p* > 2 gap.  Blocked lanes outside that bound (only near a zero start line) rerun the
+            // reference's own gap arithmetic below.
+            double gap[K], best[K];
             int bi[K];
 #pragma unroll
-            for (int k = 0; k < K; ++k) { gap[k] = CUDART_INF; bi[k] = 0; }
+            for (int k = 0; k < K; ++k) { gap[k] = CUDART_INF; best[k] = CUDART_INF; bi[k] = 0; }
             double* const prow = xrows + (tj & 1) * K * kXSlot;
             if (a.scan) {
 #pragma unroll
                 for (int k = 0; k < K; ++k) xw[(tj & 1) * K * kXSlot + k * kXSlot] = pv[k];
                 __syncwarp();
-                double best[K];
-#pragma unroll
-                for (int k = 0; k < K; ++k) best[k] = CUDART_INF;
 #pragma unroll
                 for (int kk = 0; kk < K; ++kk) {
                     const double2* r2 = reinterpret_cast<const double2*>(prow + kk * kXSlot + xseg);
+#pragma unroll 4
                     for (int j = 0; j < WP2 / 2; ++j) {
                         const double2 v = r2[j];
 #pragma unroll
                         for (int k = 0; k < K; ++k) {
-                            best[k] = fmin(best[k], v.x > pos[k] ? v.x : CUDART_INF);
-                            best[k] = fmin(best[k], v.y > pos[k] ? v.y : CUDART_INF);
+                            if (v.x > pos[k] && v.x < best[k]) { best[k] = v.x; bi[k] = (kk << 5) | (2 * j); }
+                            if (v.y > pos[k] && v.y < best[k]) { best[k] = v.y; bi[k] = (kk << 5) | (2 * j + 1); }
                         }
                     }
                 }
@@ -516,27 +517,30 @@ exact_kernel(const LaunchArgs a) {
 
             // ---- step resolution (race.py:267-274) ----
             bool fr[K], bl[K];
-            bool any_blocked = false;
+            bool any_blocked = false, need_exact = false;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 fr[k] = racing[k] && gap[k] > th[k];
                 bl[k] = racing[k] && !fr[k];
                 any_blocked |= bl[k];
+                need_exact |= bl[k] && !(best[k] > __dmul_rn(2.0, gap[k]));
             }
             double pf[K];
 #pragma unroll
             for (int k = 0; k < K; ++k) pf[k] = 0.0;
             if (__any_sync(0xffffffffu, any_blocked)) {
-                // the front: lowest index i (slot-major, then lane) with p_i > p_c and
-                // fl(p_i - p_c) == gap -- race.py:244-264 verbatim, scanned from the top index down
+                if (__any_sync(0xffffffffu, need_exact)) {
+                    // the front: lowest index i (slot-major, then lane) with p_i > p_c and
+                    // fl(p_i - p_c) == gap -- race.py:244-264 verbatim, scanned from the top index down
 #pragma unroll
-                for (int kk = K - 1; kk >= 0; --kk) {
-                    const double* r = prow + kk * kXSlot + xseg;
-                    for (int j = W - 1; j >= 0; --j) {
-                        const double pr = r[j];
+                    for (int kk = K - 1; kk >= 0; --kk) {
+                        const double* r = prow + kk * kXSlot + xseg;
+                        for (int j = W - 1; j >= 0; --j) {
+                            const double pr = r[j];
 #pragma unroll
-                        for (int k = 0; k < K; ++k)
-                            if (pr > pos[k] && __dsub_rn(pr, pos[k]) == gap[k]) bi[k] = (kk << 5) | j;
+                            for (int k = 0; k < K; ++k)
+                                if (pr > pos[k] && __dsub_rn(pr, pos[k]) == gap[k]) bi[k] = (kk << 5) | j;
+                        }
                     }
                 }
 #pragma unroll
