@@ -83,9 +83,10 @@ __device__ __forceinline__ uint32_t mt_mix(uint32_t a, uint32_t b, uint32_t m) {
 }
 
 // random_random(): (a*2^26 + b) * 2^-53 with a = w0>>5, b = w1>>6 -- an exact 53-bit fraction.
+// Evaluated as a * 2^-27 + b * 2^-53: both terms and their sum are exact doubles, so the FMA returns
+// CPython's value bit for bit with two 32-bit conversions instead of a 64-bit integer path.
 __device__ __forceinline__ double mt_random53(uint32_t w0, uint32_t w1) {
-    const uint64_t u = ((uint64_t)(w0 >> 5) << 26) | (uint64_t)(w1 >> 6);
-    return __dmul_rn((double)u, 1.0 / 9007199254740992.0);
+    return __fma_rn((double)(w0 >> 5), 1.0 / 134217728.0, __dmul_rn((double)(w1 >> 6), 1.0 / 9007199254740992.0));
 }
 
 // One thread per sim: random.Random(seed) for a u64 seed = init_by_array(key = 32-bit LE words of
