@@ -333,7 +333,9 @@ exact_kernel(const LaunchArgs a) {
                 cursor_end = a.draw_offsets[s + 1];
             }
             if (MODE == MT && running) {
-                for (int i = l; i < kMtWords; i += W) mt[i] = a.mt_states[s * kMtWords + i];
+                // 624 words = 156 16-byte chunks; the block and each sim's state are 16-byte aligned
+                const uint4* src = reinterpret_cast<const uint4*>(a.mt_states + s * kMtWords);
+                for (int i = l; i < kMtWords / 4; i += W) reinterpret_cast<uint4*>(mt)[i] = __ldg(src + i);
                 wp = kSeg;  // random.Random(seed): the first draw twists
             }
         }
