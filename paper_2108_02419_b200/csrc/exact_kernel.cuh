@@ -237,16 +237,18 @@ exact_kernel(const LaunchArgs a) {
                 slot_base += 2 * (__popc(pm) + __popc(lm));
             }
             const int used_all = slot_base;  // the whole round's words
-            uint32_t w[K][4];
+            double r01[K];  // random() from the first two words: a uniform draw, or a trial's u1
             bool ok[K];
+            uint32_t w23[K][2];
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-#pragma unroll
-                for (int t = 0; t < 4; ++t) w[k][t] = mt_temper(mt_word(off[k] + t));
+                r01[k] = mt_random53(mt_temper(mt_word(off[k])), mt_temper(mt_word(off[k] + 1)));
+                w23[k][0] = mt_temper(mt_word(off[k] + 2));
+                w23[k][1] = mt_temper(mt_word(off[k] + 3));
                 ok[k] = true;
                 if (pend[k] && lognorm[k]) {
-                    const double u1 = mt_random53(w[k][0], w[k][1]);
-                    const double u2 = __dsub_rn(1.0, mt_random53(w[k][2], w[k][3]));
+                    const double u1 = r01[k];
+                    const double u2 = __dsub_rn(1.0, mt_random53(w23[k][0], w23[k][1]));
                     // accept iff z*z/4 <= -log(u2) (Lib/random.py normalvariate).  Decide in FP32 when
                     // the two sides are far apart (relative 1e-4, absolute 1e-5: >25x the FP32 error of
                     // either side), else in FP64 exactly as CPython does -- the same decision either way.
@@ -284,7 +286,7 @@ exact_kernel(const LaunchArgs a) {
                 const bool done = pend[k] && (k < kb || (k == kb && (1u << lane) < first_bad));
                 if (done) {
                     if (lognorm[k]) ln_draw[k] = true;
-                    else d[k] = __dadd_rn(lo[k], __dmul_rn(span[k], mt_random53(w[k][0], w[k][1])));
+                    else d[k] = __dadd_rn(lo[k], __dmul_rn(span[k], r01[k]));
                     pend[k] = false;
                 }
                 any_pend |= pend[k];
