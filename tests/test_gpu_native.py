@@ -167,6 +167,10 @@ def test_full_order_pmf_chi_square_like_compare_pmf():
     cols = [i for i in range(len(keys)) if row_a[i] + row_b[i] > 0]
     stat, p, dof, _ = chi2_contingency([[row_a[i] for i in cols], [row_b[i] for i in cols]], correction=False)
     assert p > ALPHA, (stat, p, dof)
+    # the Lehmer-indexed histogram is layout-independent (2-4 competitors per lane)
+    for k in (2, 3, 4):
+        other = sim.simulate_batch(None, cfg, 400_000, 77, perms=True, lanes_per_slot=k)
+        assert (other.perms == res.perms).all() and (other.ranks == res.ranks).all()
 
 
 def test_sharding_and_lane_layout_invariance():
