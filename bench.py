@@ -259,7 +259,6 @@ def load_traffic():
 
 
 def run_ours(args):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
