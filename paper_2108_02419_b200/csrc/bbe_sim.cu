@@ -393,6 +393,21 @@ KernelFn native_for(int ch, bool scan) {
     return scan ? native_for_ch<K, true>(ch) : native_for_ch<K, false>(ch);
 }
 
+// K = 1 with a scan and W = 4m+1 or 4m+2: rows read 2 words at a time (no padding keys beyond one)
+KernelFn native_vec2_for(int ch) {
+    switch (ch) {
+        case 1: return native_kernel<1, 1, true, 2>;
+        case 3: return native_kernel<1, 3, true, 2>;
+        case 5: return native_kernel<1, 5, true, 2>;
+        case 7: return native_kernel<1, 7, true, 2>;
+        case 9: return native_kernel<1, 9, true, 2>;
+        case 11: return native_kernel<1, 11, true, 2>;
+        case 13: return native_kernel<1, 13, true, 2>;
+        case 15: return native_kernel<1, 15, true, 2>;
+    }
+    return nullptr;
+}
+
 KernelFn pick_kernel(int mode, int k, int ch, bool scan, bool ln) {
     if (mode == BBE_MODE_MT) {
         switch (k) {
@@ -418,6 +433,10 @@ KernelFn pick_kernel(int mode, int k, int ch, bool scan, bool ln) {
     }
     return nullptr;
 }
+
+#ifndef BBE_NATIVE_VEC2
+#define BBE_NATIVE_VEC2 1
+#endif
 
 struct Plan {
     int mode, n, K, W, S, CH, WP, nperm, tally_len;
@@ -447,14 +466,17 @@ int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, co
     pl->W = (n + pl->K - 1) / pl->K;
     if (rq->mode == BBE_MODE_MT) pl->W = std::max(pl->W, 8);  // <= 4 MT states (2.5 KB each) per warp
     pl->S = kWarp / pl->W;
-    pl->CH = (pl->W + 3) / 4;
-    pl->WP = 4 * pl->CH;
+    // NATIVE K = 1 with a scan: 2-word key loads when that avoids padding keys (W % 4 in {1, 2})
+    const bool vec2 = BBE_NATIVE_VEC2 && rq->mode == BBE_MODE_NATIVE && pl->K == 1 && scan &&
+                      ((pl->W + 1) & ~1) < ((pl->W + 3) & ~3);
+    pl->CH = vec2 ? (pl->W + 1) / 2 : (pl->W + 3) / 4;
+    pl->WP = (vec2 ? 2 : 4) * pl->CH;
     pl->nperm = want_perms ? nperm_for(n) : 0;
     TallyLayout TL{n, pl->nperm};
     pl->tally_len = TL.len();
     const int kmode = rq->mode == BBE_MODE_NATIVE ? NATIVE : (rq->mode == BBE_MODE_MT ? MT : INJECT);
     pl->smem = smem_bytes(kmode, (TL.hist_len() + 1) & ~1, pl->K, pl->S, pl->WP);
-    pl->fn = pick_kernel(rq->mode, pl->K, pl->CH, scan, ln);
+    pl->fn = vec2 ? native_vec2_for(pl->CH) : pick_kernel(rq->mode, pl->K, pl->CH, scan, ln);
     if (!pl->fn) return fail(BBE_EINVAL, "no kernel for this configuration");
     // the kernel's dynamic-smem limit only ever grows (a smaller later request keeps the larger
     // limit valid); residency per (kernel, dynamic smem) is queried once per device

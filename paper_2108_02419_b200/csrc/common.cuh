@@ -89,13 +89,16 @@ struct LaunchArgs {
 };
 
 // ---- dynamic shared memory ----
-// NATIVE key rows use a compile-time slot stride: the largest S*WP any W in (4(CH-1), 4CH] needs,
+// NATIVE key rows: a segment's row holds WP = VEC*CH keys (W rounded up to the load width VEC, 4 or
+// 2 words).  The slot stride is compile-time: the largest S*WP any W in (VEC(CH-1), VEC*CH] needs,
 // +4 for a padding word group at the end of every slot row (where lanes without a segment write).
-__host__ __device__ constexpr int swp_max(int CH) {
-    return CH == 1 ? 128 : (CH == 2 ? 48 : (CH == 3 ? 36 : (CH == 4 ? 32 : 4 * CH)));
+__host__ __device__ constexpr int swp_max(int VEC, int CH) {
+    int m = 0;
+    for (int w = VEC * (CH - 1) + 1; w <= VEC * CH && w <= 32; ++w) m = (32 / w) * VEC * CH > m ? (32 / w) * VEC * CH : m;
+    return m;
 }
-__host__ __device__ constexpr int native_slot_words(int CH) { return swp_max(CH) + 4; }
-__host__ __device__ constexpr int native_warp_words(int K, int CH) { return 2 * K * native_slot_words(CH); }
+__host__ __device__ constexpr int native_slot_words(int VEC, int CH) { return swp_max(VEC, CH) + 4; }
+__host__ __device__ constexpr int native_warp_words(int K, int VEC, int CH) { return 2 * K * native_slot_words(VEC, CH); }
 constexpr int kMtWords = 624;
 // side buffer: >= one speculative round's reads (4 words x 32 lanes x K slots)
 __host__ __device__ constexpr int mt_side_words(int K) { return 128 * K; }
@@ -103,7 +106,10 @@ __host__ __device__ constexpr int mt_seg_words(int K) { return kMtWords + mt_sid
 constexpr int kXSlot = 66;         // exact modes: doubles per position row (S*round_up(W,2) <= 64, + pad)
 __host__ __device__ inline size_t smem_bytes(int mode, int hist_len_even, int K, int S, int WP) {
     size_t b = (size_t)hist_len_even * 8;
-    if (mode == NATIVE) b += (size_t)kWarpsPerBlock * native_warp_words(K, (WP + 3) / 4) * 4;
+    if (mode == NATIVE) {
+        const int vec = (WP % 4) ? 2 : 4;  // the host rounds W up to 2 (VEC 2) or 4 (VEC 4)
+        b += (size_t)kWarpsPerBlock * native_warp_words(K, vec, WP / vec) * 4;
+    }
     if (mode == MT) b += (size_t)kWarpsPerBlock * S * mt_seg_words(K) * 4;
     if (mode != NATIVE) b += (size_t)kWarpsPerBlock * 2 * K * kXSlot * 8;
     return b;

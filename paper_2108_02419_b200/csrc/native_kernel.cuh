@@ -70,17 +70,19 @@ __device__ __forceinline__ void lognormal_pair(uint32_t wa, uint32_t wb, float s
 
 // SCAN = false: every theta is 0, so nobody can be blocked (gap > 0 = theta) and the front-runner
 // scan's result would never be used; the kernel then omits it.
-template <int K, int CH, bool SCAN>
+// VEC: key-row load width in words (4: LDS.128, 2: LDS.64 -- fewer padding keys when W % 4 is 1 or 2).
+template <int K, int CH, bool SCAN, int VEC = 4>
 __global__ void __launch_bounds__(kBlockThreads, K == 1 ? BBE_NATIVE_MINBLOCKS_K1 : (K == 2 ? 5 : 3))
 native_kernel(const LaunchArgs a) {
+    static_assert(VEC == 4 || VEC == 2, "key rows are read 4 or 2 words at a time");
     extern __shared__ __align__(16) unsigned long long s_dyn[];
     const TallyLayout TL{a.n, a.perms};
     const int hist_len = TL.hist_len();
     unsigned long long* s_hist = s_dyn;
     for (int i = threadIdx.x; i < hist_len; i += blockDim.x) s_hist[i] = 0ull;
 
-    constexpr int WP = 4 * CH;
-    constexpr int SLOT = native_slot_words(CH);  // words per slot row (segments, then a pad group)
+    constexpr int WP = VEC * CH;
+    constexpr int SLOT = native_slot_words(VEC, CH);  // words per slot row (segments, then a pad group)
     constexpr int PAR = K * SLOT;       // words per parity
     const int n = a.n, W = a.W, S = a.S;
     const int lane = threadIdx.x & (kWarp - 1);
@@ -92,8 +94,8 @@ native_kernel(const LaunchArgs a) {
     const unsigned segmask = lane_on ? ((W == 32 ? 0xffffffffu : ((1u << W) - 1u)) << base) : 0u;
 
     // key rows: [warp][parity][slot][SLOT]; lanes without a segment write the pad word of each row
-    uint32_t* rows = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) + warp * native_warp_words(K, CH);
-    for (int i = lane; i < native_warp_words(K, CH); i += kWarp) rows[i] = 0u;
+    uint32_t* rows = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) + warp * native_warp_words(K, VEC, CH);
+    for (int i = lane; i < native_warp_words(K, VEC, CH); i += kWarp) rows[i] = 0u;
     uint32_t* const wr = rows + (lane_on ? seg * WP + l : SLOT - 1);
     const uint32_t* const rd = rows + (lane_on ? seg * WP : 0);
     __syncthreads();
@@ -333,19 +335,32 @@ native_kernel(const LaunchArgs a) {
                 uint32_t best[K];
 #pragma unroll
                 for (int kk = 0; kk < K; ++kk) {
-                    const uint4* r4 = reinterpret_cast<const uint4*>(rd + (tj & 1) * PAR + kk * SLOT);
                     uint32_t b0[K], b1[K];
 #pragma unroll
                     for (int k = 0; k < K; ++k) { b0[k] = 0xffffffffu; b1[k] = 0xffffffffu; }
+                    if constexpr (VEC == 4) {
+                        const uint4* r4 = reinterpret_cast<const uint4*>(rd + (tj & 1) * PAR + kk * SLOT);
 #pragma unroll
-                    for (int c = 0; c < CH; ++c) {
-                        const uint4 v = r4[c];
+                        for (int c = 0; c < CH; ++c) {
+                            const uint4 v = r4[c];
 #pragma unroll
-                        for (int k = 0; k < K; ++k) {
-                            b0[k] = min(b0[k], v.x + nk[k]);
-                            b1[k] = min(b1[k], v.y + nk[k]);
-                            b0[k] = min(b0[k], v.z + nk[k]);
-                            b1[k] = min(b1[k], v.w + nk[k]);
+                            for (int k = 0; k < K; ++k) {
+                                b0[k] = min(b0[k], v.x + nk[k]);
+                                b1[k] = min(b1[k], v.y + nk[k]);
+                                b0[k] = min(b0[k], v.z + nk[k]);
+                                b1[k] = min(b1[k], v.w + nk[k]);
+                            }
+                        }
+                    } else {
+                        const uint2* r2 = reinterpret_cast<const uint2*>(rd + (tj & 1) * PAR + kk * SLOT);
+#pragma unroll
+                        for (int c = 0; c < CH; ++c) {
+                            const uint2 v = r2[c];
+#pragma unroll
+                            for (int k = 0; k < K; ++k) {
+                                b0[k] = min(b0[k], v.x + nk[k]);
+                                b1[k] = min(b1[k], v.y + nk[k]);
+                            }
                         }
                     }
 #pragma unroll
