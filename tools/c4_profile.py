@@ -1,3 +1,4 @@
+"""cProfile of one C4 dry-run session (100 RP bettors, d = 1000, native): where the host time goes."""
 import cProfile, pstats, sys, os
 sys.path.insert(0,'.'); sys.path.insert(0,'tests')
 from golden_io import c2, config_from_dict

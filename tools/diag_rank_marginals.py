@@ -1,3 +1,5 @@
+"""Rank-marginal diagnostic for a 40-runner derby field: native tallies of every layout K against a
+200k-race oracle batch, and the mean rank of exchangeable siblings (same template)."""
 import sys, math
 sys.path.insert(0,'.'); sys.path.insert(0,'tests')
 import numpy as np

@@ -1,3 +1,4 @@
+"""Small MT-exact rp_predict calls (d = 64 and 1) -- the command behind the per-launch latency list."""
 import sys, random; sys.path.insert(0,'.'); sys.path.insert(0,'tests')
 from golden_io import c2, config_from_dict, state_from_dict
 from paper_2108_02419_b200.agents import rp_predict
