@@ -236,3 +236,32 @@ def test_concurrent_host_threads_and_overlapping_calls():
     pend = [sim.simulate_batch_begin(None, cfg, 20_000, seed, ranks=True) for seed in range(3)]
     for seed, p in reversed(list(enumerate(pend))):
         assert (p.end().ranks == want[seed]).all()
+
+
+def test_mt_multi_slot_divergence_finished_and_trajectories():
+    """K > 1 in the exact kernel: tick-limit divergence, pre-finished competitors and recorded
+    trajectories all follow the reference (oracle) for a 40-runner field."""
+    cfg = _mixed_field(40)
+    # trajectories (run_race(record=True)) from the start line
+    seeds = oracle.rp_seeds(21, 3)
+    r = sim.simulate_batch(None, cfg, 3, mode="mt", seeds=seeds, records=True, trajectory_ticks=400)
+    for i, s in enumerate(seeds):
+        o = oracle.run_race(cfg, int(s))
+        assert r.final_positions[i].tolist() == o.final_positions.tolist()
+        for k in (1, 5, int(o.n_ticks_run) // 2):
+            _, pos, prev, _, _ = oracle.advance_from_start(cfg, int(s), k)
+            assert r.traj_positions[i, k].tolist() == pos.tolist()
+            assert r.traj_prev_steps[i, k].tolist() == prev.tolist()
+    # a state where some runners already finished, continued in MT mode
+    n = 40
+    st = RaceState(9, [62.0 if i % 7 == 0 else 2.0 + 0.5 * (i % 13) for i in range(n)], [3.0] * n,
+                   [8 if i % 7 == 0 else None for i in range(n)])
+    r = sim.simulate_batch(st, cfg, 4, mode="mt", seeds=np.tile(seeds[:2], 2), records=True)
+    for i in range(4):
+        o = oracle.simulate_from(st, cfg, int(seeds[i % 2]))
+        assert r.order[i].tolist() == o.order.tolist() and r.finish_ticks[i].tolist() == o.finish_ticks.tolist()
+    # divergence: the first sim that runs out of ticks is reported by global index
+    tight = RaceConfig(cfg.track_length, cfg.competitors, tick_limit=5)
+    with pytest.raises(sim.SimDivergedError) as e:
+        sim.simulate_batch(None, tight, 6, mode="mt", seeds=oracle.rp_seeds(3, 6), sim_offset=100)
+    assert e.value.sim_index == 100
