@@ -21,8 +21,7 @@
 #include <dlfcn.h>
 
 #include "../../include/bbe_sim.h"
-#include "exact_kernel.cuh"
-#include "native_kernel.cuh"
+#include "kernels.h"
 
 using namespace bbe;
 
@@ -371,69 +370,6 @@ void philox_round_keys(uint64_t seed, uint32_t* rk) {
     }
 }
 
-typedef void (*KernelFn)(LaunchArgs);
-
-template <int K, bool SCAN>
-KernelFn native_for_ch(int ch) {
-    switch (ch) {
-        case 1: return native_kernel<K, 1, SCAN>;
-        case 2: return native_kernel<K, 2, SCAN>;
-        case 3: return native_kernel<K, 3, SCAN>;
-        case 4: return native_kernel<K, 4, SCAN>;
-        case 5: return native_kernel<K, 5, SCAN>;
-        case 6: return native_kernel<K, 6, SCAN>;
-        case 7: return native_kernel<K, 7, SCAN>;
-        case 8: return native_kernel<K, 8, SCAN>;
-    }
-    return nullptr;
-}
-
-template <int K>
-KernelFn native_for(int ch, bool scan) {
-    return scan ? native_for_ch<K, true>(ch) : native_for_ch<K, false>(ch);
-}
-
-// K = 1 with a scan and W = 4m+1 or 4m+2: rows read 2 words at a time (no padding keys beyond one)
-KernelFn native_vec2_for(int ch) {
-    switch (ch) {
-        case 1: return native_kernel<1, 1, true, 2>;
-        case 3: return native_kernel<1, 3, true, 2>;
-        case 5: return native_kernel<1, 5, true, 2>;
-        case 7: return native_kernel<1, 7, true, 2>;
-        case 9: return native_kernel<1, 9, true, 2>;
-        case 11: return native_kernel<1, 11, true, 2>;
-        case 13: return native_kernel<1, 13, true, 2>;
-        case 15: return native_kernel<1, 15, true, 2>;
-    }
-    return nullptr;
-}
-
-KernelFn pick_kernel(int mode, int k, int ch, bool scan, bool ln) {
-    if (mode == BBE_MODE_MT) {
-        switch (k) {
-            case 1: return ln ? exact_kernel<1, MT, true> : exact_kernel<1, MT, false>;
-            case 2: return ln ? exact_kernel<2, MT, true> : exact_kernel<2, MT, false>;
-            case 3: return ln ? exact_kernel<3, MT, true> : exact_kernel<3, MT, false>;
-            case 4: return ln ? exact_kernel<4, MT, true> : exact_kernel<4, MT, false>;
-        }
-    } else if (mode == BBE_MODE_INJECT) {
-        switch (k) {
-            case 1: return exact_kernel<1, INJECT>;
-            case 2: return exact_kernel<2, INJECT>;
-            case 3: return exact_kernel<3, INJECT>;
-            case 4: return exact_kernel<4, INJECT>;
-        }
-    } else {
-        switch (k) {
-            case 1: return native_for<1>(ch, scan);
-            case 2: return native_for<2>(ch, scan);
-            case 3: return native_for<3>(ch, scan);
-            case 4: return native_for<4>(ch, scan);
-        }
-    }
-    return nullptr;
-}
-
 #ifndef BBE_NATIVE_VEC2
 #define BBE_NATIVE_VEC2 1
 #endif
@@ -476,7 +412,8 @@ int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, co
     pl->tally_len = TL.len();
     const int kmode = rq->mode == BBE_MODE_NATIVE ? NATIVE : (rq->mode == BBE_MODE_MT ? MT : INJECT);
     pl->smem = smem_bytes(kmode, (TL.hist_len() + 1) & ~1, pl->K, pl->S, pl->WP);
-    pl->fn = vec2 ? native_vec2_for(pl->CH) : pick_kernel(rq->mode, pl->K, pl->CH, scan, ln);
+    pl->fn = rq->mode == BBE_MODE_NATIVE ? pick_native(pl->K, pl->CH, scan, vec2 ? 2 : 4)
+                                         : pick_exact(rq->mode == BBE_MODE_MT ? MT : INJECT, pl->K, ln);
     if (!pl->fn) return fail(BBE_EINVAL, "no kernel for this configuration");
     // the kernel's dynamic-smem limit only ever grows (a smaller later request keeps the larger
     // limit valid); residency per (kernel, dynamic smem) is queried once per device
@@ -744,7 +681,7 @@ static const LibmExp& libm_exp_table() {
 static uint64_t h_run_of(uint64_t master) {  // splitmix64(splitmix64(master) ^ fnv1a("s:run"))
     uint64_t h = 0xCBF29CE484222325ull;
     for (char ch : std::string("s:run")) h = (h ^ (unsigned char)ch) * 0x100000001B3ull;
-    return splitmix64_dev(splitmix64_dev(master) ^ h);
+    return splitmix64_host(splitmix64_host(master) ^ h);
 }
 
 // Launch the race kernel for the whole request (MT: chunked seeding + race per chunk).  `d_seeds`
@@ -759,14 +696,8 @@ static int launch_all(DevCtx* ctx, const Plan& pl, LaunchArgs a, const bbe_compe
     if (!ctx->mt_table) {
         uint32_t t[kMtWords];
         mt_init_table(t);
-        BBE_CK(cudaMemcpyToSymbol(c_mt_init, t, sizeof(t)));
         const LibmExp& E = libm_exp_table();
-        const int ok = E.ok ? 1 : 0;
-        BBE_CK(cudaMemcpyToSymbol(c_exp_ok, &ok, sizeof(ok)));
-        if (E.ok) {
-            BBE_CK(cudaMemcpyToSymbol(c_exp_tab, E.tab, sizeof(E.tab)));
-            BBE_CK(cudaMemcpyToSymbol(c_exp_c, E.c, sizeof(E.c)));
-        }
+        BBE_CK(upload_mt_tables(t, E.ok ? 1 : 0, E.tab, E.c));
         ctx->mt_table = true;
     }
     a.nv_magic = 4 * std::exp(-0.5) / std::sqrt(2.0);  // random.NV_MAGICCONST, host libm
@@ -780,10 +711,8 @@ static int launch_all(DevCtx* ctx, const Plan& pl, LaunchArgs a, const bbe_compe
     const int n = a.n;
     for (int64_t c0 = 0; c0 < total; c0 += chunk) {
         const int64_t cn = std::min(chunk, total - c0);
-        mt_seed_kernel<<<(unsigned)((cn + 127) / 128), 128, 0, stream>>>(
-            d_seeds ? d_seeds + c0 : nullptr, h_run, off0 + c0, cn, pad, (uint32_t*)ctx->d_mt_scratch.p,
-            (uint32_t*)ctx->d_mt_states.p);
-        BBE_CK(cudaGetLastError());
+        BBE_CK(launch_mt_seed(stream, d_seeds ? d_seeds + c0 : nullptr, h_run, off0 + c0, cn, pad,
+                              (uint32_t*)ctx->d_mt_scratch.p, (uint32_t*)ctx->d_mt_states.p));
         LaunchArgs b = a;
         b.n_sims = cn;
         b.sim_offset = off0 + c0;
