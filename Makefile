@@ -4,9 +4,10 @@
 NVCC ?= nvcc
 CXX ?= g++
 ARCH = -gencode arch=compute_100a,code=sm_100a
-NVFLAGS = $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -Xptxas -v
+NVEXTRA ?=
+NVFLAGS = $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -Xptxas -v $(NVEXTRA)
 CXXFLAGS = -O3 -std=c++17 -fPIC
-LIBDIR = paper_2108_02419_b200/_lib
+LIBDIR ?= paper_2108_02419_b200/_lib
 LIB = $(LIBDIR)/libbbe_sim.so
 CSRC = paper_2108_02419_b200/csrc
 COMMON = $(CSRC)/common.cuh $(CSRC)/kernels.h include/bbe_sim.h

@@ -4,8 +4,8 @@
 # Run with BBE_LIB=paper_2108_02419_b200/_lib/ab/libbbe_NAME.so python tools/profile_c2.py
 set -e
 cd "$(dirname "$0")/.."
-mkdir -p paper_2108_02419_b200/_lib/ab
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared \
-    --expt-relaxed-constexpr $2 -o "paper_2108_02419_b200/_lib/ab/libbbe_$1.so" \
-    paper_2108_02419_b200/csrc/bbe_sim.cu paper_2108_02419_b200/csrc/host_mt.cpp -ldl
+OUT=paper_2108_02419_b200/_lib/ab/$1
+mkdir -p "$OUT"
+make -s -j5 LIBDIR="$OUT" NVEXTRA="$2" "$OUT/libbbe_sim.so"
+cp "$OUT/libbbe_sim.so" "paper_2108_02419_b200/_lib/ab/libbbe_$1.so"
 echo "built paper_2108_02419_b200/_lib/ab/libbbe_$1.so"
