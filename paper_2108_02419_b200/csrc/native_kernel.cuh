@@ -198,25 +198,31 @@ native_kernel(const LaunchArgs a) {
         const bool seg_done = running && ((live_mask & segmask) == 0u);
         if (__any_sync(0xffffffffu, seg_done)) {
             const bool diverged = (__ballot_sync(0xffffffffu, dv) & segmask) != 0u;
-            float lp[K];
+            // _finish_order (race.py:323-332): rank = #{i : (fin_i, L - pos_i, i) < (fin_c, L - pos_c, c)}.
+            // (fin, L - pos) as one order-preserving u64 key (biased fin | float key of L - pos; slots
+            // without a competitor sort last); the index tie-break folds into the compare:
+            // i < c counts key_i <= key_c, i > c counts key_i < key_c.
+            uint64_t key[K];
             int rank[K];
 #pragma unroll
-            for (int k = 0; k < K; ++k) { lp[k] = __fsub_rn(L, pos[k]); rank[k] = 0; }
+            for (int k = 0; k < K; ++k) {
+                const uint32_t u = __float_as_uint(__fsub_rn(L, pos[k]));
+                const uint32_t lo = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+                key[k] = has[k] ? ((uint64_t)((uint32_t)fin[k] ^ 0x80000000u) << 32) | lo : ~0ull;
+                rank[k] = 0;
+            }
 #pragma unroll
             for (int kk = 0; kk < K; ++kk) {
                 for (int j = 0; j < W; ++j) {
-                    const int32_t fr = shfl(fin[kk], base + j);
-                    const float dr = shfl(lp[kk], base + j);
+                    const uint64_t kr = shfl(key[kk], base + j);
                     const int i = kk * W + j;
 #pragma unroll
-                    for (int k = 0; k < K; ++k) {
-                        const bool less = fr < fin[k] || (fr == fin[k] && (dr < lp[k] || (dr == lp[k] && i < cidx[k])));
-                        rank[k] += (i < n && less) ? 1 : 0;
-                    }
+                    for (int k = 0; k < K; ++k) rank[k] += (kr < key[k] + (i < cidx[k] ? 1u : 0u)) ? 1 : 0;
                 }
             }
-            uint32_t seg_blk = 0;
-            for (int j = 0; j < W; ++j) seg_blk += shfl(blk_sim, base + j);
+            uint32_t seg_blk = 0;  // per-sim blocked steps: only for the per-sim output
+            if (a.blocked)
+                for (int j = 0; j < W; ++j) seg_blk += shfl(blk_sim, base + j);
             int64_t lehmer = 0;
             if (a.perms) {
                 int cnt[K];
