@@ -8,16 +8,18 @@
 // nextafter on a zero-progress step, finish at p >= L, order by (finish tick, L - pos, index).
 //
 // Front runner.  The host picks a frame (an offset of positions, L and breakpoints) in which every
-// racing position is >= a floor `lo` > 0 and below L with bits(L) - bits(lo) < 2^(31-b), b = index
-// bits of a segment.  Non-negative floats order like their IEEE bits, so key = bits(pos) - bits(lo) + 1
-// is an order-preserving (31-b)-bit key.  Each lane publishes (key << b) | lane-in-segment (0 once
-// finished) to a per-warp shared-memory row (double-buffered by tick parity, one __syncwarp per tick),
-// reads its segment's row with 128-bit broadcast loads and keeps one wrapped minimum (one VIADDMNMX per
-// rival) that yields the nearest key strictly ahead together with the lowest index holding it.
+// racing position is >= a floor `lo` > 0 and below L with bits(L) - bits(lo) < 2^(31-b), b = 5 index
+// bits.  Non-negative floats order like their IEEE bits, so key = bits(pos) - bits(lo) + 1 is an
+// order-preserving (31-b)-bit key.  Each lane publishes (key << b) | lane-in-segment (0 once finished)
+// to a per-warp shared-memory row (double-buffered by tick parity, one __syncwarp per tick), reads its
+// segment's row with 128- or 64-bit broadcast loads (VEC) and keeps one wrapped minimum (one VIADDMNMX
+// per rival) that yields the nearest key strictly ahead together with the lowest index holding it.
 //
-// Bookkeeping is kept off the per-tick path: rt (ticks advanced in the sim) is segment-uniform;
-// racing <=> fin == kRacing (int32 finish tick relative to the state's tick); the tick-limit check
-// marks racing lanes diverged; competitor-timesteps are summed from finish ticks at finalize.
+// Sims: persistent grid; each segment starts on one sim and claims the next from a per-launch counter
+// at a 4-tick block boundary (common.cuh claim_next_sim).  Bookkeeping is kept off the per-tick path:
+// rt (ticks advanced in the sim) is segment-uniform; racing <=> fin == kRacing (int32 finish tick
+// relative to the state's tick); the tick-limit check runs at block boundaries; competitor-timesteps
+// are summed from finish ticks at finalize; finish-order ranks come from one u64 key per competitor.
 #pragma once
 
 #include <type_traits>
@@ -27,12 +29,12 @@
 namespace bbe {
 
 // Build-time variants for A/B measurement (tools/ab_build.sh); the defaults are the measured best
-// (C2 on B200, round-1 kernel: 10 blocks/SM at 51 registers 0.483 ms vs 0.437 ms).
+// (C2 on B200: 8, 9 or 10 blocks/SM were slower than 7 at every step of round 1).
 #ifndef BBE_SPREAD_TAIL
 #define BBE_SPREAD_TAIL 1
 #endif
 #ifndef BBE_NATIVE_MINBLOCKS_K1
-#define BBE_NATIVE_MINBLOCKS_K1 7  // measured: 8 -> 0.436 ms, 7 -> 0.428 ms, 6 -> 0.435 ms
+#define BBE_NATIVE_MINBLOCKS_K1 7  // 64 registers -> 8 resident blocks of 4 warps
 #endif
 
 constexpr int32_t kRacing = 0x7fffffff;
