@@ -15,20 +15,22 @@
 // reproduces positions, finish ticks, order and blocked counts bit for bit.
 //
 // Mapping: one sim per SEGMENT of W consecutive lanes, competitor c = k*W + l in lane l, slot k;
-// S = 32/W sims per warp; persistent grid, a finished segment takes its next sim at a 4-tick block
+// S = 32/W sims per warp; persistent grid, a finished segment claims its next sim at a 4-tick block
 // boundary.  Front runner: rounding is monotonic, so the reference's smallest gap
 // min_i fl(p_i - p_c) equals fl(min_i p_i - p_c); each lane takes a positional min over its
-// segment's start-of-tick positions (a shared-memory row per tick parity, 128-bit loads).  The
-// index of the rival holding that gap -- needed only for a blocked step -- is found with the
-// reference's own gap arithmetic and lowest-index rule.
+// segment's start-of-tick positions (a shared-memory row per tick parity, 128-bit loads) and keeps
+// the lowest index holding it.  That is the reference's front unless two distinct positions round
+// to the same gap, which needs p* <= 2 gap; blocked lanes in that case rerun the reference's own gap
+// arithmetic and lowest-index rule.
 //
 // Draw sources:
 //   INJECT  recorded reference draws (CSR per sim); a free slot's offset in the tick = popc of free
 //           slots of lower competitor index in its segment -- the reference's consumption order.
 //   MT      per-sim CPython MT19937 (mt_stream.cuh) in shared memory.  Speculative rounds: every
 //           pending competitor reads its words at the offset it would have if each pending lognormal
-//           draw accepted its next Kinderman-Monahan trial; draws before the first rejection are
-//           final.  The whole warp twists a segment's block when its unread window runs low (the
+//           draw accepted its next Kinderman-Monahan trial (offsets from two ballots per slot);
+//           draws before the first rejection are final.  Uniform-only fields (LN = false) need no
+//           rounds: every draw is two words.  The whole warp twists a segment's block when its unread window runs low (the
 //           unread words move to a side buffer just below the block first, so the window stays
 //           contiguous and early twists leave the stream unchanged).
 #pragma once
@@ -41,7 +43,7 @@
 namespace bbe {
 
 #ifndef BBE_MT_MINBLOCKS
-#define BBE_MT_MINBLOCKS 5  // measured: 1 -> 3.82 ms, 5 -> 3.67 ms, 6 -> 4.41 ms (C2, 100k sims)
+#define BBE_MT_MINBLOCKS 5  // measured (C2, 100k sims, early round 1): 1 -> 3.82 ms, 5 -> 3.67 ms, 6 -> 4.41 ms
 #endif
 
 // LN = false (MT): the field has no lognormal competitor, so every draw takes exactly two words and a
