@@ -265,3 +265,20 @@ def test_mt_multi_slot_divergence_finished_and_trajectories():
     with pytest.raises(sim.SimDivergedError) as e:
         sim.simulate_batch(None, tight, 6, mode="mt", seeds=oracle.rp_seeds(3, 6), sim_offset=100)
     assert e.value.sim_index == 100
+
+
+@pytest.mark.parametrize("mode", ["native", "mt"])
+def test_continuation_is_pure_and_deterministic(mode):
+    """tests/test_race.py:232-235, 285-300: simulate_from never mutates its input state, the same
+    seed gives the same result, a different seed a different one."""
+    cfg = _mixed_field(10)
+    st = RaceState(7, [3.0 + i for i in range(10)], [2.0] * 10, [None] * 10)
+    snapshot = (st.tick, list(st.positions), list(st.prev_steps), list(st.finish_ticks))
+    kw = lambda s: dict(seeds=oracle.rp_seeds(s, 2000)) if mode == "mt" else {}  # noqa: E731
+    a = sim.simulate_batch(st, cfg, 2000, 5, mode=mode, records=True, **kw(5))
+    b = sim.simulate_batch(st, cfg, 2000, 5, mode=mode, records=True, **kw(5))
+    c = sim.simulate_batch(st, cfg, 2000, 6, mode=mode, records=True, **kw(6))
+    assert (st.tick, st.positions, st.prev_steps, st.finish_ticks) == snapshot
+    assert (a.order == b.order).all() and (a.final_positions == b.final_positions).all()
+    assert not (a.order == c.order).all()
+    assert sim.simulate_from(st, cfg, 123, mode=mode) == sim.simulate_from(st, cfg, 123, mode=mode)
