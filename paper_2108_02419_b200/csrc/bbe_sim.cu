@@ -19,6 +19,7 @@
 #include <vector>
 
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: named ranges for nsys / ncu timelines
 
 #include "../../include/bbe_sim.h"
 #include "kernels.h"
@@ -28,6 +29,11 @@ using namespace bbe;
 namespace {
 
 thread_local std::string g_err;
+
+struct NvtxRange {  // one named range per C-ABI call (free when no profiler is attached)
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -504,6 +510,7 @@ int bbe_mt_advance64(uint32_t* state624, int32_t* pos, int64_t count, uint64_t* 
 
 int bbe_mt_advance64_many(int64_t n_gen, uint32_t* const* states, int32_t* const* pos, const int64_t* counts,
                           uint64_t* const* outs, const int64_t* out_lens, int32_t threads) {
+    NvtxRange nvtx_range("bbe_mt_advance64_many");
     if (n_gen < 0 || (n_gen && (!states || !pos || !counts))) return fail(BBE_EINVAL, "bad arguments");
     for (int64_t g = 0; g < n_gen; ++g)
         if (!states[g] || !pos[g] || counts[g] < 0 || *pos[g] < 0 || *pos[g] > 624)
@@ -781,6 +788,7 @@ static int build_args(const Plan& pl, const bbe_race* race, const bbe_state* st,
 
 int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, const bbe_request* rq,
                        bbe_result* out) {
+    NvtxRange nvtx_range("bbe_simulate_begin");
     int rc = validate(race, comps, st, rq);
     if (rc) return rc;
     if (!out || !out->wins) return fail(BBE_EINVAL, "result needs a wins buffer");
@@ -906,6 +914,7 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
 }
 
 int bbe_simulate_end(bbe_result* out) {
+    NvtxRange nvtx_range("bbe_simulate_end");
     Lease lease;
     {
         std::lock_guard<std::mutex> g(g_ctx_mu);
@@ -950,6 +959,7 @@ int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_st
 
 int bbe_simulate_multi(int32_t n_parts, const bbe_race* race, const bbe_competitor* comps, const bbe_state* st,
                        const bbe_request* rq, bbe_result* out) {
+    NvtxRange nvtx_range("bbe_simulate_multi");
     int rc = validate(race, comps, st, rq);
     if (rc) return rc;
     if (!out || !out->wins) return fail(BBE_EINVAL, "result needs a wins buffer");
@@ -1065,6 +1075,7 @@ int bbe_simulate_multi(int32_t n_parts, const bbe_race* race, const bbe_competit
 
 int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, const bbe_request* rq,
                        const bbe_result* dev_out, uint64_t* d_tally, void* stream) {
+    NvtxRange nvtx_range("bbe_simulate_async");
     int rc = validate(race, comps, st, rq);
     if (rc) return rc;
     if (!d_tally) return fail(BBE_EINVAL, "d_tally is required");
