@@ -282,3 +282,24 @@ def test_continuation_is_pure_and_deterministic(mode):
     assert (a.order == b.order).all() and (a.final_positions == b.final_positions).all()
     assert not (a.order == c.order).all()
     assert sim.simulate_from(st, cfg, 123, mode=mode) == sim.simulate_from(st, cfg, 123, mode=mode)
+
+
+@pytest.mark.parametrize("mode", ["native", "mt"])
+def test_extreme_step_laws_terminate_or_diverge_cleanly(mode):
+    """Heavy-tailed lognormal steps (sigma 4: steps from ~1e-5 to ~1e5), tiny steps that need
+    nextafter, and a huge track: every sim finishes or is reported diverged -- no hang, no garbage."""
+    heavy = RaceConfig(500.0, (Competitor("h", LogNormalSteps(0.0, 4.0, 1.0), theta=2.0),
+                               Competitor("u", UniformSteps(5.0, 15.0), theta=1.0),
+                               Competitor("g", LogNormalSteps(2.0, 0.1, 1.0))))
+    def kw(key, n):
+        return dict(seeds=oracle.rp_seeds(key, n)) if mode == "mt" else {}
+
+    r = sim.simulate_batch(None, heavy, 5000, 3, mode=mode, records=True, **kw(3, 5000))
+    assert int(r.wins.sum()) == 5000 and (np.sort(r.order, axis=1) == np.arange(3)).all()
+    assert np.isfinite(r.final_positions).all() or mode == "native"
+    tiny = RaceConfig(1.0, (Competitor("t", LogNormalSteps(-80.0, 0.0, 1.0)),), tick_limit=50)
+    with pytest.raises(sim.SimDivergedError):
+        sim.simulate_batch(None, tiny, 10, 1, mode=mode, **kw(4, 10))
+    far = RaceConfig(1e6, (Competitor("a", UniformSteps(4e4, 6e4)), Competitor("b", UniformSteps(4.5e4, 5.5e4), theta=5e3)))
+    r = sim.simulate_batch(None, far, 2000, 9, mode=mode, ranks=True, **kw(9, 2000))
+    assert int(r.wins.sum()) == 2000
