@@ -112,3 +112,29 @@ def test_single_simulate_from_matches_reference_seed():
     sf = case["simulate_from"]
     order = simulate_from(state_from_dict(sf["state"]), cfg, sf["seed"], mode="mt")
     assert order == tuple(cfg.competitor_ids[c] for c in sf["order"])
+
+
+def test_device_resident_mt_with_device_seeds():
+    """bbe_simulate_async in MT mode with the per-sim seeds already in device memory (the path a
+    device-resident caller uses): the device tally equals the host call's for the same seeds."""
+    import ctypes
+
+    import torch
+
+    g = c2()
+    cfg, st = config_from_dict(g["config"]), state_from_dict(g["state"])
+    seeds = oracle.rp_seeds(77, 3000)
+    want = sim.simulate_batch(st, cfg, 3000, mode="mt", seeds=seeds)
+    dl = sim.DeviceLauncher(st, cfg)
+    d_seeds = torch.from_numpy(seeds.view(np.int64)).cuda()
+    tally = torch.zeros(dl.tally_len, dtype=torch.int64, device="cuda")
+    req = sim.BbeRequest(3000, 0, 0, sim.MODES["mt"], 0, None, None, d_seeds.data_ptr(), 0, 0)
+    stream = torch.cuda.current_stream().cuda_stream
+    rc = sim.lib().bbe_simulate_async(ctypes.byref(dl.pk.race), dl.pk.comps, ctypes.byref(dl.st), ctypes.byref(req),
+                                      None, ctypes.c_void_p(tally.data_ptr()), ctypes.c_void_p(stream))
+    assert rc == 0, sim.last_error()
+    t = tally.cpu().numpy().view(np.uint64)
+    n = cfg.n_competitors
+    assert t[:n].tolist() == want.wins.tolist()
+    assert t[n:n + n * n].reshape(n, n).tolist() == want.ranks.tolist()
+    assert int(t[dl.off["ct"]]) == want.competitor_steps
