@@ -398,13 +398,15 @@ exact_kernel(const LaunchArgs a) {
                     const int i = kk * W + j;
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
-                        const bool less = fr < fin[k] || (fr == fin[k] && (dr < lp[k] || (dr == lp[k] && i < cidx[k])));
+                        // non-short-circuit operators: predicated compares instead of branches
+                        const bool less = (fr < fin[k]) | ((fr == fin[k]) & ((dr < lp[k]) | ((dr == lp[k]) & (i < cidx[k]))));
                         rank[k] += (i < n && less) ? 1 : 0;
                     }
                 }
             }
-            uint32_t seg_blk = 0;
-            for (int j = 0; j < W; ++j) seg_blk += shfl(blk_sim, base + j);
+            uint32_t seg_blk = 0;  // per-sim blocked steps: only for the per-sim output
+            if (a.blocked)
+                for (int j = 0; j < W; ++j) seg_blk += shfl(blk_sim, base + j);
             int64_t lehmer = 0;
             if (a.perms) {
                 // Lehmer index of the finish order: sum_c #{c' < c : rank(c') > rank(c)} * (n-1-rank(c))!
