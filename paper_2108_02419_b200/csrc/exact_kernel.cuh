@@ -285,7 +285,7 @@ exact_kernel(const LaunchArgs a) {
             any_pend = false;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                const bool done = pend[k] && (k < kb || (k == kb && (1u << lane) < first_bad));
+                const bool done = pend[k] & ((k < kb) | ((k == kb) & ((1u << lane) < first_bad)));
                 if (done) {
                     if (lognorm[k]) ln_draw[k] = true;
                     else d[k] = __dadd_rn(lo[k], __dmul_rn(span[k], r01[k]));
