@@ -590,8 +590,41 @@ int bbe_derive_seeds(uint64_t master, int64_t first, int64_t count, uint64_t* ou
 constexpr int kWorkSlots = 64;  // concurrent native launches per device with their own work counters
 constexpr size_t kMaxStagedBytes = 256ull << 20;  // per-sim outputs staged through pinned memory up to this
 
+// The kernels' shared-memory histograms are 32-bit: a launch never runs 2^32 or more sims.
+constexpr int64_t kMaxLaunchSims = 1ll << 31;
+
+// The launch arguments of sims [c0, c0 + cn) of `a`: per-sim streams and outputs are indexed by the
+// launch-local sim index, so every per-sim pointer moves by c0.
+static LaunchArgs sub_launch(const LaunchArgs& a, int64_t c0, int64_t cn) {
+    LaunchArgs b = a;
+    const int64_t n = a.n;
+    b.n_sims = cn;
+    b.sim_offset = a.sim_offset + c0;
+    b.group_base = a.group_base + c0;
+    if (b.draw_offsets) b.draw_offsets += c0;
+    if (b.draws_used) b.draws_used += c0;
+    if (b.mt_states) b.mt_states += c0 * kMtWords;
+    if (b.winner) b.winner += c0;
+    if (b.order) b.order += c0 * n;
+    if (b.finish_ticks) b.finish_ticks += c0 * n;
+    if (b.final_pos) b.final_pos += c0 * n;
+    if (b.blocked) b.blocked += c0;
+    if (b.traj_pos) {
+        b.traj_pos += c0 * ((int64_t)b.traj_cap + 1) * n;
+        b.traj_prev += c0 * ((int64_t)b.traj_cap + 1) * n;
+    }
+    return b;
+}
+
 static int launch_one(DevCtx* ctx, const Plan& pl, const LaunchArgs& a0, cudaStream_t stream) {
     if (a0.n_sims == 0) return BBE_OK;
+    if (a0.n_sims > kMaxLaunchSims) {
+        for (int64_t c0 = 0; c0 < a0.n_sims; c0 += kMaxLaunchSims) {
+            const int rc = launch_one(ctx, pl, sub_launch(a0, c0, std::min(kMaxLaunchSims, a0.n_sims - c0)), stream);
+            if (rc) return rc;
+        }
+        return BBE_OK;
+    }
     LaunchArgs a = a0;
     {
         // the kernel leaves its counter pair zeroed; consecutive launches rotate through the ring
@@ -715,25 +748,12 @@ static int launch_all(DevCtx* ctx, const Plan& pl, LaunchArgs a, const bbe_compe
     BBE_CK(ctx->d_mt_scratch.ensure((size_t)pad * kMtWords * 4));
     const uint64_t h_run = h_run_of(seed_master);
     const int64_t off0 = a.sim_offset;
-    const int n = a.n;
     for (int64_t c0 = 0; c0 < total; c0 += chunk) {
         const int64_t cn = std::min(chunk, total - c0);
         BBE_CK(launch_mt_seed(stream, d_seeds ? d_seeds + c0 : nullptr, h_run, off0 + c0, cn, pad,
                               (uint32_t*)ctx->d_mt_scratch.p, (uint32_t*)ctx->d_mt_states.p));
-        LaunchArgs b = a;
-        b.n_sims = cn;
-        b.sim_offset = off0 + c0;
-        b.mt_states = (const uint32_t*)ctx->d_mt_states.p;
-        if (b.winner) b.winner += c0;
-        b.group_base = c0;
-        if (b.order) b.order += c0 * n;
-        if (b.finish_ticks) b.finish_ticks += c0 * n;
-        if (b.final_pos) b.final_pos += c0 * n;
-        if (b.blocked) b.blocked += c0;
-        if (b.traj_pos) {
-            b.traj_pos += c0 * ((int64_t)b.traj_cap + 1) * n;
-            b.traj_prev += c0 * ((int64_t)b.traj_cap + 1) * n;
-        }
+        LaunchArgs b = sub_launch(a, c0, cn);
+        b.mt_states = (const uint32_t*)ctx->d_mt_states.p;  // the chunk's seeded states
         int rc = launch_one(ctx, pl, b, stream);
         if (rc) return rc;
     }

@@ -56,8 +56,10 @@ exact_kernel(const LaunchArgs a) {
     extern __shared__ __align__(16) unsigned long long s_dyn[];
     const TallyLayout TL{a.n, a.perms};
     const int hist_len = TL.hist_len();
-    unsigned long long* s_hist = s_dyn;
-    for (int i = threadIdx.x; i < hist_len; i += blockDim.x) s_hist[i] = 0ull;
+    // 32-bit shared histograms (native ATOMS.ADD; a 64-bit shared add is a CAS loop).  A block's count
+    // in one bin is at most the sims of its launch, which the host keeps below 2^32 (launch_one).
+    uint32_t* s_hist = reinterpret_cast<uint32_t*>(s_dyn);
+    for (int i = threadIdx.x; i < hist_len; i += blockDim.x) s_hist[i] = 0u;
 
     const int n = a.n, W = a.W, S = a.S;
     const int lane = threadIdx.x & (kWarp - 1);
@@ -442,12 +444,12 @@ exact_kernel(const LaunchArgs a) {
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
                         if (!has[k]) continue;
-                        if (rank[k] == 0) atomicAdd(&s_hist[TL.wins() + cidx[k]], 1ull);
-                        atomicAdd(&s_hist[TL.ranks() + cidx[k] * n + rank[k]], 1ull);
+                        if (rank[k] == 0) atomicAdd(&s_hist[TL.wins() + cidx[k]], 1u);
+                        atomicAdd(&s_hist[TL.ranks() + cidx[k] * n + rank[k]], 1u);
                         if (a.group_wins && rank[k] == 0)
                             atomicAdd(&a.group_wins[((a.group_base + s) / a.group_size) * n + cidx[k]], 1ull);
                     }
-                    if (a.perms && l == 0) atomicAdd(&s_hist[TL.perms() + lehmer], 1ull);
+                    if (a.perms && l == 0) atomicAdd(&s_hist[TL.perms() + lehmer], 1u);
                 }
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
@@ -633,8 +635,8 @@ exact_kernel(const LaunchArgs a) {
     __syncthreads();
     if (threadIdx.x == 0) release_work(a.work);
     for (int i = threadIdx.x; i < hist_len; i += blockDim.x) {
-        const unsigned long long v = s_hist[i];
-        if (v) atomicAdd((unsigned long long*)&a.tally[i], v);
+        const uint32_t v = s_hist[i];
+        if (v) atomicAdd((unsigned long long*)&a.tally[i], (unsigned long long)v);
     }
 }
 

@@ -80,8 +80,10 @@ native_kernel(const LaunchArgs a) {
     extern __shared__ __align__(16) unsigned long long s_dyn[];
     const TallyLayout TL{a.n, a.perms};
     const int hist_len = TL.hist_len();
-    unsigned long long* s_hist = s_dyn;
-    for (int i = threadIdx.x; i < hist_len; i += blockDim.x) s_hist[i] = 0ull;
+    // 32-bit shared histograms (native ATOMS.ADD; a 64-bit shared add is a CAS loop).  A block's count
+    // in one bin is at most the sims of its launch, which the host keeps below 2^32 (launch_one).
+    uint32_t* s_hist = reinterpret_cast<uint32_t*>(s_dyn);
+    for (int i = threadIdx.x; i < hist_len; i += blockDim.x) s_hist[i] = 0u;
 
     constexpr int WP = VEC * CH;
     constexpr int SLOT = native_slot_words(VEC, CH);  // words per slot row (segments, then a pad group)
@@ -256,12 +258,12 @@ native_kernel(const LaunchArgs a) {
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
                         if (!has[k]) continue;
-                        if (rank[k] == 0) atomicAdd(&s_hist[TL.wins() + cidx[k]], 1ull);
-                        atomicAdd(&s_hist[TL.ranks() + cidx[k] * n + rank[k]], 1ull);
+                        if (rank[k] == 0) atomicAdd(&s_hist[TL.wins() + cidx[k]], 1u);
+                        atomicAdd(&s_hist[TL.ranks() + cidx[k] * n + rank[k]], 1u);
                         if (a.group_wins && rank[k] == 0)
                             atomicAdd(&a.group_wins[((a.group_base + s) / a.group_size) * n + cidx[k]], 1ull);
                     }
-                    if (a.perms && l == 0) atomicAdd(&s_hist[TL.perms() + lehmer], 1ull);
+                    if (a.perms && l == 0) atomicAdd(&s_hist[TL.perms() + lehmer], 1u);
                 }
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
@@ -428,7 +430,9 @@ native_kernel(const LaunchArgs a) {
                 // branch-free: only racing competitors move
                 const bool done = racing[k] && p >= L;
                 pos[k] = racing[k] ? p : pos[k];
-                prev[k] = racing[k] ? step : prev[k];
+                // a finished competitor's previous step is never read again (finished rivals never
+                // block, race.py:256-257), so it is written unconditionally
+                prev[k] = step;
                 blk_sim += bl[k] ? 1u : 0u;
                 fin[k] = done ? rt + 1 : fin[k];
             }
@@ -458,8 +462,8 @@ native_kernel(const LaunchArgs a) {
     __syncthreads();
     if (threadIdx.x == 0) release_work(a.work);
     for (int i = threadIdx.x; i < hist_len; i += blockDim.x) {
-        const unsigned long long v = s_hist[i];
-        if (v) atomicAdd((unsigned long long*)&a.tally[i], v);
+        const uint32_t v = s_hist[i];
+        if (v) atomicAdd((unsigned long long*)&a.tally[i], (unsigned long long)v);
     }
 }
 
