@@ -100,8 +100,11 @@ __host__ __device__ constexpr int swp_max(int VEC, int CH) {
 __host__ __device__ constexpr int native_slot_words(int VEC, int CH) { return swp_max(VEC, CH) + 4; }
 __host__ __device__ constexpr int native_warp_words(int K, int VEC, int CH) { return 2 * K * native_slot_words(VEC, CH); }
 constexpr int kMtWords = 624;
-// side buffer: >= one speculative round's reads (4 words x 32 lanes x K slots)
-__host__ __device__ constexpr int mt_side_words(int K) { return 128 * K; }
+// MT trial-evaluation pass (K = 1): a pending lognormal draw evaluates up to this many speculative
+// Kinderman-Monahan trials at once, on otherwise idle lanes of its segment
+constexpr int kMtMaxTrials = 8;
+// side buffer: >= one round's reads -- 4 words x 32 lanes x K slots, + the trial window's overhang
+__host__ __device__ constexpr int mt_side_words(int K) { return 128 * K + 4 * kMtMaxTrials; }
 __host__ __device__ constexpr int mt_seg_words(int K) { return kMtWords + mt_side_words(K); }
 constexpr int kXSlot = 66;         // exact modes: doubles per position row (S*round_up(W,2) <= 64, + pad)
 __host__ __device__ inline size_t smem_bytes(int mode, int hist_len_even, int K, int S, int WP) {
@@ -112,6 +115,7 @@ __host__ __device__ inline size_t smem_bytes(int mode, int hist_len_even, int K,
     }
     if (mode == MT) b += (size_t)kWarpsPerBlock * S * mt_seg_words(K) * 4;
     if (mode != NATIVE) b += (size_t)kWarpsPerBlock * 2 * K * kXSlot * 8;
+    if (mode == MT) b += (size_t)kWarpsPerBlock * kWarp * 4;  // per-warp lognormal offsets (trial pass)
     return b;
 }
 

@@ -78,9 +78,12 @@ exact_kernel(const LaunchArgs a) {
     uint32_t* const mt = seg_mt + kSide;  // the 624-word MT19937 block
     // start-of-tick positions, per warp: [parity][slot][segment * WP2 + lane-in-segment], pads -inf
     const int WP2 = (W + 1) & ~1;
-    double* const xrows = reinterpret_cast<double*>(
-        reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) +
-        (MODE == MT ? kWarpsPerBlock * S * kSeg : 0)) + warp * 2 * K * kXSlot;
+    double* const xrows_all = reinterpret_cast<double*>(
+        reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) + (MODE == MT ? kWarpsPerBlock * S * kSeg : 0));
+    double* const xrows = xrows_all + warp * 2 * K * kXSlot;
+    // MT, K = 1: the round's pending lognormal draws publish their speculative word offsets here, by
+    // rank in their segment (lane base + rank), for the lanes that evaluate their trials
+    int* const ln_off = reinterpret_cast<int*>(xrows_all + kWarpsPerBlock * 2 * K * kXSlot) + warp * kWarp;
     for (int i = lane; i < 2 * K * kXSlot; i += kWarp) xrows[i] = -CUDART_INF;
     const int xseg = lane_on ? seg * WP2 : 0;
     double* const xw = xrows + (lane_on ? seg * WP2 + l : kXSlot - 1);
@@ -167,28 +170,23 @@ exact_kernel(const LaunchArgs a) {
     // shorter window is topped up: its words move to the end of the side buffer, just below the
     // block, and the block is twisted in place -- early, but the stream is the same, since the
     // twist reads the whole old block.
+    // A round reads below offset fill_need: 4WK (every lane's 4 words), plus, for the K = 1 trial
+    // pass, kMtMaxTrials - 1 further trials of one lognormal draw.
+    const int fill_need = (K == 1 && LN) ? 4 * W + 4 * kMtMaxTrials : 4 * W * K;
     auto mt_window_fill = [&]() {
-        const bool low = running && lane_on && kSeg - wp < 4 * W * K;
+        const bool low = running && lane_on && kSeg - wp < fill_need;
         if (!__any_sync(0xffffffffu, low)) return;
-        const int keep = kSeg - wp;  // < 4WK: at most 4K words per lane
-        uint32_t carry[4 * K];
-#pragma unroll
-        for (int t = 0; t < 4 * K; ++t) {
-            const int i = l + t * W;
-            carry[t] = (low && i < keep) ? seg_mt[wp + i] : 0u;
-        }
-        __syncwarp();
-#pragma unroll
-        for (int t = 0; t < 4 * K; ++t) {
-            const int i = l + t * W;
-            if (low && i < keep) seg_mt[kSide - keep + i] = carry[t];
-        }
+        // keep < fill_need <= kSide words move down by exactly one block (624 > keep: the ranges are
+        // disjoint), ending just below the block
+        const int keep = kSeg - wp;
+        if (low)
+            for (int i = l; i < keep; i += W) seg_mt[kSide - keep + i] = seg_mt[wp + i];
         mt_twist(low);  // starts and ends with __syncwarp
         if (low) wp = kSide - keep;
     };
-    // window offset k -> raw word.  No clamp: after mt_window_fill the window holds >= 4WK words and
-    // a round reads below offset 4WK + 4, so an idle lane's read lands at most 3 words past the
-    // segment, inside the block's dynamic shared memory (the next segment or the position rows).
+    // window offset k -> raw word.  No clamp: after mt_window_fill the window holds >= fill_need words
+    // and a round reads below offset fill_need + 4, so an idle lane's read lands at most 3 words past
+    // the segment, inside the block's dynamic shared memory (the next segment or the position rows).
     auto mt_word = [&](int k) -> uint32_t { return seg_mt[wp + k]; };
     auto mt_consume = [&](int c) { wp += c; };
     // One step draw per (slot, lane) with want[k], in competitor-index order within each segment
@@ -209,6 +207,76 @@ exact_kernel(const LaunchArgs a) {
                 d[k] = want[k] ? __dadd_rn(lo[k], __dmul_rn(span[k], mt_random53(w0, w1))) : 1.0;
             }
             if (lane_on && running) mt_consume(slot_base);
+            return;
+        }
+        if constexpr (K == 1) {
+            // ---- K = 1: one trial-evaluation pass per round ----
+            // Offsets are speculative as below (each pending lognormal draw takes 4 words); then the
+            // pending lognormal draw of rank i in its segment evaluates its trials j = 0..T-1 (words
+            // off_i + 4j) on lanes i*T + j, T = the largest power of two <= kMtMaxTrials with m*T <= W
+            // for m such draws.  In index
+            // order, draw i starts `shift` trials into its grid (the extra trials of the draws before
+            // it) and accepts at the first accepting trial from there; the lanes after it move by its
+            // extra trials.  A draw with no accepting trial left in its grid ends the round: it and
+            // every later draw stay pending, its grid's words are consumed.
+            bool pend = want[0], got_ln = false;
+            double u1a = 0.0, u2a = 1.0;
+            d[0] = 1.0;
+            while (__any_sync(0xffffffffu, pend)) {
+                mt_window_fill();
+                const unsigned pm = __ballot_sync(0xffffffffu, pend) & segmask;
+                const unsigned lm = __ballot_sync(0xffffffffu, pend && lognorm[0]) & segmask;
+                const int off = 2 * (__popc(pm & lt_mask) + __popc(lm & lt_mask));
+                const int used_all = 2 * (__popc(pm) + __popc(lm));
+                const int m = __popc(lm);
+                // T: the largest power of two <= kMtMaxTrials with m*T <= W (shifts, no division)
+                const int lt = (8 * m <= W) ? 3 : (4 * m <= W) ? 2 : (2 * m <= W) ? 1 : 0;
+                const int T = 1 << lt;
+                const int ti = l >> lt, tj = l & (T - 1);
+                if (pend && lognorm[0]) ln_off[base + __popc(lm & lt_mask)] = off;
+                __syncwarp();
+                bool acc = false;
+                if (lane_on && running && ti < m) {
+                    const int at = ln_off[base + ti] + 4 * tj;
+                    acc = km_accept(mt_temper(mt_word(at)), mt_word(at + 1), mt_temper(mt_word(at + 2)),
+                                    mt_temper(mt_word(at + 3)), a.nv_magic);
+                }
+                const unsigned am = __ballot_sync(0xffffffffu, acc) & segmask;
+                int shift = 0, my_shift = 0, my_grid = 0, fail_lane = kWarp, fail_used = 0;
+                unsigned rem = lm;
+                for (int i = 0; i < m; ++i) {
+                    const int li = __ffs(rem) - 1;
+                    rem &= rem - 1u;
+                    const unsigned avail = ((am >> (base + i * T)) & ((1u << T) - 1u)) >> shift;
+                    if (!avail) {
+                        fail_lane = li;
+                        fail_used = ln_off[base + i] + 4 * T;
+                        break;
+                    }
+                    const int t = __ffs(avail) - 1;  // extra trials of draw i
+                    if (lane == li) my_grid = shift + t;
+                    shift += t;
+                    if (lane > li) my_shift = shift;
+                }
+                __syncwarp();  // ln_off reads precede the next round's writes
+                if (pend && lane < fail_lane) {
+                    const int at = off + 4 * (lognorm[0] ? my_grid : my_shift);
+                    const double r = mt_random53(mt_temper(mt_word(at)), mt_temper(mt_word(at + 1)));
+                    if (lognorm[0]) {
+                        got_ln = true;
+                        u1a = r;
+                        u2a = __dsub_rn(1.0, mt_random53(mt_temper(mt_word(at + 2)), mt_temper(mt_word(at + 3))));
+                    } else {
+                        d[0] = __dadd_rn(lo[0], __dmul_rn(span[0], r));
+                    }
+                    pend = false;
+                }
+                if (lane_on && running) mt_consume(fail_lane < kWarp ? fail_used : used_all + 4 * shift);
+            }
+            if (got_ln) {
+                const double z = __ddiv_rn(__dmul_rn(a.nv_magic, __dsub_rn(u1a, 0.5)), u2a);
+                d[0] = __dmul_rn(scale[0], libm_exp(__dadd_rn(mu[0], __dmul_rn(z, sigma[0]))));
+            }
             return;
         }
         double ln_u1[K], ln_u2[K];  // the accepted Kinderman-Monahan pair of a lognormal competitor
