@@ -22,6 +22,7 @@ M64 = (1 << 64) - 1
 
 
 _INPLACE_OK: bool | None = None
+_MT_SPLIT_MIN = 16384  # rp_predict(mode="mt") splits d >= 2x this into two overlapped launches
 _IDX_OFF, _STATE_OFF = 16, 20  # CPython RandomObject: PyObject_HEAD (16 B), int index, uint32_t state[624]
 
 
@@ -118,6 +119,20 @@ def dry_run_seeds_many(rngs, ds, out_lens) -> list:
     return outs
 
 
+def _end_both(first, second):
+    """Wait for two pending batches; both are always ended (their contexts released), and the first
+    batch's error, if any, wins -- it holds the lower sim indices."""
+    out, err = [], None
+    for p in (first, second):
+        try:
+            out.append(p.end())
+        except Exception as e:  # noqa: BLE001 -- re-raised below
+            err = err or e
+    if err is not None:
+        raise err
+    return out
+
+
 def rp_predict(state, config, d: int, rng, *, mode: str = "mt") -> tuple[float, ...]:
     """Laplace-smoothed win probabilities from d dry-run continuations, computed on the GPU.
 
@@ -131,7 +146,18 @@ def rp_predict(state, config, d: int, rng, *, mode: str = "mt") -> tuple[float, 
         dry_run_seeds(rng, d, want=False)
         return tuple(1 / (d + n) for _ in range(n))
     if mode == "mt":
-        res = simulate_batch(state, config, d, mode="mt", seeds=dry_run_seeds(rng, d), ranks=False)
+        if d < 2 * _MT_SPLIT_MIN:
+            res = simulate_batch(state, config, d, mode="mt", seeds=dry_run_seeds(rng, d), ranks=False)
+        else:
+            # two halves, each enqueued as soon as its seeds exist: the host draws the second half's
+            # seeds while the GPU seeds and races the first, and the second launch (its own stream)
+            # fills the first one's tail.  Same seeds, same sims: the summed tallies are unchanged.
+            h = d // 2
+            first = simulate_batch_begin(state, config, h, mode="mt", seeds=dry_run_seeds(rng, h), ranks=False)
+            second = simulate_batch_begin(state, config, d - h, mode="mt", seeds=dry_run_seeds(rng, d - h),
+                                          sim_offset=h, ranks=False)
+            r0, r1 = _end_both(first, second)
+            return tuple((int(a) + int(b) + 1) / (d + n) for a, b in zip(r0.wins, r1.wins))
     else:
         # the first dry-run seed keys the Philox stream; the other d-1 draws only advance the
         # bettor's stream, which the host does while the kernel runs

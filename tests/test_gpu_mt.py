@@ -59,6 +59,25 @@ def test_rp_predict_mt_equals_reference():
     assert agent.random() == g["agent_next_random"]  # the bettor's stream advanced exactly as the reference's
 
 
+def test_rp_predict_mt_split_launches_equal_oracle():
+    """d >= 2 * _MT_SPLIT_MIN runs as two overlapped launches: the probabilities are still the
+    reference algorithm's over the bettor's d getrandbits(64) seeds, and the stream advances by d."""
+    import random
+
+    from paper_2108_02419_b200 import agents
+
+    g = c2()
+    cfg, st = config_from_dict(g["config"]), state_from_dict(g["state"])
+    d = 2 * agents._MT_SPLIT_MIN + 7
+    agent, twin = random.Random(5), random.Random(5)
+    probs = rp_predict(st, cfg, d, agent, mode="mt")
+    seeds = np.array([twin.getrandbits(64) for _ in range(d)], np.uint64)
+    ob = oracle.batch(cfg, d, state=st, seeds=seeds, threads=8)
+    n = cfg.n_competitors
+    assert probs == tuple((int(w) + 1) / (d + n) for w in ob["wins"])
+    assert agent.random() == twin.random()
+
+
 @pytest.mark.parametrize("n_sims", [1, 97, 20_000])
 def test_c2_batch_matches_oracle(n_sims):
     g = c2()
