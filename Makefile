@@ -1,6 +1,6 @@
 # Builds the product library (sm_100a device code + host C++) and the test oracle.
-# The kernel translation units (native K = 1, native K = 2-4, exact) and the host code compile in
-# parallel (make -j).
+# The kernel translation units (native K = 1 and K = 2-4, each per ticks-per-block NT; exact) and the
+# host code compile in parallel (make -j).
 NVCC ?= nvcc
 CXX ?= g++
 ARCH = -gencode arch=compute_100a,code=sm_100a
@@ -11,8 +11,9 @@ LIBDIR ?= paper_2108_02419_b200/_lib
 LIB = $(LIBDIR)/libbbe_sim.so
 CSRC = paper_2108_02419_b200/csrc
 COMMON = $(CSRC)/common.cuh $(CSRC)/kernels.h include/bbe_sim.h
-OBJS = $(LIBDIR)/bbe_sim.o $(LIBDIR)/kernels_native_k1.o $(LIBDIR)/kernels_native.o $(LIBDIR)/kernels_exact.o \
-       $(LIBDIR)/host_mt.o
+NATIVE_OBJS = $(LIBDIR)/kernels_native_k1_nt8.o $(LIBDIR)/kernels_native_k1_nt16.o \
+              $(LIBDIR)/kernels_native_kn_nt4.o $(LIBDIR)/kernels_native_kn_nt16.o
+OBJS = $(LIBDIR)/bbe_sim.o $(NATIVE_OBJS) $(LIBDIR)/kernels_exact.o $(LIBDIR)/host_mt.o
 
 all: $(LIB) oracle
 
@@ -20,13 +21,15 @@ $(LIBDIR)/bbe_sim.o: $(CSRC)/bbe_sim.cu $(COMMON)
 	@mkdir -p $(LIBDIR)
 	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $(LIBDIR)/ptxas_host.log || (cat $(LIBDIR)/ptxas_host.log; exit 1)
 
-$(LIBDIR)/kernels_native_k1.o: $(CSRC)/kernels_native.cu $(CSRC)/native_kernel.cuh $(COMMON)
+# native kernels: one object per (K half, ticks per block NT)
+NATIVE_DEPS = $(CSRC)/kernels_native.cu $(CSRC)/native_kernel.cuh $(COMMON)
+$(LIBDIR)/kernels_native_k1_nt%.o: $(NATIVE_DEPS)
 	@mkdir -p $(LIBDIR)
-	$(NVCC) $(NVFLAGS) -DBBE_NATIVE_K1 -c -o $@ $< 2> $(LIBDIR)/ptxas_native_k1.log || (cat $(LIBDIR)/ptxas_native_k1.log; exit 1)
+	$(NVCC) $(NVFLAGS) -DBBE_NATIVE_K1 -DBBE_NATIVE_NT=$* -c -o $@ $< 2> $(LIBDIR)/ptxas_native_k1_nt$*.log || (cat $(LIBDIR)/ptxas_native_k1_nt$*.log; exit 1)
 
-$(LIBDIR)/kernels_native.o: $(CSRC)/kernels_native.cu $(CSRC)/native_kernel.cuh $(COMMON)
+$(LIBDIR)/kernels_native_kn_nt%.o: $(NATIVE_DEPS)
 	@mkdir -p $(LIBDIR)
-	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $(LIBDIR)/ptxas_native.log || (cat $(LIBDIR)/ptxas_native.log; exit 1)
+	$(NVCC) $(NVFLAGS) -DBBE_NATIVE_NT=$* -c -o $@ $< 2> $(LIBDIR)/ptxas_native_kn_nt$*.log || (cat $(LIBDIR)/ptxas_native_kn_nt$*.log; exit 1)
 
 $(LIBDIR)/kernels_exact.o: $(CSRC)/kernels_exact.cu $(CSRC)/exact_kernel.cuh $(CSRC)/mt_stream.cuh $(COMMON)
 	@mkdir -p $(LIBDIR)
@@ -38,7 +41,7 @@ $(LIBDIR)/host_mt.o: $(CSRC)/host_mt.cpp
 
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $^ -ldl
-	@cat $(LIBDIR)/ptxas_native_k1.log $(LIBDIR)/ptxas_native.log $(LIBDIR)/ptxas_exact.log > $(LIBDIR)/ptxas.log
+	@cat $(LIBDIR)/ptxas_native_k1_nt*.log $(LIBDIR)/ptxas_native_kn_nt*.log $(LIBDIR)/ptxas_exact.log > $(LIBDIR)/ptxas.log
 
 oracle:
 	$(MAKE) -s -C oracle

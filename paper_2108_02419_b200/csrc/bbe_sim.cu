@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -381,14 +382,52 @@ void philox_round_keys(uint64_t seed, uint32_t* rk) {
 #endif
 
 struct Plan {
-    int mode, n, K, W, S, CH, WP, nperm, tally_len;
+    int mode, n, K, W, S, CH, WP, nperm, tally_len, NT;
     size_t smem;
     KernelFn fn;
     int grid;
 };
 
-int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, const bbe_request* rq, int want_perms,
-              Plan* pl) {
+// Expected ticks until the last racing competitor finishes, ignoring blocking: max over racing c of
+// (L - pos_c) / (mean step of c), the mean step at the smaller responsiveness multiplier.
+double expected_ticks(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st) {
+    double t = 0.0;
+    for (int c = 0; c < race->n; ++c) {
+        if (!st->from_start && st->finish_ticks[c] >= 0) continue;
+        const bbe_competitor& p = comps[c];
+        const double draw = p.family == BBE_FAMILY_LOGNORMAL ? p.scale * std::exp(p.mu + 0.5 * p.sigma * p.sigma)
+                                                             : 0.5 * (p.lo + p.hi);
+        const double step = p.pref_factor * std::min(p.early_mult, p.late_mult) * draw;
+        const double rem = race->track_length - (st->from_start ? 0.0 : st->positions[c]);
+        if (step > 0.0) t = std::max(t, rem / step);
+    }
+    return t;
+}
+
+// NATIVE ticks per block (native_kernel.cuh NT) from the expected race length T.  A boundary costs
+// about 1.5 ticks' work at C2 (more in scan-free fields) and a finished segment idles (NT-1)/2 ticks
+// on average; the thresholds are read off a sweep of NT over race lengths (profiles/r1_ticks_sweep.md):
+// K = 1: 16 from ~43 ticks, else 8; K = 2 without a scan: 16 from ~21 ticks, else 4; other layouts 4
+// (longer blocks spill there).  BBE_TICKS overrides (tuning).
+int pick_ticks(int K, bool scan, double T) {
+    static const int env = [] {
+        const char* e = std::getenv("BBE_TICKS");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (env == 4 || env == 8 || env == 16) return K == 1 ? (env == 16 ? 16 : 8) : env;
+    if (K == 1) return T >= 43.0 ? 16 : 8;
+    if (K == 2 && !scan) return T >= 21.0 ? 16 : 4;
+    return 4;
+}
+
+KernelFn pick_native(int k, int ch, bool scan, int vec, int nt) {
+    if (k == 1) return nt == 16 ? pick_native_k1_nt16(ch, scan, vec) : pick_native_k1_nt8(ch, scan, vec);
+    if (vec != 4) return nullptr;
+    return nt == 16 ? pick_native_kn_nt16(k, ch, scan) : pick_native_kn_nt4(k, ch, scan);
+}
+
+int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, const bbe_state* st,
+              const bbe_request* rq, int want_perms, Plan* pl) {
     bool scan = false;  // any theta > 0: the front-runner scan is needed
     bool ln = false;    // any lognormal competitor (MT: speculative draw rounds)
     for (int c = 0; c < race->n; ++c) {
@@ -418,8 +457,13 @@ int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, co
     pl->tally_len = TL.len();
     const int kmode = rq->mode == BBE_MODE_NATIVE ? NATIVE : (rq->mode == BBE_MODE_MT ? MT : INJECT);
     pl->smem = smem_bytes(kmode, (TL.hist_len() + 1) & ~1, pl->K, pl->S, pl->WP);
-    pl->fn = rq->mode == BBE_MODE_NATIVE ? pick_native(pl->K, pl->CH, scan, vec2 ? 2 : 4)
+    pl->NT = rq->mode == BBE_MODE_NATIVE ? pick_ticks(pl->K, scan, expected_ticks(race, comps, st)) : 4;
+    pl->fn = rq->mode == BBE_MODE_NATIVE ? pick_native(pl->K, pl->CH, scan, vec2 ? 2 : 4, pl->NT)
                                          : pick_exact(rq->mode == BBE_MODE_MT ? MT : INJECT, pl->K, ln);
+    if (!pl->fn && rq->mode == BBE_MODE_NATIVE && pl->NT != 4) {
+        pl->NT = 4;  // that block length is not built for this layout
+        pl->fn = pick_native(pl->K, pl->CH, scan, vec2 ? 2 : 4, 4);
+    }
     if (!pl->fn) return fail(BBE_EINVAL, "no kernel for this configuration");
     // the kernel's dynamic-smem limit only ever grows (a smaller later request keeps the larger
     // limit valid); residency per (kernel, dynamic smem) is queried once per device
@@ -818,7 +862,7 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
     const int n = race->n;
     const int64_t ns = rq->n_sims;
     Plan pl;
-    if ((rc = make_plan(ctx, race, comps, rq, out->perms != nullptr, &pl))) return rc;
+    if ((rc = make_plan(ctx, race, comps, st, rq, out->perms != nullptr, &pl))) return rc;
     cudaStream_t s = ctx->stream;
 
     // parameters and the zeroed tally: one pinned staging block, one H2D copy
@@ -1104,7 +1148,7 @@ int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const 
     DevCtx* const ctx = lease.c;
     Plan pl;
     const bool perms = nperm_for(race->n) > 0;
-    if ((rc = make_plan(ctx, race, comps, rq, perms, &pl))) return rc;
+    if ((rc = make_plan(ctx, race, comps, st, rq, perms, &pl))) return rc;
     cudaStream_t s = (cudaStream_t)stream;  // NULL = legacy default stream (torch's default)
     // parameters: staged through pinned memory; the copy is ordered on `s` before the kernel, and
     // the staging block is not reused until that copy has been consumed (sync on an event).

@@ -15,9 +15,14 @@ namespace bbe {
 
 typedef void (*KernelFn)(LaunchArgs);
 
-// NATIVE: K competitors per lane, CH key chunks of VEC (4 or 2) words, SCAN = some theta > 0
-KernelFn pick_native(int k, int ch, bool scan, int vec);
-KernelFn pick_native_k1(int ch, bool scan, int vec);  // the K = 1 half (its own translation unit)
+// NATIVE: K competitors per lane, CH key chunks of VEC (4 or 2) words, SCAN = some theta > 0, NT
+// ticks per block; nullptr where that combination is not built (see kernels_native.cu)
+KernelFn pick_native(int k, int ch, bool scan, int vec, int nt);
+// the per-translation-unit halves (kernels_native.cu built once per K half and NT)
+KernelFn pick_native_k1_nt8(int ch, bool scan, int vec);
+KernelFn pick_native_k1_nt16(int ch, bool scan, int vec);
+KernelFn pick_native_kn_nt4(int k, int ch, bool scan);
+KernelFn pick_native_kn_nt16(int k, int ch, bool scan);
 // INJECT / MT (mode: INJECT or MT), K competitors per lane, LN = some lognormal competitor (MT)
 KernelFn pick_exact(int mode, int k, bool ln);
 // c_mt_init (init_genrand(19650218)), and the host libm's exp table for MT lognormal steps

@@ -16,7 +16,7 @@
 // per rival) that yields the nearest key strictly ahead together with the lowest index holding it.
 //
 // Sims: persistent grid; each segment starts on one sim and claims the next from a per-launch counter
-// at a 4-tick block boundary (common.cuh claim_next_sim).  Bookkeeping is kept off the per-tick path:
+// at a block boundary of NT ticks (common.cuh claim_next_sim).  Bookkeeping is kept off the per-tick path:
 // rt (ticks advanced in the sim) is segment-uniform; racing <=> fin == kRacing (int32 finish tick
 // relative to the state's tick); the tick-limit check runs at block boundaries; competitor-timesteps
 // are summed from finish ticks at finalize; finish-order ranks come from one u64 key per competitor.
@@ -73,7 +73,11 @@ __device__ __forceinline__ void lognormal_pair(uint32_t wa, uint32_t wb, float s
 // SCAN = false: every theta is 0, so nobody can be blocked (gap > 0 = theta) and the front-runner
 // scan's result would never be used; the kernel then omits it.
 // VEC: key-row load width in words (4: LDS.128, 2: LDS.64 -- fewer padding keys when W % 4 is 1 or 2).
-template <int K, int CH, bool SCAN, int VEC = 4>
+// NT: ticks per block (a multiple of 4: one Philox call per slot per 4 ticks).  A block boundary --
+// limit check, finish ballot, refill, the next draws -- costs about 1.5 ticks' work in C2, while a
+// finished segment idles (NT-1)/2 ticks on average until the next boundary, so the host picks NT
+// from the race's expected remaining length (bbe_sim.cu pick_ticks).
+template <int K, int CH, bool SCAN, int VEC = 4, int NT = 4>
 __global__ void __launch_bounds__(kBlockThreads, K == 1 ? BBE_NATIVE_MINBLOCKS_K1 : (K == 2 ? 5 : 3))
 native_kernel(const LaunchArgs a) {
     static_assert(VEC == 4 || VEC == 2, "key rows are read 4 or 2 words at a time");
@@ -154,7 +158,8 @@ native_kernel(const LaunchArgs a) {
     float pos[K], prev[K];
     int32_t fin[K];
     bool started[K];  // racing when the sim began (its competitor-timesteps = ticks until it stops)
-    float rawd[K][kTicksPerBlock];
+    static_assert(NT % 4 == 0 && NT >= 4 && NT <= 16, "4, 8, 12 or 16 ticks per block");
+    float rawd[K][NT];
     uint32_t blk_sim = 0;
     unsigned long long ct_tot = 0, blk_tot = 0, n_div = 0;
     int64_t first_div = INT64_MAX;
@@ -292,31 +297,36 @@ native_kernel(const LaunchArgs a) {
         }
         if (!__any_sync(0xffffffffu, running)) break;
 
-        // ---------------- Philox: 4 draws per slot for this block of ticks ----------------
+        // ---------------- Philox: 4 draws per slot per call, NT/4 calls per block of ticks -------------
+        // counter word 0 = tick / 4, so the stream does not depend on the block length
         __syncwarp();  // key rows: the previous block's reads precede this block's writes
         {
             const uint64_t gs = (uint64_t)(a.sim_offset + s);
-            const uint32_t blk = (uint32_t)rt >> 2;
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const U4 w = philox_rk(U4{blk, (uint32_t)cidx[k], (uint32_t)gs, (uint32_t)(gs >> 32)}, a.rk);
-                rawd[k][0] = fmaf(span[k], one_plus_u(w.x), lms[k]);
-                rawd[k][1] = fmaf(span[k], one_plus_u(w.y), lms[k]);
-                rawd[k][2] = fmaf(span[k], one_plus_u(w.z), lms[k]);
-                rawd[k][3] = fmaf(span[k], one_plus_u(w.w), lms[k]);
-                if (any_lognorm) {  // warp-uniform: no divergent second copy of the Philox rounds
-                    float l0, l1, l2, l3;
-                    lognormal_pair(w.x, w.y, sg2[k], lmu2[k], l0, l1);
-                    lognormal_pair(w.z, w.w, sg2[k], lmu2[k], l2, l3);
-                    rawd[k][0] = lognorm[k] ? l0 : rawd[k][0];
-                    rawd[k][1] = lognorm[k] ? l1 : rawd[k][1];
-                    rawd[k][2] = lognorm[k] ? l2 : rawd[k][2];
-                    rawd[k][3] = lognorm[k] ? l3 : rawd[k][3];
+            for (int h = 0; h < NT / 4; ++h) {
+                const uint32_t blk = ((uint32_t)rt >> 2) + h;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const U4 w = philox_rk(U4{blk, (uint32_t)cidx[k], (uint32_t)gs, (uint32_t)(gs >> 32)}, a.rk);
+                    float* const rd4 = &rawd[k][4 * h];
+                    rd4[0] = fmaf(span[k], one_plus_u(w.x), lms[k]);
+                    rd4[1] = fmaf(span[k], one_plus_u(w.y), lms[k]);
+                    rd4[2] = fmaf(span[k], one_plus_u(w.z), lms[k]);
+                    rd4[3] = fmaf(span[k], one_plus_u(w.w), lms[k]);
+                    if (any_lognorm) {  // warp-uniform: no divergent second copy of the Philox rounds
+                        float l0, l1, l2, l3;
+                        lognormal_pair(w.x, w.y, sg2[k], lmu2[k], l0, l1);
+                        lognormal_pair(w.z, w.w, sg2[k], lmu2[k], l2, l3);
+                        rd4[0] = lognorm[k] ? l0 : rd4[0];
+                        rd4[1] = lognorm[k] ? l1 : rd4[1];
+                        rd4[2] = lognorm[k] ? l2 : rd4[2];
+                        rd4[3] = lognorm[k] ? l3 : rd4[3];
+                    }
                 }
             }
         }
 
-        // ---------------- 4 synchronous ticks ----------------
+        // ---------------- NT synchronous ticks ----------------
         auto tick = [&](const int tj) {
             bool racing[K];
 #pragma unroll
@@ -439,7 +449,7 @@ native_kernel(const LaunchArgs a) {
             rt += 1;
         };
 #pragma unroll
-        for (int tj = 0; tj < kTicksPerBlock; ++tj) tick(tj);
+        for (int tj = 0; tj < NT; ++tj) tick(tj);
     }
 
     // ---------------- flush ----------------

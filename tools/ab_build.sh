@@ -6,6 +6,6 @@ set -e
 cd "$(dirname "$0")/.."
 OUT=paper_2108_02419_b200/_lib/ab/$1
 mkdir -p "$OUT"
-make -s -j5 LIBDIR="$OUT" NVEXTRA="$2" "$OUT/libbbe_sim.so"
+make -s -j8 LIBDIR="$OUT" NVEXTRA="$2" "$OUT/libbbe_sim.so"
 cp "$OUT/libbbe_sim.so" "paper_2108_02419_b200/_lib/ab/libbbe_$1.so"
 echo "built paper_2108_02419_b200/_lib/ab/libbbe_$1.so"
