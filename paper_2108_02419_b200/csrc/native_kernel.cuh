@@ -33,6 +33,9 @@ namespace bbe {
 #ifndef BBE_SPREAD_TAIL
 #define BBE_SPREAD_TAIL 1
 #endif
+#ifndef BBE_NATIVE_MINBLOCKS_K2
+#define BBE_NATIVE_MINBLOCKS_K2 5
+#endif
 #ifndef BBE_NATIVE_MINBLOCKS_K1
 #define BBE_NATIVE_MINBLOCKS_K1 7  // 64 registers -> 8 resident blocks of 4 warps
 #endif
@@ -78,7 +81,7 @@ __device__ __forceinline__ void lognormal_pair(uint32_t wa, uint32_t wb, float s
 // finished segment idles (NT-1)/2 ticks on average until the next boundary, so the host picks NT
 // from the race's expected remaining length (bbe_sim.cu pick_ticks).
 template <int K, int CH, bool SCAN, int VEC = 4, int NT = 4>
-__global__ void __launch_bounds__(kBlockThreads, K == 1 ? BBE_NATIVE_MINBLOCKS_K1 : (K == 2 ? 5 : 3))
+__global__ void __launch_bounds__(kBlockThreads, K == 1 ? BBE_NATIVE_MINBLOCKS_K1 : (K == 2 ? BBE_NATIVE_MINBLOCKS_K2 : 3))
 native_kernel(const LaunchArgs a) {
     static_assert(VEC == 4 || VEC == 2, "key rows are read 4 or 2 words at a time");
     extern __shared__ __align__(16) unsigned long long s_dyn[];
@@ -297,34 +300,30 @@ native_kernel(const LaunchArgs a) {
         }
         if (!__any_sync(0xffffffffu, running)) break;
 
-        // ---------------- Philox: 4 draws per slot per call, NT/4 calls per block of ticks -------------
+        // ---------------- Philox: 4 draws per slot per call ----------------
         // counter word 0 = tick / 4, so the stream does not depend on the block length
-        __syncwarp();  // key rows: the previous block's reads precede this block's writes
-        {
+        auto draw4 = [&](const int h) {
             const uint64_t gs = (uint64_t)(a.sim_offset + s);
+            const uint32_t blk = ((uint32_t)rt >> 2) + h;
 #pragma unroll
-            for (int h = 0; h < NT / 4; ++h) {
-                const uint32_t blk = ((uint32_t)rt >> 2) + h;
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const U4 w = philox_rk(U4{blk, (uint32_t)cidx[k], (uint32_t)gs, (uint32_t)(gs >> 32)}, a.rk);
-                    float* const rd4 = &rawd[k][4 * h];
-                    rd4[0] = fmaf(span[k], one_plus_u(w.x), lms[k]);
-                    rd4[1] = fmaf(span[k], one_plus_u(w.y), lms[k]);
-                    rd4[2] = fmaf(span[k], one_plus_u(w.z), lms[k]);
-                    rd4[3] = fmaf(span[k], one_plus_u(w.w), lms[k]);
-                    if (any_lognorm) {  // warp-uniform: no divergent second copy of the Philox rounds
-                        float l0, l1, l2, l3;
-                        lognormal_pair(w.x, w.y, sg2[k], lmu2[k], l0, l1);
-                        lognormal_pair(w.z, w.w, sg2[k], lmu2[k], l2, l3);
-                        rd4[0] = lognorm[k] ? l0 : rd4[0];
-                        rd4[1] = lognorm[k] ? l1 : rd4[1];
-                        rd4[2] = lognorm[k] ? l2 : rd4[2];
-                        rd4[3] = lognorm[k] ? l3 : rd4[3];
-                    }
+            for (int k = 0; k < K; ++k) {
+                const U4 w = philox_rk(U4{blk, (uint32_t)cidx[k], (uint32_t)gs, (uint32_t)(gs >> 32)}, a.rk);
+                float* const rd4 = &rawd[k][4 * h];
+                rd4[0] = fmaf(span[k], one_plus_u(w.x), lms[k]);
+                rd4[1] = fmaf(span[k], one_plus_u(w.y), lms[k]);
+                rd4[2] = fmaf(span[k], one_plus_u(w.z), lms[k]);
+                rd4[3] = fmaf(span[k], one_plus_u(w.w), lms[k]);
+                if (any_lognorm) {  // warp-uniform: no divergent second copy of the Philox rounds
+                    float l0, l1, l2, l3;
+                    lognormal_pair(w.x, w.y, sg2[k], lmu2[k], l0, l1);
+                    lognormal_pair(w.z, w.w, sg2[k], lmu2[k], l2, l3);
+                    rd4[0] = lognorm[k] ? l0 : rd4[0];
+                    rd4[1] = lognorm[k] ? l1 : rd4[1];
+                    rd4[2] = lognorm[k] ? l2 : rd4[2];
+                    rd4[3] = lognorm[k] ? l3 : rd4[3];
                 }
             }
-        }
+        };
 
         // ---------------- NT synchronous ticks ----------------
         auto tick = [&](const int tj) {
@@ -448,6 +447,9 @@ native_kernel(const LaunchArgs a) {
             }
             rt += 1;
         };
+        __syncwarp();  // key rows: the previous block's reads precede this block's writes
+#pragma unroll
+        for (int h = 0; h < NT / 4; ++h) draw4(h);  // independent Philox chains, issued together
 #pragma unroll
         for (int tj = 0; tj < NT; ++tj) tick(tj);
     }
