@@ -16,7 +16,7 @@ import random
 import numpy as np
 
 from .race import RaceState
-from .sim import _P, lib, simulate_batch, simulate_batch_begin
+from .sim import _P, lib, simulate_batch, simulate_batch_begin, winner_counts
 
 M64 = (1 << 64) - 1
 
@@ -49,8 +49,8 @@ def _advance(rng, d: int, out: np.ndarray | None, out_len: int) -> bool:
     if type(rng) is not random.Random or not _inplace_ok():
         return False
     base = id(rng)
-    rc = lib().bbe_mt_advance64(ctypes.c_void_p(base + _STATE_OFF), ctypes.c_void_p(base + _IDX_OFF), d,
-                                None if out is None else out.ctypes.data_as(_P(ctypes.c_uint64)), out_len)
+    rc = lib().bbe_mt_advance64(base + _STATE_OFF, base + _IDX_OFF, d, None if out is None else out.ctypes.data,
+                                out_len)
     if rc != 0:
         raise RuntimeError("bbe_mt_advance64 failed")
     return True
@@ -162,9 +162,9 @@ def rp_predict(state, config, d: int, rng, *, mode: str = "mt") -> tuple[float, 
         # the first dry-run seed keys the Philox stream; the other d-1 draws only advance the
         # bettor's stream, which the host does while the kernel runs
         key = int(dry_run_seeds(rng, 1)[0])
-        pending = simulate_batch_begin(state, config, d, key, mode=mode, ranks=False)
-        dry_run_seeds(rng, d - 1, want=False)
-        res = pending.end()
+        wins = winner_counts(state, config, d, key, lambda: dry_run_seeds(rng, d - 1, want=False), mode=mode)
+        dn = d + n
+        return tuple((w + 1) / dn for w in wins)
     return tuple((int(w) + 1) / (d + n) for w in res.wins)
 
 

@@ -15,6 +15,7 @@ from __future__ import annotations
 import ctypes
 import math
 import os
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -157,7 +158,7 @@ def lib():
         L.bbe_mt_advance64_many.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32]
         L.bbe_mt_advance64_many.restype = ctypes.c_int
-        L.bbe_mt_advance64.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, _P(ctypes.c_uint64),
+        L.bbe_mt_advance64.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                                        ctypes.c_int64]
         L.bbe_mt_advance64.restype = ctypes.c_int
         L.bbe_param_bytes.argtypes = [ctypes.c_int32]
@@ -425,6 +426,56 @@ class PendingSim:
                 _raise(rc, self._res)
             self._done = self._build(self._res)
         return self._done
+
+
+class _WinsCall:
+    """The ctypes structures of one winner-tally call, kept per thread and reused: rp_predict's
+    native path makes one such call per prediction, and building the request/result structures
+    costs more host time than the rest of the call's Python."""
+
+    def __init__(self):
+        self.req = BbeRequest()
+        self.res = BbeResult()
+        self.wins = np.zeros(MAX_COMPETITORS, np.uint64)
+        self.res.wins = self.wins.ctypes.data
+        self.res.first_diverged = -1
+        self.res.first_bad_draws = -1
+        self.busy = False
+
+
+_tls = threading.local()
+
+
+def winner_counts(state, config, n_sims: int, seed: int, host_work=None, *, mode: str = "native") -> list:
+    """Winner counts of ``n_sims`` continuations (``simulate_batch(..., ranks=False).wins`` as a
+    list of ints), through per-thread reused call structures.  ``host_work()``, if given, runs
+    while the kernel does (between bbe_simulate_begin and bbe_simulate_end)."""
+    c = getattr(_tls, "wins_call", None)
+    if c is None or c.busy:  # first use on this thread, or re-entered from host_work
+        c = _WinsCall()
+        if getattr(_tls, "wins_call", None) is None:
+            _tls.wins_call = c
+    pk = pack_config(config)
+    st, keep = pack_state(state, pk.n)
+    q = c.req
+    q.n_sims, q.sim_offset, q.seed, q.mode = int(n_sims), 0, int(seed) & M64, MODES[mode]
+    c.busy = True
+    try:
+        L = lib()
+        rc = L.bbe_simulate_begin(ctypes.byref(pk.race), pk.comps, ctypes.byref(st), ctypes.byref(q),
+                                  ctypes.byref(c.res))
+        if rc != BBE_OK:
+            _raise(rc, c.res)
+        try:
+            if host_work is not None:
+                host_work()
+        finally:
+            rc = L.bbe_simulate_end(ctypes.byref(c.res))
+        if rc != BBE_OK:
+            _raise(rc, c.res)
+        return c.wins[:pk.n].tolist()
+    finally:
+        c.busy = False
 
 
 def simulate_batch_begin(*args, **kwargs) -> PendingSim:
