@@ -14,6 +14,9 @@
  *                         tallies): run_batch(BatchConfig(workers=N)), batch.py:120-124.
  *   bbe_simulate_async    the same, device-resident: tallies accumulate into a device buffer on a
  *                         caller stream (used by the multi-GPU path before one NCCL all-reduce).
+ *   bbe_rp_predict        agents.py:153-166 rp_predict(state, config, d, rng) in one call: the d
+ *                         getrandbits(64) dry-run seeds drawn from the bettor's own MT19937 state
+ *                         (advanced in place), the d continuations, the winner counts.
  *   bbe_derive_seeds      seeding.py:50-59 derive_seed(master, "run", i) for a range of i.
  *   bbe_last_error        -- (error text for the Python exceptions of race.py:27-32, batch.py:30-38)
  *
@@ -34,7 +37,7 @@
 extern "C" {
 #endif
 
-#define BBE_ABI_VERSION 2
+#define BBE_ABI_VERSION 3 /* 3: bbe_rp_predict */
 #define BBE_MAX_COMPETITORS 128
 #define BBE_MAX_PERM_COMPETITORS 6 /* batch.py:27 MAX_FULL_OUTCOME_COMPETITORS */
 
@@ -163,6 +166,20 @@ int bbe_simulate_end(bbe_result* out);
  * (a cudaStream_t, NULL = legacy default).  Asynchronous: read d_tally after the stream syncs. */
 int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const bbe_state* state,
                        const bbe_request* req, const bbe_result* dev_out, uint64_t* d_tally, void* stream);
+
+/* rp_predict (agents.py:153-166) in one call.  The bettor's CPython random.Random is given as its
+ * MT19937 state (`state624`, 624 words) and position (`pos`, 0..624) -- random.Random.getstate()[1],
+ * or the generator object's own fields -- and is advanced in place by exactly d getrandbits(64), as
+ * the reference's loop advances it (agents.py:164).  wins[n] receives the winner counts of the d
+ * continuations of `state`; the caller forms the Laplace probabilities (w + 1) / (d + n).
+ *   mode BBE_MODE_MT:     dry run i replays random.Random(seed_i), seed_i the i-th getrandbits(64)
+ *                         (simulate_from, race.py:393-406): the reference's own counts, bit for bit.
+ *   mode BBE_MODE_NATIVE: the Philox stream keyed by seed_0 (statistically equal); the other d-1
+ *                         draws only advance the stream, on the host while the GPU runs.
+ * Synchronous.  BBE_EDIVERGED: a dry run exceeded tick_limit (first_diverged, if not NULL, receives
+ * its index in 0..d-1; the stream is advanced by d all the same). */
+int bbe_rp_predict(const bbe_race* race, const bbe_competitor* comps, const bbe_state* state, int64_t d,
+                   int32_t mode, uint32_t* state624, int32_t* pos, uint64_t* wins, int64_t* first_diverged);
 
 /* d_tally layout: [wins n][ranks n*n][perms n! or 0][ct][blocked][diverged count][bad-draw count]
  *                 [(2^63-1) - first_diverged, or 0 = none][(2^63-1) - first_bad_draws, or 0 = none]

@@ -16,7 +16,7 @@ import random
 import numpy as np
 
 from .race import RaceState
-from .sim import _P, lib, simulate_batch, simulate_batch_begin, winner_counts
+from .sim import _P, lib, rp_predict_counts, simulate_batch, simulate_batch_begin
 
 M64 = (1 << 64) - 1
 
@@ -145,6 +145,13 @@ def rp_predict(state, config, d: int, rng, *, mode: str = "mt") -> tuple[float, 
     if d <= 0:
         dry_run_seeds(rng, d, want=False)
         return tuple(1 / (d + n) for _ in range(n))
+    if type(rng) is random.Random and _inplace_ok():
+        # one C call: the d seeds drawn from the bettor's own MT19937 fields (advanced in place), the
+        # dry runs on the GPU (bbe_rp_predict; MT: two overlapped halves when d is large)
+        base = id(rng)
+        wins = rp_predict_counts(state, config, d, base + _STATE_OFF, base + _IDX_OFF, mode=mode)
+        dn = d + n
+        return tuple((w + 1) / dn for w in wins)
     if mode == "mt":
         if d < 2 * _MT_SPLIT_MIN:
             res = simulate_batch(state, config, d, mode="mt", seeds=dry_run_seeds(rng, d), ranks=False)
@@ -162,9 +169,9 @@ def rp_predict(state, config, d: int, rng, *, mode: str = "mt") -> tuple[float, 
         # the first dry-run seed keys the Philox stream; the other d-1 draws only advance the
         # bettor's stream, which the host does while the kernel runs
         key = int(dry_run_seeds(rng, 1)[0])
-        wins = winner_counts(state, config, d, key, lambda: dry_run_seeds(rng, d - 1, want=False), mode=mode)
-        dn = d + n
-        return tuple((w + 1) / dn for w in wins)
+        pending = simulate_batch_begin(state, config, d, key, mode=mode, ranks=False)
+        dry_run_seeds(rng, d - 1, want=False)
+        res = pending.end()
     return tuple((int(w) + 1) / (d + n) for w in res.wins)
 
 

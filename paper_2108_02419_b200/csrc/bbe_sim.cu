@@ -20,6 +20,9 @@
 #include <vector>
 
 #include <dlfcn.h>
+#ifdef BBE_TIMING
+#include <chrono>
+#endif
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX3: named ranges for nsys / ncu timelines
 
 #include "../../include/bbe_sim.h"
@@ -30,6 +33,35 @@ using namespace bbe;
 namespace {
 
 thread_local std::string g_err;
+
+#ifdef BBE_TIMING  // host-side timing probes of the call path (A/B builds only)
+struct Probe {
+    const char* name[16] = {};
+    double sum[16] = {};
+    long cnt[16] = {}, seen[16] = {};
+    ~Probe() {
+        for (int i = 0; i < 16; ++i)
+            if (cnt[i]) std::fprintf(stderr, "probe %-28s %8.2f us\n", name[i], sum[i] / cnt[i]);
+    }
+} g_probe;
+inline double now_us() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+#define PROBE_T0 double t_probe = now_us();
+#define PROBE(i, nm)                                         \
+    do {                                                     \
+        const double t1_ = now_us();                         \
+        g_probe.name[i] = nm;                                \
+        if (++g_probe.seen[i] > 50) {                        \
+            g_probe.sum[i] += t1_ - t_probe;                 \
+            g_probe.cnt[i] += 1;                             \
+        }                                                    \
+        t_probe = t1_;                                       \
+    } while (0)
+#else
+#define PROBE_T0
+#define PROBE(i, nm)
+#endif
 
 struct NvtxRange {  // one named range per C-ABI call (free when no profiler is attached)
     explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
@@ -84,7 +116,7 @@ struct DevCtx {
     int sm_count = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    HostBuf h_params, h_tally;
+    HostBuf h_params, h_tally, h_seeds;  // h_seeds: bbe_rp_predict's MT dry-run seeds
     DevBuf d_params, d_draws, d_offsets, d_winner, d_order, d_fin, d_fpos, d_blocked, d_dused;
     DevBuf d_seeds, d_mt_states, d_mt_scratch;  // MT mode
     DevBuf d_traj;                               // trajectories (positions, previous steps)
@@ -631,6 +663,7 @@ int bbe_derive_seeds(uint64_t master, int64_t first, int64_t count, uint64_t* ou
     return BBE_OK;
 }
 
+constexpr int64_t kRpSplitMin = 16384;  // bbe_rp_predict MT: d >= 2x this runs as two halves
 constexpr int kWorkSlots = 64;  // concurrent native launches per device with their own work counters
 constexpr size_t kMaxStagedBytes = 256ull << 20;  // per-sim outputs staged through pinned memory up to this
 
@@ -853,6 +886,7 @@ static int build_args(const Plan& pl, const bbe_race* race, const bbe_state* st,
 int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, const bbe_request* rq,
                        bbe_result* out) {
     NvtxRange nvtx_range("bbe_simulate_begin");
+    PROBE_T0
     int rc = validate(race, comps, st, rq);
     if (rc) return rc;
     if (!out || !out->wins) return fail(BBE_EINVAL, "result needs a wins buffer");
@@ -861,9 +895,11 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
     DevCtx* const ctx = lease.c;
     const int n = race->n;
     const int64_t ns = rq->n_sims;
+    PROBE(0, "begin: validate+acquire");
     Plan pl;
     if ((rc = make_plan(ctx, race, comps, st, rq, out->perms != nullptr, &pl))) return rc;
     cudaStream_t s = ctx->stream;
+    PROBE(1, "begin: plan");
 
     // parameters and the zeroed tally: one pinned staging block, one H2D copy
     const size_t pbytes = (param_bytes(n) + 63) & ~(size_t)63;
@@ -881,7 +917,9 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
     std::memset((char*)ctx->h_params.p + pbytes, 0, tbytes + gbytes);
     uint64_t* const d_tally = (uint64_t*)((char*)ctx->d_params.p + pbytes);
     uint64_t* const d_groups = groups ? d_tally + pl.tally_len : nullptr;
+    PROBE(2, "begin: pack");
     BBE_CK(cudaMemcpyAsync(ctx->d_params.p, ctx->h_params.p, pbytes + tbytes + gbytes, cudaMemcpyHostToDevice, s));
+    PROBE(3, "begin: H2D api");
 
     const double* d_draws = nullptr;
     const int64_t* d_offsets = nullptr;
@@ -928,11 +966,16 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
     dev.group_wins = d_groups;
     LaunchArgs a;
     build_args(pl, race, st, rq, (const double*)ctx->d_params.p, d_draws, d_offsets, d_tally, &dev, fr, &a);
+    PROBE(4, "begin: outputs+args");
     BBE_CK(cudaEventRecord(ctx->ev0, s));
+    PROBE(5, "begin: record ev0");
     if ((rc = launch_all(ctx, pl, a, comps, d_seeds, rq->seed_master, s))) return rc;
+    PROBE(6, "begin: launch");
     BBE_CK(cudaEventRecord(ctx->ev1, s));
+    PROBE(7, "begin: record ev1");
 
     BBE_CK(cudaMemcpyAsync(ctx->h_tally.p, d_tally, tbytes, cudaMemcpyDeviceToHost, s));
+    PROBE(8, "begin: D2H api");
     // Per-sim outputs go device -> pinned staging asynchronously (a copy into pageable memory would
     // block this call until the kernel ends); _end copies them into the caller's buffers.  Very
     // large outputs (trajectories) are copied directly.
@@ -989,7 +1032,9 @@ int bbe_simulate_end(bbe_result* out) {
     if (!lease.c) return fail(BBE_EINVAL, "no call in flight for this result");
     DevCtx* const ctx = lease.c;
     ctx->pending = false;
+    PROBE_T0
     BBE_CK(cudaStreamSynchronize(ctx->stream));
+    PROBE(9, "end: sync");
     for (const auto& c : ctx->pend_copies) std::memcpy(c.dst, c.src, c.bytes);
     ctx->pend_copies.clear();
     const int n = ctx->pend_n;
@@ -1008,11 +1053,119 @@ int bbe_simulate_end(bbe_result* out) {
     if (ns) cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
     out->kernel_ms = ms;
     out->lanes_per_slot = pl.K;
+    PROBE(10, "end: copy-out+elapsed");
     if (T[TL.n_div()]) return fail(BBE_EDIVERGED, "race exceeded tick_limit=" + std::to_string(ctx->pend_limit) +
                                                       " in sim " + std::to_string(out->first_diverged));
     if (T[TL.n_bad()]) return fail(BBE_EDRAWS, "injected draw stream under/over-consumed in sim " +
                                                    std::to_string(out->first_bad_draws));
     return BBE_OK;
+}
+
+}  // extern "C"
+
+// bbe_rp_predict: one winner-tally launch of rq on ctx's stream -- parameters + zeroed tally H2D,
+// the kernel(s), the tally D2H into ctx->h_tally.  d_seeds (MT) must already be on ctx's stream.
+static int enqueue_tally(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, const bbe_state* st,
+                         const bbe_request& rq, const uint64_t* d_seeds, const Plan& pl) {
+    cudaStream_t s = ctx->stream;
+    const size_t pbytes = (param_bytes(race->n) + 63) & ~(size_t)63;
+    const size_t tbytes = (size_t)pl.tally_len * sizeof(uint64_t);
+    BBE_CK(cudaEventSynchronize(ctx->ev1));  // a previous async launch on this ctx has read its params
+    BBE_CK(ctx->h_params.ensure(pbytes + tbytes));
+    BBE_CK(ctx->d_params.ensure(pbytes + tbytes));
+    BBE_CK(ctx->h_tally.ensure(tbytes));
+    pack_params(race, comps, st, (double*)ctx->h_params.p);
+    const NativeFrame fr = native_frame(race, st, pl.W);
+    pack_params_f32(race, comps, st, (double*)ctx->h_params.p, fr);
+    std::memset((char*)ctx->h_params.p + pbytes, 0, tbytes);
+    uint64_t* const d_tally = (uint64_t*)((char*)ctx->d_params.p + pbytes);
+    BBE_CK(cudaMemcpyAsync(ctx->d_params.p, ctx->h_params.p, pbytes + tbytes, cudaMemcpyHostToDevice, s));
+    LaunchArgs a;
+    build_args(pl, race, st, &rq, (const double*)ctx->d_params.p, nullptr, nullptr, d_tally, nullptr, fr, &a);
+    int rc = launch_all(ctx, pl, a, comps, d_seeds, 0, s);
+    if (rc) return rc;
+    BBE_CK(cudaMemcpyAsync(ctx->h_tally.p, d_tally, tbytes, cudaMemcpyDeviceToHost, s));
+    return BBE_OK;
+}
+
+// bbe_rp_predict, MT: draw `count` dry-run seeds from the bettor's stream straight into ctx's pinned
+// staging, copy them up and enqueue the seeding + race kernels for sims [off, off + count).
+static int enqueue_mt_part(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, const bbe_state* st,
+                           int64_t off, int64_t count, uint32_t* state624, int32_t* pos, Plan* pl) {
+    bbe_request rq{};
+    rq.n_sims = count;
+    rq.sim_offset = off;
+    rq.mode = BBE_MODE_MT;
+    int rc = make_plan(ctx, race, comps, st, &rq, 0, pl);
+    if (rc) return rc;
+    BBE_CK(ctx->h_seeds.ensure((size_t)count * sizeof(uint64_t)));
+    BBE_CK(ctx->d_seeds.ensure((size_t)count * sizeof(uint64_t)));
+    BBE_CK(cudaEventSynchronize(ctx->ev1));  // the staging's previous contents have been copied
+    *pos = (int32_t)bbe_host_mt_getrandbits64(state624, (uint32_t)*pos, count, (uint64_t*)ctx->h_seeds.p, count);
+    BBE_CK(cudaMemcpyAsync(ctx->d_seeds.p, ctx->h_seeds.p, (size_t)count * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                           ctx->stream));
+    return enqueue_tally(ctx, race, comps, st, rq, (const uint64_t*)ctx->d_seeds.p, *pl);
+}
+
+// Wait for a bbe_rp_predict launch and add its winner counts into wins[n]; divergence -> error.
+static int finish_tally(DevCtx* ctx, const Plan& pl, int n, int64_t limit, uint64_t* wins, int64_t* first_div) {
+    BBE_CK(cudaStreamSynchronize(ctx->stream));
+    const uint64_t* T = (const uint64_t*)ctx->h_tally.p;
+    const TallyLayout TL{n, pl.nperm};
+    for (int c = 0; c < n; ++c) wins[c] += T[TL.wins() + c];
+    if (T[TL.n_div()]) {
+        const int64_t fd = decode_first(T[TL.first_div()]);
+        if (first_div && (*first_div < 0 || fd < *first_div)) *first_div = fd;
+        return fail(BBE_EDIVERGED, "race exceeded tick_limit=" + std::to_string(limit) + " in sim " + std::to_string(fd));
+    }
+    return BBE_OK;
+}
+
+extern "C" {
+
+int bbe_rp_predict(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, int64_t d, int32_t mode,
+                   uint32_t* state624, int32_t* pos, uint64_t* wins, int64_t* first_diverged) {
+    NvtxRange nvtx_range("bbe_rp_predict");
+    if (!state624 || !pos || !wins || *pos < 0 || *pos > 624 || d < 0) return fail(BBE_EINVAL, "bad arguments");
+    if (mode != BBE_MODE_NATIVE && mode != BBE_MODE_MT) return fail(BBE_EINVAL, "rp_predict modes: native, mt");
+    bbe_request rq{};
+    rq.n_sims = d;
+    rq.mode = mode;
+    int rc = validate(race, comps, st, &rq);
+    if (rc) return rc;
+    const int n = race->n;
+    std::fill(wins, wins + n, 0ull);
+    if (first_diverged) *first_diverged = -1;
+    if (d == 0) return BBE_OK;
+    Lease lease;
+    if ((rc = acquire_ctx(lease))) return rc;
+    DevCtx* const ctx = lease.c;
+    if (mode == BBE_MODE_NATIVE) {
+        // the first dry-run seed keys the Philox stream; the other d-1 draws advance the bettor's
+        // stream on the host while the kernel runs
+        uint64_t key = 0;
+        *pos = (int32_t)bbe_host_mt_getrandbits64(state624, (uint32_t)*pos, 1, &key, 1);
+        rq.seed = key;
+        Plan pl;
+        if ((rc = make_plan(ctx, race, comps, st, &rq, 0, &pl))) return rc;
+        if ((rc = enqueue_tally(ctx, race, comps, st, rq, nullptr, pl))) return rc;
+        *pos = (int32_t)bbe_host_mt_getrandbits64(state624, (uint32_t)*pos, d - 1, nullptr, 0);
+        return finish_tally(ctx, pl, n, race->tick_limit, wins, first_diverged);
+    }
+    // MT: every dry run replays random.Random(getrandbits(64)).  Large calls run as two halves on two
+    // streams: the host draws the second half's seeds while the GPU runs the first, and the second
+    // launch fills the first one's tail.
+    const int64_t h = d >= 2 * kRpSplitMin ? d / 2 : d;
+    Plan p0, p1;
+    if ((rc = enqueue_mt_part(ctx, race, comps, st, 0, h, state624, pos, &p0))) return rc;
+    if (h == d) return finish_tally(ctx, p0, n, race->tick_limit, wins, first_diverged);
+    Lease lease2;
+    if ((rc = acquire_ctx(lease2))) return rc;
+    rc = enqueue_mt_part(lease2.c, race, comps, st, h, d - h, state624, pos, &p1);
+    const int rc0 = finish_tally(ctx, p0, n, race->tick_limit, wins, first_diverged);
+    if (rc) return rc;
+    const int rc1 = finish_tally(lease2.c, p1, n, race->tick_limit, wins, first_diverged);
+    return rc0 ? rc0 : rc1;
 }
 
 int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, const bbe_request* rq,

@@ -37,7 +37,7 @@ MAX_COMPETITORS = 128
 MAX_PERM_COMPETITORS = 6
 M64 = (1 << 64) - 1
 
-ABI_VERSION = 2  # include/bbe_sim.h BBE_ABI_VERSION
+ABI_VERSION = 3  # include/bbe_sim.h BBE_ABI_VERSION
 
 EXPORTED_SYMBOLS = (
     "bbe_simulate",
@@ -58,6 +58,7 @@ EXPORTED_SYMBOLS = (
     "bbe_mt_exp_exact",
     "bbe_mt_advance64",
     "bbe_mt_advance64_many",
+    "bbe_rp_predict",
 )
 
 
@@ -161,6 +162,9 @@ def lib():
         L.bbe_mt_advance64.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                                        ctypes.c_int64]
         L.bbe_mt_advance64.restype = ctypes.c_int
+        L.bbe_rp_predict.argtypes = [_P(BbeRace), _P(BbeCompetitor), _P(BbeState), ctypes.c_int64, ctypes.c_int32,
+                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.bbe_rp_predict.restype = ctypes.c_int
         L.bbe_param_bytes.argtypes = [ctypes.c_int32]
         L.bbe_param_bytes.restype = ctypes.c_int64
         L.bbe_last_error.restype = ctypes.c_char_p
@@ -428,54 +432,35 @@ class PendingSim:
         return self._done
 
 
-class _WinsCall:
-    """The ctypes structures of one winner-tally call, kept per thread and reused: rp_predict's
-    native path makes one such call per prediction, and building the request/result structures
-    costs more host time than the rest of the call's Python."""
+class _PredictBufs(threading.local):
+    """Per-thread output buffers of bbe_rp_predict (reused: one call at a time per thread)."""
 
     def __init__(self):
-        self.req = BbeRequest()
-        self.res = BbeResult()
         self.wins = np.zeros(MAX_COMPETITORS, np.uint64)
-        self.res.wins = self.wins.ctypes.data
-        self.res.first_diverged = -1
-        self.res.first_bad_draws = -1
-        self.busy = False
+        self.first = np.zeros(1, np.int64)
 
 
-_tls = threading.local()
+_pbufs = _PredictBufs()
 
 
-def winner_counts(state, config, n_sims: int, seed: int, host_work=None, *, mode: str = "native") -> list:
-    """Winner counts of ``n_sims`` continuations (``simulate_batch(..., ranks=False).wins`` as a
-    list of ints), through per-thread reused call structures.  ``host_work()``, if given, runs
-    while the kernel does (between bbe_simulate_begin and bbe_simulate_end)."""
-    c = getattr(_tls, "wins_call", None)
-    if c is None or c.busy:  # first use on this thread, or re-entered from host_work
-        c = _WinsCall()
-        if getattr(_tls, "wins_call", None) is None:
-            _tls.wins_call = c
+def rp_predict_counts(state, config, d: int, state624_addr: int, pos_addr: int, *, mode: str = "mt") -> list:
+    """``bbe_rp_predict``: winner counts of d dry runs whose seeds are d getrandbits(64) of the MT19937
+    state at ``state624_addr`` (624 uint32) / ``pos_addr`` (int32), advanced in place (a CPython
+    random.Random's own fields, agents.py); returns the counts as a list of ints."""
     pk = pack_config(config)
     st, keep = pack_state(state, pk.n)
-    q = c.req
-    q.n_sims, q.sim_offset, q.seed, q.mode = int(n_sims), 0, int(seed) & M64, MODES[mode]
-    c.busy = True
-    try:
-        L = lib()
-        rc = L.bbe_simulate_begin(ctypes.byref(pk.race), pk.comps, ctypes.byref(st), ctypes.byref(q),
-                                  ctypes.byref(c.res))
-        if rc != BBE_OK:
-            _raise(rc, c.res)
-        try:
-            if host_work is not None:
-                host_work()
-        finally:
-            rc = L.bbe_simulate_end(ctypes.byref(c.res))
-        if rc != BBE_OK:
-            _raise(rc, c.res)
-        return c.wins[:pk.n].tolist()
-    finally:
-        c.busy = False
+    b = _pbufs
+    rc = lib().bbe_rp_predict(ctypes.byref(pk.race), pk.comps, ctypes.byref(st), int(d), MODES[mode], state624_addr,
+                              pos_addr, b.wins.ctypes.data, b.first.ctypes.data)
+    if rc != BBE_OK:
+        if rc == BBE_EDIVERGED:
+            raise SimDivergedError(int(b.first[0]), last_error())
+        if rc == BBE_EINVAL:
+            raise RaceConfigError(last_error())
+        if rc == BBE_ENODEV:
+            raise BackendUnavailable(last_error())
+        raise RuntimeError(f"bbe_rp_predict failed ({rc}): {last_error()}")
+    return b.wins[:pk.n].tolist()
 
 
 def simulate_batch_begin(*args, **kwargs) -> PendingSim:

@@ -28,7 +28,7 @@ def test_library_exports_every_header_symbol():
     assert declared and set(declared) == set(sim.EXPORTED_SYMBOLS)
     for name in declared:
         assert hasattr(L, name), name
-    assert L.bbe_version() == 2
+    assert L.bbe_version() == sim.ABI_VERSION == 3
 
 
 def test_tally_layout():

@@ -157,3 +157,20 @@ def test_device_resident_mt_with_device_seeds():
     assert t[:n].tolist() == want.wins.tolist()
     assert t[n:n + n * n].reshape(n, n).tolist() == want.ranks.tolist()
     assert int(t[dl.off["ct"]]) == want.competitor_steps
+
+
+@pytest.mark.parametrize("mode", ["mt", "native"])
+@pytest.mark.parametrize("d", [1, 3000, 2 * 16384 + 3])
+def test_rp_predict_c_entry_equals_python_path(mode, d):
+    """rp_predict on a plain random.Random takes the one-call C entry (bbe_rp_predict); a subclass
+    takes the Python path (dry_run_seeds + simulate_batch).  Same probabilities, same stream."""
+    import random
+
+    class Sub(random.Random):
+        pass
+
+    g = c2()
+    cfg, st = config_from_dict(g["config"]), state_from_dict(g["state"])
+    a, b = random.Random(77), Sub(77)
+    assert rp_predict(st, cfg, d, a, mode=mode) == rp_predict(st, cfg, d, b, mode=mode)
+    assert a.getstate() == b.getstate()
