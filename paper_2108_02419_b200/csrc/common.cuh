@@ -11,7 +11,10 @@ namespace bbe {
 constexpr int kWarp = 32;
 constexpr int kBlockThreads = 128;
 constexpr int kWarpsPerBlock = kBlockThreads / kWarp;
-constexpr int kTicksPerBlock = 4;  // Philox4x32 yields 4 words per call: one per tick
+#ifndef BBE_EXACT_TICKS
+#define BBE_EXACT_TICKS 8  // C2 MT: 4 -> 2.54 ms, 8 -> 2.43, 16 -> 2.42 (bit-identical; 8 idles less on short races)
+#endif
+constexpr int kTicksPerBlock = BBE_EXACT_TICKS;  // exact kernels: ticks between finalize/refill boundaries
 
 // Parameter block fields (SoA, stride n), host-packed in double (see bbe_sim.cu: pack_params).
 enum Field {
