@@ -31,6 +31,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -362,7 +364,10 @@ def run_ours(args):
         # MT mode: the reference's own MT19937 streams, bit-identical results (seeds are H2D inputs)
         mt_steps = max(3, min(args.steps, 20))
         e2e_mt_s = time_calls("mt", mt_steps)
-        mt_kernel_ms = launcher.last_kernel_ms()  # seed kernel + race kernel of the last MT call
+        # device time of one MT batch of the same size (seeding + race kernels, one stream, CUDA events)
+        mt_seeds = np.arange(1, sims + 1, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+        mt_kernel_ms = min(sim.simulate_batch(state, cfg, sims, mode="mt", seeds=mt_seeds, ranks=False).kernel_ms
+                           for _ in range(3))
 
         sweep = sweep_configs(args, torch, sim) if args.sweep else None
         cpu = cpu_baseline_pyref(cfg, state, args.cpu_sample) if args.cpu_sample else None
