@@ -238,11 +238,13 @@ int validate(const bbe_race* race, const bbe_competitor* comps, const bbe_state*
     return BBE_OK;
 }
 
-// Competitors per lane K for the NATIVE kernel (profiles/r1_k_sweep.md: every K timed for n = 1..128,
-// with and without blocking competitors).  util(K) = occupied slots / (32 K) with S = 32 / ceil(n/K)
-// races per warp.  n > 32: the smallest K that fits.  With a front-runner scan (some theta > 0):
-// K = 1, or K = 2 when that fills >= 20 % more slots.  Without: K = 2 (more independent work per
-// lane), K = 1 when it fills > 10 % more slots, K = 3 when that fills > 15 % more than K = 2.
+// Competitors per lane K for the NATIVE kernel (profiles/r1_k_sweep.md: every K timed for n = 6..128,
+// with and without blocking competitors, after the 8/16-tick blocks).  util(K) = occupied slots /
+// (32 K) with S = 32 / ceil(n/K) races per warp.  n > 32: K = 3 when it fits and fills >= 20 % more
+// slots than K = 2, else the smallest K that fits.  With a front-runner scan (some theta > 0): K = 1,
+// or K = 2 when that fills >= 40 % more slots (K = 1 runs 16-tick blocks, K = 2 with a scan 4).
+// Without: K = 2 (more independent work per lane), K = 1 when it fills > 10 % more slots, K = 3 when
+// that fills > 15 % more than K = 2.
 double slot_util(int n, int k) {
     const int w = (n + k - 1) / k;
     if (w > kWarp) return 0.0;
@@ -252,12 +254,14 @@ double slot_util(int n, int k) {
 int choose_k(int n, bool scan, int hint) {
     if (hint > 0 && hint <= 4 && (n + hint - 1) / hint <= kWarp) return hint;
     if (n > kWarp) {
+        const double w2 = slot_util(n, 2), w3 = slot_util(n, 3);
+        if (w2 > 0.0 && w3 > 0.0) return w3 >= 1.2 * w2 ? 3 : 2;
         for (int k = 2; k <= 4; ++k)
             if ((n + k - 1) / k <= kWarp) return k;
         return -1;
     }
     const double u1 = slot_util(n, 1), u2 = slot_util(n, 2), u3 = slot_util(n, 3);
-    if (scan) return u2 >= 1.2 * u1 ? 2 : 1;
+    if (scan) return u2 >= 1.4 * u1 ? 2 : 1;
     if (u1 > 1.1 * u2) return 1;
     return u3 > 1.15 * u2 ? 3 : 2;
 }
