@@ -240,8 +240,9 @@ int validate(const bbe_race* race, const bbe_competitor* comps, const bbe_state*
 
 // Competitors per lane K for the NATIVE kernel (profiles/r1_k_sweep.md: every K timed for n = 6..128,
 // with and without blocking competitors, after the 8/16-tick blocks).  util(K) = occupied slots /
-// (32 K) with S = 32 / ceil(n/K) races per warp.  n > 32: K = 3 when it fits and fills >= 20 % more
-// slots than K = 2, else the smallest K that fits.  With a front-runner scan (some theta > 0): K = 1,
+// (32 K) with S = 32 / ceil(n/K) races per warp.  n > 32: without a scan K = 3 when it fits and fills
+// >= 20 % more slots than K = 2, else (and with a scan: profiles/r1_sweep.md, n = 40) the smallest K
+// that fits.  With a front-runner scan (some theta > 0): K = 1,
 // or K = 2 when that fills >= 40 % more slots (K = 1 runs 16-tick blocks, K = 2 with a scan 4).
 // Without: K = 2 (more independent work per lane), K = 1 when it fills > 10 % more slots, K = 3 when
 // that fills > 15 % more than K = 2.
@@ -255,7 +256,7 @@ int choose_k(int n, bool scan, int hint) {
     if (hint > 0 && hint <= 4 && (n + hint - 1) / hint <= kWarp) return hint;
     if (n > kWarp) {
         const double w2 = slot_util(n, 2), w3 = slot_util(n, 3);
-        if (w2 > 0.0 && w3 > 0.0) return w3 >= 1.2 * w2 ? 3 : 2;
+        if (!scan && w2 > 0.0 && w3 > 0.0) return w3 >= 1.2 * w2 ? 3 : 2;
         for (int k = 2; k <= 4; ++k)
             if ((n + k - 1) / k <= kWarp) return k;
         return -1;

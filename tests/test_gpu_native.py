@@ -264,7 +264,7 @@ def test_layout_rule_and_layout_invariance_from_the_start():
     """choose_k picks the measured-best layout (profiles/r1_k_sweep.md) and every layout gives the
     same per-sim results: the FP32 frame does not depend on it (from-start races included)."""
     for n, scan, want in ((10, True, 1), (12, True, 1), (20, True, 2), (22, True, 1), (10, False, 2),
-                          (5, False, 1), (24, False, 3), (40, True, 3), (48, False, 3), (64, False, 2),
+                          (5, False, 1), (24, False, 3), (40, True, 2), (40, False, 3), (48, False, 3), (64, False, 2),
                           (96, False, 3), (128, True, 4)):
         comps = tuple(Competitor(f"c{i + 1}", UniformSteps(10.0, 20.0), theta=8.0 if (scan and i % 4 == 1) else 0.0)
                       for i in range(n))
