@@ -303,3 +303,37 @@ def test_extreme_step_laws_terminate_or_diverge_cleanly(mode):
     far = RaceConfig(1e6, (Competitor("a", UniformSteps(4e4, 6e4)), Competitor("b", UniformSteps(4.5e4, 5.5e4), theta=5e3)))
     r = sim.simulate_batch(None, far, 2000, 9, mode=mode, ranks=True, **kw(9, 2000))
     assert int(r.wins.sum()) == 2000
+
+
+@pytest.mark.parametrize("mode", ["mt", "native"])
+def test_rp_predict_c_entry_errors(mode):
+    """bbe_rp_predict: a dry run past tick_limit raises with the first failing dry-run index (both MT
+    halves included) and still advances the bettor's stream by d; bad arguments are rejected."""
+    import ctypes
+    import random
+
+    from paper_2108_02419_b200.agents import rp_predict
+
+    cfg = RaceConfig(100.0, (Competitor("a", UniformSteps(1.0, 1.0)), Competitor("b", UniformSteps(1.0, 1.0))),
+                     tick_limit=10)
+    st = RaceState(50, [10.0, 20.0], [1.0, 1.0], [None, None])
+    d = 40_000
+    rng, twin = random.Random(3), random.Random(3)
+    with pytest.raises(sim.SimDivergedError) as e:
+        rp_predict(st, cfg, d, rng, mode=mode)
+    assert e.value.sim_index == 0
+    for _ in range(d):
+        twin.getrandbits(64)
+    assert rng.getstate() == twin.getstate()
+    pk = sim.pack_config(cfg)
+    stc, keep = sim.pack_state(st, pk.n)
+    mt = np.zeros(624, np.uint32)
+    pos = np.array([625], np.int32)  # outside 0..624
+    wins = np.zeros(2, np.uint64)
+    rc = sim.lib().bbe_rp_predict(ctypes.byref(pk.race), pk.comps, ctypes.byref(stc), 10, sim.MODES[mode],
+                                  mt.ctypes.data, pos.ctypes.data, wins.ctypes.data, None)
+    assert rc == 1
+    pos[0] = 0
+    rc = sim.lib().bbe_rp_predict(ctypes.byref(pk.race), pk.comps, ctypes.byref(stc), 10, sim.MODES["inject"],
+                                  mt.ctypes.data, pos.ctypes.data, wins.ctypes.data, None)
+    assert rc == 1
