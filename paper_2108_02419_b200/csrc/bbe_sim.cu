@@ -123,6 +123,17 @@ struct DevCtx {
     DevBuf d_work;                               // work counters, a ring of kWorkSlots pairs
     std::map<std::pair<const void*, size_t>, int> occupancy;  // blocks per SM by (kernel, smem)
     int work_slot = 0;
+    // bbe_rp_predict NATIVE: parameter H2D + kernel + tally D2H as one CUDA graph (one launch call
+    // instead of three), re-instantiated when the kernel, grid or buffers change
+    struct RpGraph {
+        cudaGraph_t graph = nullptr;  // kept: its kernel node addresses the exec's node
+        cudaGraphExec_t exec = nullptr;
+        cudaGraphNode_t knode = nullptr;
+        const void* fn = nullptr;
+        int grid = 0;
+        size_t smem = 0, bytes = 0, tbytes = 0;
+        const void *hp = nullptr, *dp = nullptr, *ht = nullptr;
+    } rp_graph;
     bool mt_table = false;                       // c_mt_init uploaded on this device
     // the call in flight between bbe_simulate_begin and bbe_simulate_end
     bool pending = false;
@@ -698,6 +709,21 @@ static LaunchArgs sub_launch(const LaunchArgs& a, int64_t c0, int64_t cn) {
     return b;
 }
 
+// The launch's work-counter pair (the kernel leaves it zeroed; consecutive launches rotate through
+// the ring) and its persistent grid (never more blocks than the launch's sims need).
+static int prepare_launch(DevCtx* ctx, const Plan& pl, cudaStream_t stream, LaunchArgs* a, int* grid) {
+    if (!ctx->d_work.p) {
+        BBE_CK(ctx->d_work.ensure(kWorkSlots * 2 * sizeof(unsigned long long)));
+        BBE_CK(cudaMemsetAsync(ctx->d_work.p, 0, kWorkSlots * 2 * sizeof(unsigned long long), stream));
+        BBE_CK(cudaStreamSynchronize(stream));
+    }
+    a->work = (unsigned long long*)ctx->d_work.p + 2 * ctx->work_slot;
+    ctx->work_slot = (ctx->work_slot + 1) % kWorkSlots;
+    const int64_t sims_per_block = (int64_t)kWarpsPerBlock * pl.S;
+    *grid = (int)std::max<int64_t>(1, std::min<int64_t>(pl.grid, (a->n_sims + sims_per_block - 1) / sims_per_block));
+    return BBE_OK;
+}
+
 static int launch_one(DevCtx* ctx, const Plan& pl, const LaunchArgs& a0, cudaStream_t stream) {
     if (a0.n_sims == 0) return BBE_OK;
     if (a0.n_sims > kMaxLaunchSims) {
@@ -708,19 +734,9 @@ static int launch_one(DevCtx* ctx, const Plan& pl, const LaunchArgs& a0, cudaStr
         return BBE_OK;
     }
     LaunchArgs a = a0;
-    {
-        // the kernel leaves its counter pair zeroed; consecutive launches rotate through the ring
-        if (!ctx->d_work.p) {
-            BBE_CK(ctx->d_work.ensure(kWorkSlots * 2 * sizeof(unsigned long long)));
-            BBE_CK(cudaMemsetAsync(ctx->d_work.p, 0, kWorkSlots * 2 * sizeof(unsigned long long), stream));
-            BBE_CK(cudaStreamSynchronize(stream));
-        }
-        a.work = (unsigned long long*)ctx->d_work.p + 2 * ctx->work_slot;
-        ctx->work_slot = (ctx->work_slot + 1) % kWorkSlots;
-    }
-    // persistent grid: never more blocks than this launch's sims need
-    const int64_t sims_per_block = (int64_t)kWarpsPerBlock * pl.S;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(pl.grid, (a.n_sims + sims_per_block - 1) / sims_per_block));
+    int grid = 0;
+    int rc = prepare_launch(ctx, pl, stream, &a, &grid);
+    if (rc) return rc;
     pl.fn<<<grid, kBlockThreads, pl.smem, stream>>>(a);
     BBE_CK(cudaGetLastError());
     return BBE_OK;
@@ -1068,6 +1084,61 @@ int bbe_simulate_end(bbe_result* out) {
 
 }  // extern "C"
 
+// bbe_rp_predict NATIVE: the staged parameters' H2D, the kernel and the tally D2H as one graph
+// launch.  The graph is captured once per (kernel, grid, buffers) and its kernel node's arguments
+// are replaced every call (seed, work slot, frame); the copies read and write the same staging.
+static int launch_graph(DevCtx* ctx, const Plan& pl, LaunchArgs a, size_t bytes, size_t tbytes, uint64_t* d_tally) {
+    cudaStream_t s = ctx->stream;
+    int grid = 0;
+    int rc = prepare_launch(ctx, pl, s, &a, &grid);
+    if (rc) return rc;
+    DevCtx::RpGraph& g = ctx->rp_graph;
+    const bool same = g.exec && g.fn == (const void*)pl.fn && g.grid == grid && g.smem == pl.smem && g.bytes == bytes &&
+                      g.tbytes == tbytes && g.hp == ctx->h_params.p && g.dp == ctx->d_params.p && g.ht == ctx->h_tally.p;
+    if (!same) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        if (g.graph) cudaGraphDestroy(g.graph);
+        g = DevCtx::RpGraph{};
+        cudaGraph_t graph = nullptr;
+        BBE_CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        cudaMemcpyAsync(ctx->d_params.p, ctx->h_params.p, bytes, cudaMemcpyHostToDevice, s);
+        pl.fn<<<grid, kBlockThreads, pl.smem, s>>>(a);
+        cudaMemcpyAsync(ctx->h_tally.p, d_tally, tbytes, cudaMemcpyDeviceToHost, s);
+        BBE_CK(cudaStreamEndCapture(s, &graph));
+        size_t nn = 0;
+        BBE_CK(cudaGraphGetNodes(graph, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        BBE_CK(cudaGraphGetNodes(graph, nodes.data(), &nn));
+        for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType t;
+            BBE_CK(cudaGraphNodeGetType(nd, &t));
+            if (t == cudaGraphNodeTypeKernel) g.knode = nd;
+        }
+        g.graph = graph;
+        BBE_CK(cudaGraphInstantiate(&g.exec, graph, 0));
+        if (!g.knode) return fail(BBE_ECUDA, "captured graph has no kernel node");
+        g.fn = (const void*)pl.fn;
+        g.grid = grid;
+        g.smem = pl.smem;
+        g.bytes = bytes;
+        g.tbytes = tbytes;
+        g.hp = ctx->h_params.p;
+        g.dp = ctx->d_params.p;
+        g.ht = ctx->h_tally.p;
+    } else {
+        cudaKernelNodeParams kp{};
+        void* args[] = {&a};
+        kp.func = (void*)pl.fn;
+        kp.gridDim = dim3(grid);
+        kp.blockDim = dim3(kBlockThreads);
+        kp.sharedMemBytes = (unsigned)pl.smem;
+        kp.kernelParams = args;
+        BBE_CK(cudaGraphExecKernelNodeSetParams(g.exec, g.knode, &kp));
+    }
+    BBE_CK(cudaGraphLaunch(g.exec, s));
+    return BBE_OK;
+}
+
 // bbe_rp_predict: one winner-tally launch of rq on ctx's stream -- parameters + zeroed tally H2D,
 // the kernel(s), the tally D2H into ctx->h_tally.  d_seeds (MT) must already be on ctx's stream.
 static int enqueue_tally(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, const bbe_state* st,
@@ -1084,9 +1155,11 @@ static int enqueue_tally(DevCtx* ctx, const bbe_race* race, const bbe_competitor
     pack_params_f32(race, comps, st, (double*)ctx->h_params.p, fr);
     std::memset((char*)ctx->h_params.p + pbytes, 0, tbytes);
     uint64_t* const d_tally = (uint64_t*)((char*)ctx->d_params.p + pbytes);
-    BBE_CK(cudaMemcpyAsync(ctx->d_params.p, ctx->h_params.p, pbytes + tbytes, cudaMemcpyHostToDevice, s));
     LaunchArgs a;
     build_args(pl, race, st, &rq, (const double*)ctx->d_params.p, nullptr, nullptr, d_tally, nullptr, fr, &a);
+    if (pl.mode == BBE_MODE_NATIVE && rq.n_sims > 0 && rq.n_sims <= kMaxLaunchSims)
+        return launch_graph(ctx, pl, a, pbytes + tbytes, tbytes, d_tally);
+    BBE_CK(cudaMemcpyAsync(ctx->d_params.p, ctx->h_params.p, pbytes + tbytes, cudaMemcpyHostToDevice, s));
     int rc = launch_all(ctx, pl, a, comps, d_seeds, 0, s);
     if (rc) return rc;
     BBE_CK(cudaMemcpyAsync(ctx->h_tally.p, d_tally, tbytes, cudaMemcpyDeviceToHost, s));
