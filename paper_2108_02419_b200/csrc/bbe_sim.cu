@@ -118,7 +118,7 @@ struct DevCtx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     HostBuf h_params, h_tally, h_seeds;  // h_seeds: bbe_rp_predict's MT dry-run seeds
     DevBuf d_params, d_draws, d_offsets, d_winner, d_order, d_fin, d_fpos, d_blocked, d_dused;
-    DevBuf d_seeds, d_mt_states, d_mt_scratch;  // MT mode
+    DevBuf d_seeds, d_mt_states;  // MT mode
     DevBuf d_traj;                               // trajectories (positions, previous steps)
     DevBuf d_work;                               // work counters, a ring of kWorkSlots pairs
     std::map<std::pair<const void*, size_t>, int> occupancy;  // blocks per SM by (kernel, smem)
@@ -742,7 +742,7 @@ static int launch_one(DevCtx* ctx, const Plan& pl, const LaunchArgs& a0, cudaStr
     return BBE_OK;
 }
 
-constexpr int64_t kMtChunk = 131072;  // sims seeded per MT chunk: 2 x 320 MB of state + scratch
+constexpr int64_t kMtChunk = 131072;  // sims seeded per MT chunk: 320 MB of seeded states
 
 // init_genrand(19650218) (CPython _randommodule.c), the start of every init_by_array
 static void mt_init_table(uint32_t* t) {
@@ -843,13 +843,12 @@ static int launch_all(DevCtx* ctx, const Plan& pl, LaunchArgs a, const bbe_compe
     const int64_t chunk = std::min<int64_t>(total, kMtChunk);
     const int64_t pad = (chunk + 31) & ~31;
     BBE_CK(ctx->d_mt_states.ensure((size_t)pad * kMtWords * 4));
-    BBE_CK(ctx->d_mt_scratch.ensure((size_t)pad * kMtWords * 4));
     const uint64_t h_run = h_run_of(seed_master);
     const int64_t off0 = a.sim_offset;
     for (int64_t c0 = 0; c0 < total; c0 += chunk) {
         const int64_t cn = std::min(chunk, total - c0);
-        BBE_CK(launch_mt_seed(stream, d_seeds ? d_seeds + c0 : nullptr, h_run, off0 + c0, cn, pad,
-                              (uint32_t*)ctx->d_mt_scratch.p, (uint32_t*)ctx->d_mt_states.p));
+        BBE_CK(launch_mt_seed(stream, d_seeds ? d_seeds + c0 : nullptr, h_run, off0 + c0, cn,
+                              (uint32_t*)ctx->d_mt_states.p));
         LaunchArgs b = sub_launch(a, c0, cn);
         b.mt_states = (const uint32_t*)ctx->d_mt_states.p;  // the chunk's seeded states
         int rc = launch_one(ctx, pl, b, stream);

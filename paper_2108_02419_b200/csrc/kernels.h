@@ -29,7 +29,7 @@ KernelFn pick_exact(int mode, int k, bool ln);
 cudaError_t upload_mt_tables(const uint32_t* init624, int exp_ok, const uint64_t* exp_tab256, const double* exp_c8);
 // random.Random(seed) for n sims (per-sim seeds, or derive_seed(master, "run", offset + i) via h_run)
 cudaError_t launch_mt_seed(cudaStream_t stream, const uint64_t* seeds, uint64_t h_run, int64_t sim_offset, int64_t n,
-                           int64_t n_pad, uint32_t* scratch, uint32_t* states);
+                           uint32_t* states);
 // splitmix64 (seeding.py:24-28), shared with the device code
 uint64_t splitmix64_host(uint64_t x);
 

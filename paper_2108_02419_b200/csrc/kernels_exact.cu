@@ -33,9 +33,8 @@ cudaError_t upload_mt_tables(const uint32_t* init624, int exp_ok, const uint64_t
 }
 
 cudaError_t launch_mt_seed(cudaStream_t stream, const uint64_t* seeds, uint64_t h_run, int64_t sim_offset, int64_t n,
-                           int64_t n_pad, uint32_t* scratch, uint32_t* states) {
-    mt_seed_kernel<<<(unsigned)((n + 127) / 128), 128, 0, stream>>>(seeds, h_run, sim_offset, n, n_pad, scratch,
-                                                                     states);
+                           uint32_t* states) {
+    mt_seed_kernel<<<(unsigned)((n + 127) / 128), 128, 0, stream>>>(seeds, h_run, sim_offset, n, states);
     return cudaGetLastError();
 }
 

@@ -7,9 +7,9 @@
 // Modules/_randommodule.c (init_genrand, init_by_array, genrand_uint32, random_random) and
 // Lib/random.py (uniform, normalvariate, lognormvariate).
 //
-// Layout: (1) mt_seed_kernel, one thread per sim, runs init_by_array's two serial passes
-// (pass-1 words spill to a word-major scratch so every store and load is coalesced) and writes the
-// seeded 624-word state sim-major through a 32x32 shared-memory transpose; (2) the race kernel keeps
+// Layout: (1) mt_seed_kernel, one thread per sim, runs init_by_array's two serial passes (pass 1
+// twice, the second time in lockstep with pass 2, so nothing but the final state is stored) and
+// writes the seeded 624-word state sim-major through a 32x32 shared-memory transpose; (2) the race kernel keeps
 // each segment's state in shared memory and regenerates it in place, W lanes per 624-word twist.
 #pragma once
 
@@ -123,9 +123,17 @@ __device__ __forceinline__ bool km_accept(uint32_t w0, uint32_t w1_raw, uint32_t
 }
 
 // One thread per sim: random.Random(seed) for a u64 seed = init_by_array(key = 32-bit LE words of
-// the seed, one word when seed < 2^32).  states: [n][624] u32; scratch: [624][n_pad] u32.
+// the seed, one word when seed < 2^32), CPython _randommodule.c.  states: [n][624] u32.
+//   pass 1 (624 steps):  mt[i] = (mt[i] ^ ((mt[i-1] ^ (mt[i-1] >> 30)) * 1664525)) + key[j] + j,
+//                        i = 1..623, then mt[0] = mt[623] and i = 1 once more (-> m1);
+//   pass 2 (623 steps):  mt[i] = (mt[i] ^ ((mt[i-1] ^ (mt[i-1] >> 30)) * 1566083941)) - i,
+//                        i = 2..623 reading pass 1's mt[i], then the wrap and i = 1; mt[0] = 2^31.
+// Pass 2 starts from m1, which needs all of pass 1, and then reads pass 1's words in order -- so
+// pass 1 runs twice: once for m1, then again in lockstep with pass 2 (two independent chains per
+// thread).  Nothing is stored but the final state, which leaves through a 32x32 shared-memory
+// transpose so every store is coalesced.
 __global__ void __launch_bounds__(128) mt_seed_kernel(const uint64_t* seeds, uint64_t h_run, int64_t sim_offset,
-                                                      int64_t n, int64_t n_pad, uint32_t* scratch, uint32_t* states) {
+                                                      int64_t n, uint32_t* states) {
     __shared__ uint32_t tile[4][32][33];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -134,38 +142,35 @@ __global__ void __launch_bounds__(128) mt_seed_kernel(const uint64_t* seeds, uin
     const uint64_t seed = on ? (seeds ? seeds[s] : derive_seed_run_dev(h_run, (uint64_t)(sim_offset + s))) : 0ull;
     const uint32_t key0 = (uint32_t)seed, key1 = (uint32_t)(seed >> 32);
     const int keylen = key1 ? 2 : 1;
+    auto step1 = [&](uint32_t init_i, uint32_t prev, int j) {
+        return (init_i ^ ((prev ^ (prev >> 30)) * 1664525u)) + (j ? key1 : key0) + (uint32_t)j;
+    };
 
-    // pass 1 (k = 624 iterations): i = 1..623, then wrap (mt[0] = mt[623]) and i = 1 once more
+    // pass 1, first run: only its last word and the extra step at i = 1 (m1) are kept
     uint32_t prev = c_mt_init[0];
+    uint32_t p1_1 = 0;  // pass 1's word 1 (read again by the extra step)
     int j = 0;
     for (int i = 1; i < kMtN; ++i) {
-        const uint32_t v = (c_mt_init[i] ^ ((prev ^ (prev >> 30)) * 1664525u)) + (j ? key1 : key0) + (uint32_t)j;
-        if (on) scratch[(int64_t)i * n_pad + s] = v;
-        prev = v;
+        prev = step1(c_mt_init[i], prev, j);
+        if (i == 1) p1_1 = prev;
         if (++j >= keylen) j = 0;
     }
-    const uint32_t m0 = prev;
-    const uint32_t p1 = on ? scratch[n_pad + s] : 0u;
-    const uint32_t m1 = (p1 ^ ((m0 ^ (m0 >> 30)) * 1664525u)) + (j ? key1 : key0) + (uint32_t)j;
+    const uint32_t m1 = step1(p1_1, prev, j);  // mt[0] = mt[623]; i = 1
+    // (keylen is 1 or 2 and 623 steps precede it, so the key index here is 623 % keylen)
 
-    // pass 2 (k = 623 iterations): i = 2..623, then wrap and i = 1; mt[0] = 0x80000000 at the end.
-    // Words 2..623 stream out through the transpose tile, 32 at a time.
-    prev = m1;
+    // pass 1 again (q, its word i) in lockstep with pass 2 (prev2), 32 words at a time
+    uint32_t q = p1_1;  // pass 1's word 1
+    int jq = (keylen == 2) ? 1 : 0;  // key index of pass 1's step at i = 2
+    uint32_t prev2 = m1;
     for (int blk0 = 0; blk0 < kMtN; blk0 += 32) {
-        // the 32 pass-1 words of this block are independent loads: issue them all before the chain
-        uint32_t p[32];
-#pragma unroll
-        for (int t = 0; t < 32; ++t) {
-            const int i = blk0 + t;
-            p[t] = (on && i >= 2 && i < kMtN) ? scratch[(int64_t)i * n_pad + s] : 0u;
-        }
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
             const int i = blk0 + t;
             if (i >= 2 && i < kMtN) {
-                const uint32_t v = (p[t] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)i;
-                prev = v;
-                tile[warp][t][lane] = v;
+                q = step1(c_mt_init[i], q, jq);
+                jq = (keylen == 2) ? (jq ^ 1) : 0;
+                prev2 = (q ^ ((prev2 ^ (prev2 >> 30)) * 1566083941u)) - (uint32_t)i;
+                tile[warp][t][lane] = prev2;
             }
         }
         __syncwarp();
@@ -176,7 +181,7 @@ __global__ void __launch_bounds__(128) mt_seed_kernel(const uint64_t* seeds, uin
         }
         __syncwarp();
     }
-    const uint32_t f1 = (m1 ^ ((prev ^ (prev >> 30)) * 1566083941u)) - 1u;
+    const uint32_t f1 = (m1 ^ ((prev2 ^ (prev2 >> 30)) * 1566083941u)) - 1u;
     if (on) {
         states[s * kMtN + 0] = 0x80000000u;
         states[s * kMtN + 1] = f1;
