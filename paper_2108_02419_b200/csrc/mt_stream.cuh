@@ -140,35 +140,27 @@ __global__ void __launch_bounds__(128) mt_seed_kernel(const uint64_t* seeds, uin
     const int64_t warp_base = s - lane;
     const bool on = s < n;
     const uint64_t seed = on ? (seeds ? seeds[s] : derive_seed_run_dev(h_run, (uint64_t)(sim_offset + s))) : 0ull;
+    // key[j] + j of pass 1's step at i: j = (i - 1) % keylen, so odd i add ka and even i add kb
     const uint32_t key0 = (uint32_t)seed, key1 = (uint32_t)(seed >> 32);
-    const int keylen = key1 ? 2 : 1;
-    auto step1 = [&](uint32_t init_i, uint32_t prev, int j) {
-        return (init_i ^ ((prev ^ (prev >> 30)) * 1664525u)) + (j ? key1 : key0) + (uint32_t)j;
-    };
+    const uint32_t ka = key0, kb = key1 ? key1 + 1u : key0;
+    auto step1 = [&](uint32_t init_i, uint32_t prev, uint32_t kj) { return (init_i ^ ((prev ^ (prev >> 30)) * 1664525u)) + kj; };
 
     // pass 1, first run: only its last word and the extra step at i = 1 (m1) are kept
-    uint32_t prev = c_mt_init[0];
-    uint32_t p1_1 = 0;  // pass 1's word 1 (read again by the extra step)
-    int j = 0;
-    for (int i = 1; i < kMtN; ++i) {
-        prev = step1(c_mt_init[i], prev, j);
-        if (i == 1) p1_1 = prev;
-        if (++j >= keylen) j = 0;
-    }
-    const uint32_t m1 = step1(p1_1, prev, j);  // mt[0] = mt[623]; i = 1
-    // (keylen is 1 or 2 and 623 steps precede it, so the key index here is 623 % keylen)
+    const uint32_t p1_1 = step1(c_mt_init[1], c_mt_init[0], ka);  // pass 1's word 1 (read again below)
+    uint32_t prev = p1_1;
+#pragma unroll 2
+    for (int i = 2; i < kMtN; ++i) prev = step1(c_mt_init[i], prev, (i & 1) ? ka : kb);
+    const uint32_t m1 = step1(p1_1, prev, kb);  // mt[0] = mt[623]; i = 1 with j = 623 % keylen
 
     // pass 1 again (q, its word i) in lockstep with pass 2 (prev2), 32 words at a time
-    uint32_t q = p1_1;  // pass 1's word 1
-    int jq = (keylen == 2) ? 1 : 0;  // key index of pass 1's step at i = 2
+    uint32_t q = p1_1;
     uint32_t prev2 = m1;
     for (int blk0 = 0; blk0 < kMtN; blk0 += 32) {
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
             const int i = blk0 + t;
             if (i >= 2 && i < kMtN) {
-                q = step1(c_mt_init[i], q, jq);
-                jq = (keylen == 2) ? (jq ^ 1) : 0;
+                q = step1(c_mt_init[i], q, (i & 1) ? ka : kb);
                 prev2 = (q ^ ((prev2 ^ (prev2 >> 30)) * 1566083941u)) - (uint32_t)i;
                 tile[warp][t][lane] = prev2;
             }
