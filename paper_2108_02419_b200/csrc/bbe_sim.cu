@@ -1156,7 +1156,11 @@ static int enqueue_tally(DevCtx* ctx, const bbe_race* race, const bbe_competitor
     uint64_t* const d_tally = (uint64_t*)((char*)ctx->d_params.p + pbytes);
     LaunchArgs a;
     build_args(pl, race, st, &rq, (const double*)ctx->d_params.p, nullptr, nullptr, d_tally, nullptr, fr, &a);
-    if (pl.mode == BBE_MODE_NATIVE && rq.n_sims > 0 && rq.n_sims <= kMaxLaunchSims)
+    // the graph is kept per context and re-captured when its grid changes, so it is used only for
+    // calls that fill the persistent grid (their grid is the same from call to call)
+    const int64_t sims_per_block = (int64_t)kWarpsPerBlock * pl.S;
+    if (pl.mode == BBE_MODE_NATIVE && rq.n_sims <= kMaxLaunchSims &&
+        (rq.n_sims + sims_per_block - 1) / sims_per_block >= pl.grid)
         return launch_graph(ctx, pl, a, pbytes + tbytes, tbytes, d_tally);
     BBE_CK(cudaMemcpyAsync(ctx->d_params.p, ctx->h_params.p, pbytes + tbytes, cudaMemcpyHostToDevice, s));
     int rc = launch_all(ctx, pl, a, comps, d_seeds, 0, s);
