@@ -1,6 +1,7 @@
 /* c_abi_demo.c -- the C-ABI (include/bbe_sim.h) used from plain C, no Python: a 10-runner race,
  * 20,000 dry runs from a mid-race state in each mode, win probabilities as rp_predict returns them
- * ((wins + 1) / (d + n), agents.py:166).
+ * ((wins + 1) / (d + n), agents.py:166); then rp_predict itself (bbe_rp_predict) for a bettor whose
+ * generator is CPython's random.Random(5), kept here as its MT19937 state.
  *
  *   gcc -O2 -Iinclude examples/c_abi_demo.c -Lpaper_2108_02419_b200/_lib -lbbe_sim \
  *       -Wl,-rpath,$PWD/paper_2108_02419_b200/_lib -o c_abi_demo && ./c_abi_demo
@@ -13,6 +14,23 @@
 #include "bbe_sim.h"
 
 #define N 10
+
+/* random.Random(5): MT19937 init_by_array with the one-word key {5} (CPython _randommodule.c) */
+static void mt_seed_small(uint32_t mt[624], int32_t* pos, uint32_t key) {
+    mt[0] = 19650218u;
+    for (int i = 1; i < 624; ++i) mt[i] = 1812433253u * (mt[i - 1] ^ (mt[i - 1] >> 30)) + (uint32_t)i;
+    int i = 1;
+    for (int k = 624; k; --k) {
+        mt[i] = (mt[i] ^ ((mt[i - 1] ^ (mt[i - 1] >> 30)) * 1664525u)) + key;
+        if (++i >= 624) { mt[0] = mt[623]; i = 1; }
+    }
+    for (int k = 623; k; --k) {
+        mt[i] = (mt[i] ^ ((mt[i - 1] ^ (mt[i - 1] >> 30)) * 1566083941u)) - (uint32_t)i;
+        if (++i >= 624) { mt[0] = mt[623]; i = 1; }
+    }
+    mt[0] = 0x80000000u;
+    *pos = 624;
+}
 
 int main(void) {
     bbe_race race = {2000.0, 1000000, N, 0};
@@ -68,5 +86,21 @@ int main(void) {
         if (total != (uint64_t)d) return 3;
     }
     free(seeds);
+
+    /* rp_predict(state, config, d, random.Random(5)) in one call: the d dry-run seeds are the
+     * bettor's getrandbits(64) draws, and its state is advanced in place exactly as the reference's */
+    uint32_t mt[624];
+    int32_t mpos;
+    mt_seed_small(mt, &mpos, 5u);
+    uint64_t wins[N];
+    int64_t first_div = -1;
+    const int rc = bbe_rp_predict(&race, comps, &st, d, BBE_MODE_MT, mt, &mpos, wins, &first_div);
+    if (rc != BBE_OK) {
+        fprintf(stderr, "bbe_rp_predict failed (%d): %s\n", rc, bbe_last_error());
+        return 4;
+    }
+    printf("rp_mt  pos %d probs", (int)mpos);
+    for (int c = 0; c < N; ++c) printf(" %.17g", (double)(wins[c] + 1) / (double)(d + N));
+    printf("\n");
     return 0;
 }

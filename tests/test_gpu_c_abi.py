@@ -5,6 +5,8 @@ oracle for the same derive_seed(11, "run", i) seeds."""
 import os
 import subprocess
 
+import numpy as np
+
 import pytest
 
 import oracle
@@ -22,7 +24,7 @@ def test_c_program_drives_the_library(tmp_path):
                     f"-Wl,-rpath,{lib_dir}", "-o", exe], check=True)
     out = subprocess.run([exe], check=True, capture_output=True, text=True).stdout.splitlines()
     rows = {line.split()[0]: [float(x) for x in line.split("probs")[1].split()] for line in out}
-    assert set(rows) == {"native", "mt"}
+    assert set(rows) == {"native", "mt", "rp_mt"}
     n, d = 10, 20000
     comps = tuple(Competitor(f"c{c}", UniformSteps(10.0 + c % 3, 20.0 + c % 4), theta=8.0 if c % 2 else 0.0)
                   for c in range(n))
@@ -31,3 +33,12 @@ def test_c_program_drives_the_library(tmp_path):
     ref = oracle.batch(cfg, d, state=st, master=11, threads=8)
     assert rows["mt"] == [(int(w) + 1) / (d + n) for w in ref["wins"]]
     assert abs(sum(rows["native"]) - 1.0) < 1e-9
+    # bbe_rp_predict with random.Random(5) as the bettor: the reference's rp_predict over its seeds
+    import random
+
+    bettor = random.Random(5)
+    seeds = [bettor.getrandbits(64) for _ in range(d)]
+    ref = oracle.batch(cfg, d, state=st, seeds=np.array(seeds, np.uint64), threads=8)
+    assert rows["rp_mt"] == [(int(w) + 1) / (d + n) for w in ref["wins"]]
+    pos = int([line for line in out if line.startswith("rp_mt")][0].split()[2])
+    assert pos == bettor.getstate()[1][624]
