@@ -679,7 +679,10 @@ int bbe_derive_seeds(uint64_t master, int64_t first, int64_t count, uint64_t* ou
     return BBE_OK;
 }
 
-constexpr int64_t kRpSplitMin = 16384;  // bbe_rp_predict MT: d >= 2x this runs as two halves
+constexpr int64_t kRpSplitMin = 16384;  // bbe_rp_predict MT: one part per this many dry runs
+#ifndef BBE_RP_PARTS
+#define BBE_RP_PARTS 2  // at most this many parts (streams) per MT bbe_rp_predict call (C2: 3 or 4 parts were 1.5 % slower)
+#endif
 constexpr int kWorkSlots = 64;  // concurrent native launches per device with their own work counters
 constexpr size_t kMaxStagedBytes = 256ull << 20;  // per-sim outputs staged through pinned memory up to this
 
@@ -1233,20 +1236,29 @@ int bbe_rp_predict(const bbe_race* race, const bbe_competitor* comps, const bbe_
         *pos = (int32_t)bbe_host_mt_getrandbits64(state624, (uint32_t)*pos, d - 1, nullptr, 0);
         return finish_tally(ctx, pl, n, race->tick_limit, wins, first_diverged);
     }
-    // MT: every dry run replays random.Random(getrandbits(64)).  Large calls run as two halves on two
-    // streams: the host draws the second half's seeds while the GPU runs the first, and the second
-    // launch fills the first one's tail.
-    const int64_t h = d >= 2 * kRpSplitMin ? d / 2 : d;
-    Plan p0, p1;
-    if ((rc = enqueue_mt_part(ctx, race, comps, st, 0, h, state624, pos, &p0))) return rc;
-    if (h == d) return finish_tally(ctx, p0, n, race->tick_limit, wins, first_diverged);
-    Lease lease2;
-    if ((rc = acquire_ctx(lease2))) return rc;
-    rc = enqueue_mt_part(lease2.c, race, comps, st, h, d - h, state624, pos, &p1);
-    const int rc0 = finish_tally(ctx, p0, n, race->tick_limit, wins, first_diverged);
-    if (rc) return rc;
-    const int rc1 = finish_tally(lease2.c, p1, n, race->tick_limit, wins, first_diverged);
-    return rc0 ? rc0 : rc1;
+    // MT: every dry run replays random.Random(getrandbits(64)).  Large calls run as P parts on P
+    // streams (P = d / kRpSplitMin, at most BBE_RP_PARTS): the host draws part p+1's seeds while the
+    // GPU runs part p, and each launch fills the previous one's tail.
+    const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(BBE_RP_PARTS, d / kRpSplitMin));
+    Lease extra[BBE_RP_PARTS];
+    DevCtx* cx[BBE_RP_PARTS];
+    Plan pp[BBE_RP_PARTS];
+    int rcs[BBE_RP_PARTS];
+    cx[0] = ctx;
+    int enq = 0;  // parts enqueued
+    for (int p = 0; p < parts; ++p) {
+        if (p > 0 && (rc = acquire_ctx(extra[p]))) break;
+        if (p > 0) cx[p] = extra[p].c;
+        const int64_t a0 = d * p / parts, a1 = d * (p + 1) / parts;
+        if ((rc = enqueue_mt_part(cx[p], race, comps, st, a0, a1 - a0, state624, pos, &pp[p]))) break;
+        enq = p + 1;
+    }
+    int first_rc = BBE_OK;
+    for (int p = 0; p < enq; ++p) {
+        rcs[p] = finish_tally(cx[p], pp[p], n, race->tick_limit, wins, first_diverged);
+        if (rcs[p] && !first_rc) first_rc = rcs[p];
+    }
+    return rc ? rc : first_rc;
 }
 
 int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, const bbe_request* rq,
