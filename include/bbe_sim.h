@@ -17,6 +17,8 @@
  *   bbe_rp_predict        agents.py:153-166 rp_predict(state, config, d, rng) in one call: the d
  *                         getrandbits(64) dry-run seeds drawn from the bettor's own MT19937 state
  *                         (advanced in place), the d continuations, the winner counts.
+ *   bbe_prepare / bbe_launch_prepared   bbe_simulate_async for one race state launched many times
+ *                         (parameters uploaded once).
  *   bbe_derive_seeds      seeding.py:50-59 derive_seed(master, "run", i) for a range of i.
  *   bbe_last_error        -- (error text for the Python exceptions of race.py:27-32, batch.py:30-38)
  *
@@ -37,7 +39,7 @@
 extern "C" {
 #endif
 
-#define BBE_ABI_VERSION 3 /* 3: bbe_rp_predict */
+#define BBE_ABI_VERSION 4 /* 3: bbe_rp_predict; 4: prepared races */
 #define BBE_MAX_COMPETITORS 128
 #define BBE_MAX_PERM_COMPETITORS 6 /* batch.py:27 MAX_FULL_OUTCOME_COMPETITORS */
 
@@ -180,6 +182,20 @@ int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const 
  * its index in 0..d-1; the stream is advanced by d all the same). */
 int bbe_rp_predict(const bbe_race* race, const bbe_competitor* comps, const bbe_state* state, int64_t d,
                    int32_t mode, uint32_t* state624, int32_t* pos, uint64_t* wins, int64_t* first_diverged);
+
+/* Prepared race (NATIVE): the parameter block is packed and uploaded once, on the current device,
+ * so repeated device-resident launches of one race state (the bench's steps, a shard's calls) copy
+ * nothing per launch.  bbe_launch_prepared adds the tallies of sims [sim_offset, sim_offset +
+ * n_sims) into d_tally (device, bbe_tally_len(n) u64) on `stream`, asynchronously; a prepared race
+ * serves one launch at a time (callers serialise).  bbe_prepared_kernel_ms: device time of the last
+ * launch (waits for it), -1 if none. */
+typedef struct bbe_prepared bbe_prepared;
+int bbe_prepare(const bbe_race* race, const bbe_competitor* comps, const bbe_state* state,
+                int32_t lanes_per_slot_hint, bbe_prepared** out);
+int bbe_launch_prepared(bbe_prepared* prepared, int64_t n_sims, int64_t sim_offset, uint64_t seed,
+                        uint64_t* d_tally, void* stream);
+float bbe_prepared_kernel_ms(bbe_prepared* prepared);
+void bbe_release_prepared(bbe_prepared* prepared);
 
 /* d_tally layout: [wins n][ranks n*n][perms n! or 0][ct][blocked][diverged count][bad-draw count]
  *                 [(2^63-1) - first_diverged, or 0 = none][(2^63-1) - first_bad_draws, or 0 = none]

@@ -1415,6 +1415,120 @@ int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const 
     return BBE_OK;
 }
 
+// ---- prepared races (device-resident parameters) ----
+}  // extern "C"
+
+struct bbe_prepared {
+    int dev = -1;
+    Plan pl{};
+    bbe_race race{};
+    int64_t tick = 0;
+    int32_t from_start = 0;
+    NativeFrame fr{};
+    double* d_params = nullptr;
+    unsigned long long* d_work = nullptr;
+    int work_slot = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool timed = false;
+};
+
+static void free_prepared(bbe_prepared* p) {
+    if (!p) return;
+    if (p->d_params) cudaFree(p->d_params);
+    if (p->d_work) cudaFree(p->d_work);
+    if (p->ev0) cudaEventDestroy(p->ev0);
+    if (p->ev1) cudaEventDestroy(p->ev1);
+    delete p;
+}
+
+extern "C" {
+
+int bbe_prepare(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, int32_t lanes_per_slot_hint,
+                bbe_prepared** out) {
+    NvtxRange nvtx_range("bbe_prepare");
+    if (!out) return fail(BBE_EINVAL, "out is NULL");
+    *out = nullptr;
+    bbe_request rq{};
+    rq.n_sims = INT64_MAX / 2;  // plan for a full persistent grid; each launch trims it
+    rq.mode = BBE_MODE_NATIVE;
+    rq.lanes_per_slot_hint = lanes_per_slot_hint;
+    int rc = validate(race, comps, st, &rq);
+    if (rc) return rc;
+    Lease lease;
+    if ((rc = acquire_ctx(lease))) return rc;
+    bbe_prepared* p = new bbe_prepared();
+    p->dev = lease.c->dev;
+    if ((rc = make_plan(lease.c, race, comps, st, &rq, 0, &p->pl))) {
+        free_prepared(p);
+        return rc;
+    }
+    p->race = *race;
+    p->tick = st->from_start ? 0 : st->tick;
+    p->from_start = st->from_start;
+    p->fr = native_frame(race, st, p->pl.W);
+    const size_t pbytes = param_bytes(race->n);
+    std::vector<double> h(pbytes / sizeof(double) + 1);
+    pack_params(race, comps, st, h.data());
+    pack_params_f32(race, comps, st, h.data(), p->fr);
+    cudaError_t e = cudaMalloc(&p->d_params, pbytes);
+    if (e == cudaSuccess) e = cudaMemcpy(p->d_params, h.data(), pbytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_work, kWorkSlots * 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(p->d_work, 0, kWorkSlots * 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaEventCreate(&p->ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&p->ev1);
+    if (e != cudaSuccess) {
+        free_prepared(p);
+        return fail(BBE_ECUDA, std::string("bbe_prepare: ") + cudaGetErrorString(e));
+    }
+    *out = p;
+    return BBE_OK;
+}
+
+int bbe_launch_prepared(bbe_prepared* p, int64_t n_sims, int64_t sim_offset, uint64_t seed, uint64_t* d_tally,
+                        void* stream) {
+    if (!p || !d_tally || n_sims < 0 || sim_offset < 0) return fail(BBE_EINVAL, "bad arguments");
+    int dev = -1;
+    BBE_CK(cudaGetDevice(&dev));
+    if (dev != p->dev) return fail(BBE_EINVAL, "prepared on device " + std::to_string(p->dev) + ", current device " +
+                                                std::to_string(dev));
+    cudaStream_t s = (cudaStream_t)stream;
+    bbe_request rq{};
+    rq.n_sims = n_sims;
+    rq.sim_offset = sim_offset;
+    rq.seed = seed;
+    rq.mode = BBE_MODE_NATIVE;
+    bbe_state st{};
+    st.tick = p->tick;
+    st.from_start = p->from_start;
+    LaunchArgs a0;
+    build_args(p->pl, &p->race, &st, &rq, p->d_params, nullptr, nullptr, d_tally, nullptr, p->fr, &a0);
+    BBE_CK(cudaEventRecord(p->ev0, s));
+    for (int64_t c0 = 0; c0 < n_sims; c0 += kMaxLaunchSims) {
+        LaunchArgs a = sub_launch(a0, c0, std::min(kMaxLaunchSims, n_sims - c0));
+        a.work = p->d_work + 2 * p->work_slot;
+        p->work_slot = (p->work_slot + 1) % kWorkSlots;
+        const int64_t spb = (int64_t)kWarpsPerBlock * p->pl.S;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(p->pl.grid, (a.n_sims + spb - 1) / spb));
+        p->pl.fn<<<grid, kBlockThreads, p->pl.smem, s>>>(a);
+        BBE_CK(cudaGetLastError());
+    }
+    BBE_CK(cudaEventRecord(p->ev1, s));
+    p->timed = n_sims > 0;
+    return BBE_OK;
+}
+
+float bbe_prepared_kernel_ms(bbe_prepared* p) {
+    if (!p || !p->timed || cudaEventSynchronize(p->ev1) != cudaSuccess) return -1.f;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p->ev0, p->ev1) != cudaSuccess) {
+        cudaGetLastError();
+        return -1.f;
+    }
+    return ms;
+}
+
+void bbe_release_prepared(bbe_prepared* p) { free_prepared(p); }
+
 int bbe_mt_exp_exact(void) { return libm_exp_table().ok ? 1 : 0; }
 
 }  // extern "C"

@@ -37,7 +37,7 @@ MAX_COMPETITORS = 128
 MAX_PERM_COMPETITORS = 6
 M64 = (1 << 64) - 1
 
-ABI_VERSION = 3  # include/bbe_sim.h BBE_ABI_VERSION
+ABI_VERSION = 4  # include/bbe_sim.h BBE_ABI_VERSION
 
 EXPORTED_SYMBOLS = (
     "bbe_simulate",
@@ -59,6 +59,10 @@ EXPORTED_SYMBOLS = (
     "bbe_mt_advance64",
     "bbe_mt_advance64_many",
     "bbe_rp_predict",
+    "bbe_prepare",
+    "bbe_launch_prepared",
+    "bbe_prepared_kernel_ms",
+    "bbe_release_prepared",
 )
 
 
@@ -165,6 +169,16 @@ def lib():
         L.bbe_rp_predict.argtypes = [_P(BbeRace), _P(BbeCompetitor), _P(BbeState), ctypes.c_int64, ctypes.c_int32,
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         L.bbe_rp_predict.restype = ctypes.c_int
+        L.bbe_prepare.argtypes = [_P(BbeRace), _P(BbeCompetitor), _P(BbeState), ctypes.c_int32,
+                                  _P(ctypes.c_void_p)]
+        L.bbe_prepare.restype = ctypes.c_int
+        L.bbe_launch_prepared.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64,
+                                          ctypes.c_void_p, ctypes.c_void_p]
+        L.bbe_launch_prepared.restype = ctypes.c_int
+        L.bbe_prepared_kernel_ms.argtypes = [ctypes.c_void_p]
+        L.bbe_prepared_kernel_ms.restype = ctypes.c_float
+        L.bbe_release_prepared.argtypes = [ctypes.c_void_p]
+        L.bbe_release_prepared.restype = None
         L.bbe_param_bytes.argtypes = [ctypes.c_int32]
         L.bbe_param_bytes.restype = ctypes.c_int64
         L.bbe_last_error.restype = ctypes.c_char_p
@@ -520,10 +534,12 @@ def run_race(config, seed: int, record: bool = True, *, mode: str = "mt", with_p
 
 
 class DeviceLauncher:
-    """Pre-packed race for repeated device-resident launches (``bbe_simulate_async``).
+    """Pre-packed race for repeated device-resident launches.
 
     Tallies are added into a caller-owned device buffer (e.g. a torch int64 CUDA tensor, passed by
-    ``data_ptr()``) on a caller stream (``torch.cuda.current_stream().cuda_stream``).
+    ``data_ptr()``) on a caller stream (``torch.cuda.current_stream().cuda_stream``).  NATIVE launches
+    use a prepared race (``bbe_prepare``: parameters uploaded once, nothing copied per launch); MT
+    launches go through ``bbe_simulate_async``.
     """
 
     def __init__(self, state, config, *, lanes_per_slot: int = 0):
@@ -534,9 +550,33 @@ class DeviceLauncher:
         off = lambda f: int(lib().bbe_tally_offset(self.pk.n, f))  # noqa: E731
         self.off = {name: off(i) for i, name in enumerate(
             ["wins", "ranks", "perms", "ct", "blocked", "n_div", "n_bad", "first_div", "first_bad"])}
+        self._prep = None
+        self._last_prepared = False
+
+    def _prepared(self):
+        if self._prep is None:
+            h = ctypes.c_void_p()
+            rc = lib().bbe_prepare(ctypes.byref(self.pk.race), self.pk.comps, ctypes.byref(self.st),
+                                   self.lanes_per_slot, ctypes.byref(h))
+            if rc != BBE_OK:
+                _raise(rc, BbeResult())
+            self._prep = h
+        return self._prep
+
+    def __del__(self):
+        if getattr(self, "_prep", None) is not None and _lib is not None:
+            _lib.bbe_release_prepared(self._prep)
+            self._prep = None
 
     def launch(self, d_tally_ptr: int, n_sims: int, seed: int, *, sim_offset: int = 0, stream: int = 0,
                mode: str = "native") -> None:
+        if mode == "native":
+            rc = lib().bbe_launch_prepared(self._prepared(), int(n_sims), int(sim_offset), int(seed) & M64,
+                                           d_tally_ptr, stream)
+            if rc != BBE_OK:
+                _raise(rc, BbeResult())
+            self._last_prepared = True
+            return
         # mode "mt": sim i replays random.Random(derive_seed(seed, "run", sim_offset + i)), derived on the GPU
         req = BbeRequest(int(n_sims), int(sim_offset), int(seed) & M64, MODES[mode], self.lanes_per_slot, None,
                          None, None, int(seed) & M64)
@@ -545,7 +585,11 @@ class DeviceLauncher:
                                       ctypes.c_void_p(stream))
         if rc != BBE_OK:
             _raise(rc, BbeResult())
+        self._last_prepared = False
 
-    @staticmethod
-    def last_kernel_ms() -> float:
+    def last_kernel_ms(self) -> float:
+        """Device time of this launcher's last launch (waits for it)."""
+        if self._last_prepared:
+            return float(lib().bbe_prepared_kernel_ms(self._prep))
         return float(lib().bbe_last_kernel_ms())
+

@@ -19,7 +19,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "bbe_sim.h")).read()
-    return sorted(set(re.findall(r"^(?:int|int64_t|float|const char\*)\s+(bbe_\w+)\(", src, re.M)))
+    return sorted(set(re.findall(r"^(?:int|int64_t|float|void|const char\*)\s+(bbe_\w+)\(", src, re.M)))
 
 
 def test_library_exports_every_header_symbol():
@@ -28,7 +28,7 @@ def test_library_exports_every_header_symbol():
     assert declared and set(declared) == set(sim.EXPORTED_SYMBOLS)
     for name in declared:
         assert hasattr(L, name), name
-    assert L.bbe_version() == sim.ABI_VERSION == 3
+    assert L.bbe_version() == sim.ABI_VERSION == 4
 
 
 def test_tally_layout():
