@@ -277,3 +277,28 @@ def test_layout_rule_and_layout_invariance_from_the_start():
             o = sim.simulate_batch(None, cfg, 3000, 11, records=True, lanes_per_slot=k)
             assert (o.order == r.order).all() and (o.finish_ticks == r.finish_ticks).all()
             assert (o.final_positions == r.final_positions).all() and (o.blocked == r.blocked).all()
+
+
+def test_prepared_race_equals_per_call_upload():
+    """bbe_prepare / bbe_launch_prepared (parameters uploaded once) add the same tallies as
+    bbe_simulate_async (parameters uploaded per call), for a whole range and for two shards."""
+    import ctypes
+
+    import torch
+
+    g = c2()
+    cfg, st = config_from_dict(g["config"]), state_from_dict(g["state"])
+    dl = sim.DeviceLauncher(st, cfg)
+    s = torch.cuda.current_stream().cuda_stream
+    a = torch.zeros(dl.tally_len, dtype=torch.int64, device="cuda")
+    b = torch.zeros_like(a)
+    dl.launch(a.data_ptr(), 50_000, 99, stream=s)  # prepared
+    req = sim.BbeRequest(30_000, 0, 99, sim.MODES["native"], 0, None, None, None, 0, 0)
+    for off, ns in ((0, 30_000), (30_000, 20_000)):
+        req.n_sims, req.sim_offset = ns, off
+        rc = sim.lib().bbe_simulate_async(ctypes.byref(dl.pk.race), dl.pk.comps, ctypes.byref(dl.st),
+                                          ctypes.byref(req), None, ctypes.c_void_p(b.data_ptr()), ctypes.c_void_p(s))
+        assert rc == 0, sim.last_error()
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    assert dl.last_kernel_ms() > 0.0
