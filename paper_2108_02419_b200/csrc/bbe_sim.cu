@@ -1458,7 +1458,8 @@ int bbe_prepare(const bbe_race* race, const bbe_competitor* comps, const bbe_sta
     if ((rc = acquire_ctx(lease))) return rc;
     bbe_prepared* p = new bbe_prepared();
     p->dev = lease.c->dev;
-    if ((rc = make_plan(lease.c, race, comps, st, &rq, 0, &p->pl))) {
+    // the device tally has bbe_tally_len(n) entries: full-order bins for n <= 6 (as bbe_simulate_async)
+    if ((rc = make_plan(lease.c, race, comps, st, &rq, nperm_for(race->n) > 0, &p->pl))) {
         free_prepared(p);
         return rc;
     }

@@ -279,15 +279,21 @@ def test_layout_rule_and_layout_invariance_from_the_start():
             assert (o.final_positions == r.final_positions).all() and (o.blocked == r.blocked).all()
 
 
-def test_prepared_race_equals_per_call_upload():
+@pytest.mark.parametrize("field", ["c2", "derby5_from_start"])
+def test_prepared_race_equals_per_call_upload(field):
     """bbe_prepare / bbe_launch_prepared (parameters uploaded once) add the same tallies as
-    bbe_simulate_async (parameters uploaded per call), for a whole range and for two shards."""
+    bbe_simulate_async (parameters uploaded per call), for a whole range and for two shards -- every
+    tally field, including the full-order bins of n <= 6 fields."""
     import ctypes
 
     import torch
 
+    from paper_2108_02419_b200.batch import resize_race
+
     g = c2()
     cfg, st = config_from_dict(g["config"]), state_from_dict(g["state"])
+    if field != "c2":
+        cfg, st = resize_race(cfg, 5), None
     dl = sim.DeviceLauncher(st, cfg)
     s = torch.cuda.current_stream().cuda_stream
     a = torch.zeros(dl.tally_len, dtype=torch.int64, device="cuda")
@@ -300,5 +306,5 @@ def test_prepared_race_equals_per_call_upload():
                                           ctypes.byref(req), None, ctypes.c_void_p(b.data_ptr()), ctypes.c_void_p(s))
         assert rc == 0, sim.last_error()
     torch.cuda.synchronize()
-    assert torch.equal(a, b)
+    assert torch.equal(a, b) and int(a[dl.off["ct"]]) > 0
     assert dl.last_kernel_ms() > 0.0
