@@ -680,6 +680,9 @@ int bbe_derive_seeds(uint64_t master, int64_t first, int64_t count, uint64_t* ou
 }
 
 constexpr int64_t kRpSplitMin = 16384;  // bbe_rp_predict MT: one part per this many dry runs
+#ifndef BBE_RP_FIRST
+#define BBE_RP_FIRST 15  // percent of an MT bbe_rp_predict call in its first part (C2: 50 -> 2.53 ms, 25 -> 2.50, 15 -> 2.49)
+#endif
 #ifndef BBE_RP_PARTS
 #define BBE_RP_PARTS 2  // at most this many parts (streams) per MT bbe_rp_predict call (C2: 3 or 4 parts were 1.5 % slower)
 #endif
@@ -1249,7 +1252,15 @@ int bbe_rp_predict(const bbe_race* race, const bbe_competitor* comps, const bbe_
     for (int p = 0; p < parts; ++p) {
         if (p > 0 && (rc = acquire_ctx(extra[p]))) break;
         if (p > 0) cx[p] = extra[p].c;
-        const int64_t a0 = d * p / parts, a1 = d * (p + 1) / parts;
+        // part boundaries: the first part is BBE_RP_FIRST % of d (its seeds are the only ones drawn
+        // before the GPU starts), the rest is split evenly
+        auto cut = [&](int q) -> int64_t {
+            if (q == 0) return 0;
+            if (q == parts) return d;
+            const int64_t first = d * BBE_RP_FIRST / 100;
+            return parts == 1 ? d : first + (d - first) * (q - 1) / (parts - 1);
+        };
+        const int64_t a0 = cut(p), a1 = cut(p + 1);
         if ((rc = enqueue_mt_part(cx[p], race, comps, st, a0, a1 - a0, state624, pos, &pp[p]))) break;
         enq = p + 1;
     }
