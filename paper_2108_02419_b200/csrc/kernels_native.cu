@@ -72,7 +72,7 @@ KernelFn BBE_CAT(pick_native_kn_nt, BBE_NATIVE_NT)(int k, int ch, bool scan) {
 #else
     // K = 2 with a scan stays at 4: 8 and 16 measured slower there (derby20: 12.3 -> 13.1 / 19.4 ms,
     // and 12.8 ms with the 16 ticks run as a loop of 4-tick groups)
-    return (k == 2 && !scan) ? native_for<2>(ch, false) : nullptr;
+    return (k == 2 && !scan) ? native_for_ch<2, false>(ch) : nullptr;
 #endif
 }
 #endif
