@@ -56,11 +56,6 @@ exact_kernel(const LaunchArgs a) {
     extern __shared__ __align__(16) unsigned long long s_dyn[];
     const TallyLayout TL{a.n, a.perms};
     const int hist_len = TL.hist_len();
-    // 32-bit shared histograms (native ATOMS.ADD; a 64-bit shared add is a CAS loop).  A block's count
-    // in one bin is at most the sims of its launch, which the host keeps below 2^32 (launch_one).
-    uint32_t* s_hist = reinterpret_cast<uint32_t*>(s_dyn);
-    for (int i = threadIdx.x; i < hist_len; i += blockDim.x) s_hist[i] = 0u;
-
     const int n = a.n, W = a.W, S = a.S;
     const int lane = threadIdx.x & (kWarp - 1);
     const int warp = threadIdx.x >> 5;
@@ -73,17 +68,23 @@ exact_kernel(const LaunchArgs a) {
     // MT: this segment's words: [side buffer: kSide][current block: 624]; the unread stream is the
     // contiguous window seg_mt[wp, kSeg)
     constexpr int kSide = mt_side_words(K);
-    uint32_t* const seg_mt = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) +
-                             (warp * S + (lane_on ? seg : 0)) * kSeg;
+    // dynamic shared memory: [MT segment words][position rows][lognormal offsets (MT)][histograms] --
+    // the histograms last, so the per-word pointers do not depend on the field size
+    uint32_t* const smem_w = reinterpret_cast<uint32_t*>(s_dyn);
+    uint32_t* const seg_mt = smem_w + (warp * S + (lane_on ? seg : 0)) * kSeg;
     uint32_t* const mt = seg_mt + kSide;  // the 624-word MT19937 block
     // start-of-tick positions, per warp: [parity][slot][segment * WP2 + lane-in-segment], pads -inf
     const int WP2 = (W + 1) & ~1;
-    double* const xrows_all = reinterpret_cast<double*>(
-        reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) + (MODE == MT ? kWarpsPerBlock * S * kSeg : 0));
+    double* const xrows_all = reinterpret_cast<double*>(smem_w + (MODE == MT ? kWarpsPerBlock * S * kSeg : 0));
     double* const xrows = xrows_all + warp * 2 * K * kXSlot;
     // MT, K = 1: the round's pending lognormal draws publish their speculative word offsets here, by
     // rank in their segment (lane base + rank), for the lanes that evaluate their trials
-    int* const ln_off = reinterpret_cast<int*>(xrows_all + kWarpsPerBlock * 2 * K * kXSlot) + warp * kWarp;
+    int* const ln_off_all = reinterpret_cast<int*>(xrows_all + kWarpsPerBlock * 2 * K * kXSlot);
+    int* const ln_off = ln_off_all + warp * kWarp;
+    // 32-bit shared histograms (native ATOMS.ADD; a 64-bit shared add is a CAS loop).  A block's count
+    // in one bin is at most the sims of its launch, which the host keeps below 2^32 (launch_one).
+    uint32_t* const s_hist = reinterpret_cast<uint32_t*>(ln_off_all + (MODE == MT ? kWarpsPerBlock * kWarp : 0));
+    for (int i = threadIdx.x; i < hist_len; i += blockDim.x) s_hist[i] = 0u;
     for (int i = lane; i < 2 * K * kXSlot; i += kWarp) xrows[i] = -CUDART_INF;
     const int xseg = lane_on ? seg * WP2 : 0;
     double* const xw = xrows + (lane_on ? seg * WP2 + l : kXSlot - 1);
@@ -141,8 +142,7 @@ exact_kernel(const LaunchArgs a) {
     // Regenerate a segment's block in place (MT19937 twist): all 32 lanes of the warp twist one
     // needing segment at a time, 20 chunks of 32 words (32 < 227 keeps every "new" dependency in an
     // earlier chunk), so a segment's twist costs the same whether or not its warp-mates need one.
-    uint32_t* const warp_mt = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) +
-                              warp * S * kSeg;
+    uint32_t* const warp_mt = smem_w + warp * S * kSeg;
     auto mt_twist = [&](bool need) {
         unsigned todo = __ballot_sync(0xffffffffu, need && l == 0);  // one bit per needing segment
         __syncwarp();
