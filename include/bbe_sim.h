@@ -24,7 +24,9 @@
  *
  * All types are plain C; no torch or CUDA types appear.  Host pointers are caller-owned and only
  * touched during the call.  Calls are thread-safe: concurrent calls on one device each lease their
- * own context (stream + staging buffers) from a per-device pool.
+ * own context (stream + staging buffers) from a per-device pool.  The caller must not let another
+ * thread use the same generator state (bbe_rp_predict, bbe_mt_advance64*) during a call; from
+ * Python, bind those through ctypes.PyDLL (the GIL then excludes every other thread).
  *
  * Return codes: BBE_OK, BBE_EINVAL (-> RaceConfigError), BBE_EDIVERGED (-> RaceDivergedError /
  * BatchRunError(first_diverged)), BBE_EDRAWS (inject stream under/over-consumed), BBE_ECUDA,
@@ -39,7 +41,7 @@
 extern "C" {
 #endif
 
-#define BBE_ABI_VERSION 4 /* 3: bbe_rp_predict; 4: prepared races */
+#define BBE_ABI_VERSION 5 /* 3: bbe_rp_predict; 4: prepared races; 5: BBE_MODE_NATIVE64, bbe_prepare(mode) */
 #define BBE_MAX_COMPETITORS 128
 #define BBE_MAX_PERM_COMPETITORS 6 /* batch.py:27 MAX_FULL_OUTCOME_COMPETITORS */
 
@@ -56,7 +58,9 @@ enum {
 enum {
     BBE_MODE_NATIVE = 0, /* in-register Philox4x32-10, FP32 race state: statistically equivalent */
     BBE_MODE_INJECT = 1, /* recorded reference draws (CSR), FP64 state: bit-exact to the reference */
-    BBE_MODE_MT = 2      /* CPython MT19937 from per-sim seeds, FP64 state: bit-exact from seeds */
+    BBE_MODE_MT = 2,     /* CPython MT19937 from per-sim seeds, FP64 state: bit-exact from seeds */
+    BBE_MODE_NATIVE64 = 3 /* in-register Philox4x32-10, FP64 state and the reference's FP64 operations:
+                             statistically equivalent (only the word generator differs), 53-bit draws */
 };
 
 enum { BBE_FAMILY_UNIFORM = 0, BBE_FAMILY_LOGNORMAL = 1 };
@@ -176,22 +180,25 @@ int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const 
  * continuations of `state`; the caller forms the Laplace probabilities (w + 1) / (d + n).
  *   mode BBE_MODE_MT:     dry run i replays random.Random(seed_i), seed_i the i-th getrandbits(64)
  *                         (simulate_from, race.py:393-406): the reference's own counts, bit for bit.
- *   mode BBE_MODE_NATIVE: the Philox stream keyed by seed_0 (statistically equal); the other d-1
+ *   mode BBE_MODE_NATIVE: the Philox stream keyed by seed_0 (statistically equal, FP32 state); the other d-1
  *                         draws only advance the stream, on the host while the GPU runs.
+ *   mode BBE_MODE_NATIVE64: the same Philox stream with the reference's FP64 race arithmetic.
  * Synchronous.  BBE_EDIVERGED: a dry run exceeded tick_limit (first_diverged, if not NULL, receives
- * its index in 0..d-1; the stream is advanced by d all the same). */
+ * its index k in 0..d-1); the stream is left advanced by k + 1 draws, where the reference's loop
+ * raises (agents.py:164).  Writes to the generator happen with the caller's GIL held when the call
+ * is bound through ctypes.PyDLL; the GIL is dropped for the GPU wait after the last write. */
 int bbe_rp_predict(const bbe_race* race, const bbe_competitor* comps, const bbe_state* state, int64_t d,
                    int32_t mode, uint32_t* state624, int32_t* pos, uint64_t* wins, int64_t* first_diverged);
 
-/* Prepared race (NATIVE): the parameter block is packed and uploaded once, on the current device,
+/* Prepared race (NATIVE / NATIVE64): the parameter block is packed and uploaded once, on the current device,
  * so repeated device-resident launches of one race state (the bench's steps, a shard's calls) copy
  * nothing per launch.  bbe_launch_prepared adds the tallies of sims [sim_offset, sim_offset +
  * n_sims) into d_tally (device, bbe_tally_len(n) u64) on `stream`, asynchronously; a prepared race
  * serves one launch at a time (callers serialise).  bbe_prepared_kernel_ms: device time of the last
  * launch (waits for it), -1 if none. */
 typedef struct bbe_prepared bbe_prepared;
-int bbe_prepare(const bbe_race* race, const bbe_competitor* comps, const bbe_state* state,
-                int32_t lanes_per_slot_hint, bbe_prepared** out);
+int bbe_prepare(const bbe_race* race, const bbe_competitor* comps, const bbe_state* state, int32_t mode,
+                int32_t lanes_per_slot_hint, bbe_prepared** out); /* mode: BBE_MODE_NATIVE or _NATIVE64 */
 int bbe_launch_prepared(bbe_prepared* prepared, int64_t n_sims, int64_t sim_offset, uint64_t seed,
                         uint64_t* d_tally, void* stream);
 float bbe_prepared_kernel_ms(bbe_prepared* prepared);

@@ -96,6 +96,9 @@ def lib():
                                              P(i64)]
         L.orc_batch.argtypes = [P(OrcRace), P(OrcComp), i32, i64, P(d), P(d), P(i64), i64, P(u64), u64,
                                 i32, P(u64), P(u64), P(i32), P(i64), P(i64), P(i64)]
+        L.orc_batch_px.argtypes = [P(OrcRace), P(OrcComp), i32, i64, P(d), P(d), P(i64), i64, i64, u64, i32,
+                                   P(u64), P(u64), P(i32), P(i64), P(d), P(i64), P(i64), P(i64), P(i64)]
+        L.orc_philox4x32_10.argtypes = [P(ctypes.c_uint32), u64, P(ctypes.c_uint32)]
         L.orc_mt_random.argtypes = [u64, i64, P(d)]
         L.orc_mt_uniform.argtypes = [u64, d, d, i64, P(d)]
         L.orc_mt_getrandbits64.argtypes = [u64, i64, P(u64)]
@@ -235,6 +238,48 @@ def batch(cfg, n_sims: int, *, state=None, seeds=None, master: int = 0, threads:
                              ctypes.byref(blk), ctypes.byref(fd))
     return dict(wins=wins, ranks=ranks.reshape(n, n), winners=win_arr, ct=ct.value, blocked=blk.value, rc=rc,
                 first_diverged=fd.value)
+
+
+def batch_px(cfg, n_sims: int, key: int, *, state=None, sim_offset: int = 0, threads: int = 1,
+             records: bool = False):
+    """The NATIVE64 stream (native64_kernel.cuh) on the CPU: sims sim_offset .. sim_offset + n_sims - 1 of
+    the Philox4x32-10 stream keyed by ``key``, the reference's race engine in FP64.  Returns dict(wins,
+    ranks, ct, blocked, rc, first_diverged) and, with records=True, order / finish_ticks /
+    final_positions / blocked_per_sim arrays."""
+    race, comps = pack_race(cfg)
+    n = race.n
+    wins = np.zeros(n, np.uint64)
+    ranks = np.zeros(n * n, np.uint64)
+    order = fin = fpos = blk = None
+    if records:
+        order = np.zeros((n_sims, n), np.int32)
+        fin = np.zeros((n_sims, n), np.int64)
+        fpos = np.zeros((n_sims, n), np.float64)
+        blk = np.zeros(n_sims, np.int64)
+    ct, bl, fd = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    if state is None:
+        args = (1, 0, None, None, None)
+    else:
+        pos = np.array(state.positions, np.float64)
+        prev = np.array(state.prev_steps, np.float64)
+        f0 = _fin_array(state.finish_ticks)
+        args = (0, int(state.tick), _ptr(pos, ctypes.c_double), _ptr(prev, ctypes.c_double), _ptr(f0, ctypes.c_int64))
+    rc = lib().orc_batch_px(ctypes.byref(race), comps, *args, int(n_sims), int(sim_offset), key & 0xFFFFFFFFFFFFFFFF,
+                            threads, _ptr(wins, ctypes.c_uint64), _ptr(ranks, ctypes.c_uint64),
+                            _ptr(order, ctypes.c_int32), _ptr(fin, ctypes.c_int64), _ptr(fpos, ctypes.c_double),
+                            _ptr(blk, ctypes.c_int64), ctypes.byref(ct), ctypes.byref(bl), ctypes.byref(fd))
+    out = dict(wins=wins, ranks=ranks.reshape(n, n), ct=ct.value, blocked=bl.value, rc=rc, first_diverged=fd.value)
+    if records:
+        out.update(order=order, finish_ticks=fin, final_positions=fpos, blocked_per_sim=blk)
+    return out
+
+
+def philox4x32_10(counter, key: int) -> list:
+    """One Philox4x32-10 block: four counter words and a 64-bit key -> four output words."""
+    c = np.array(counter, np.uint32)
+    out = np.zeros(4, np.uint32)
+    lib().orc_philox4x32_10(_ptr(c, ctypes.c_uint32), key & 0xFFFFFFFFFFFFFFFF, _ptr(out, ctypes.c_uint32))
+    return [int(x) for x in out]
 
 
 def rp_seeds(agent_seed: int, d: int) -> np.ndarray:

@@ -196,8 +196,37 @@ typedef struct {
 
 enum { ORC_OK = 0, ORC_EDIVERGED = 2, ORC_EDRAWS = 3, ORC_EINVAL = 1 };
 
-/* Draw source: an MT stream (the reference) or a replay of recorded draw values. */
+/* ------------------------------------------------------------------------------------------ */
+/* Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11 "Parallel random numbers: as easy as 1, 2, 3"): */
+/* the counter-based word generator of the NATIVE / NATIVE64 kernels.  Pinned to ATen's independent */
+/* philox_engine (torch/include/ATen/core/PhiloxRNGEngine.h) by tests/golden/make_philox_golden.py. */
+/* ------------------------------------------------------------------------------------------ */
+void orc_philox4x32_10(const uint32_t* ctr_in, uint64_t key, uint32_t* out) {
+    uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+    uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+    for (int r = 0; r < 10; r++) {
+        uint64_t p0 = (uint64_t)0xD2511F53u * c0, p1 = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0, n1 = (uint32_t)p1;
+        uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1, n3 = (uint32_t)p0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* CPython's random_random() formula applied to two words: a 53-bit fraction in [0, 1) */
+static double res53(uint32_t w0, uint32_t w1) {
+    uint32_t a = w0 >> 5, b = w1 >> 6;
+    return (a * 67108864.0 + b) * (1.0 / 9007199254740992.0);
+}
+
+/* Draw source: an MT stream (the reference), a replay of recorded draw values, or the NATIVE64
+ * Philox stream (counter-based: the draw of competitor c at the sim's relative tick rt). */
 typedef struct {
+    int philox;    /* 1: NATIVE64 stream keyed by `key` for global sim index `gs` */
+    uint64_t key, gs;
+    int64_t rt;    /* ticks this sim has advanced (-1: run_race's priming draws) */
     orc_mt* mt;
     const double* replay;
     int64_t replay_len;
@@ -207,9 +236,29 @@ typedef struct {
     int underflow;
 } orc_draws;
 
-static double draw_raw(orc_draws* d, const orc_comp* c) {
+/* NATIVE64 draw (native64_kernel.cuh): counter (rt / 2, c, gs) -- word 0 = 0xFFFFFFFF for the
+ * priming draws -- gives (x, y, z, w); a uniform takes lo + (hi - lo) * random53 of (x, y) at even
+ * rt and (z, w) at odd rt; a lognormal takes scale * exp(mu + z * sigma) with the Box-Muller normal
+ * of u1 = 1 - random53(x, y), u2 = random53(z, w): the cosine branch at even rt, the sine at odd. */
+static double draw_philox(const orc_draws* d, const orc_comp* cp, int c) {
+    uint32_t ctr[4] = {d->rt < 0 ? 0xFFFFFFFFu : (uint32_t)(d->rt >> 1), (uint32_t)c, (uint32_t)d->gs,
+                       (uint32_t)(d->gs >> 32)};
+    uint32_t w[4];
+    orc_philox4x32_10(ctr, d->key, w);
+    int odd = d->rt >= 0 && (d->rt & 1);
+    if (cp->family == 0) return cp->lo + (cp->hi - cp->lo) * (odd ? res53(w[2], w[3]) : res53(w[0], w[1]));
+    double u1 = 1.0 - res53(w[0], w[1]), u2 = res53(w[2], w[3]);
+    double r = sqrt(-2.0 * log(u1));
+    double t = 3.141592653589793 * (2.0 * u2);
+    double z = odd ? r * sin(t) : r * cos(t);
+    return cp->scale * exp(cp->mu + z * cp->sigma);
+}
+
+static double draw_raw(orc_draws* d, const orc_comp* c, int ci) {
     double v;
-    if (d->replay) {
+    if (d->philox) {
+        v = draw_philox(d, c, ci);
+    } else if (d->replay) {
         if (d->cursor >= d->replay_len) { d->underflow = 1; v = c->family ? c->scale : c->lo; }
         else v = d->replay[d->cursor];
     } else if (c->family == 0) {
@@ -249,7 +298,7 @@ static void initial_state(const orc_race* r, const orc_comp* comps, orc_draws* d
     for (int c = 0; c < r->n; c++) {
         double pref = orc_preference_factor(r->conditions, comps[c].preference, comps[c].pref_sensitivity);
         double resp = resp_at(&comps[c], 0.0, r->track_length);
-        st->prev[c] = resp * pref * draw_raw(d, &comps[c]);
+        st->prev[c] = resp * pref * draw_raw(d, &comps[c], c);
         st->pos[c] = 0.0;
         st->fin[c] = -1;
     }
@@ -286,7 +335,7 @@ static void advance(const orc_race* r, const orc_comp* comps, orc_draws* d, orc_
         int f = front_runner(st, n, c, &gap);
         if (f < 0 || gap > cp->theta) {
             double pref = orc_preference_factor(r->conditions, cp->preference, cp->pref_sensitivity);
-            steps[c] = resp * pref * draw_raw(d, cp);
+            steps[c] = resp * pref * draw_raw(d, cp, c);
         } else {
             double a = st->prev[c], b = st->prev[f];
             steps[c] = resp * (b < a ? b : a); /* Python min(a, b) */
@@ -356,6 +405,7 @@ static int run_core(const orc_race* r, const orc_comp* comps, orc_draws* d, orc_
             break;
         }
         for (int c = 0; c < n; c++) ct += st->fin[c] < 0;
+        d->rt = st->tick - start;
         advance(r, comps, d, st, steps);
     }
     if (d->replay && rc == ORC_OK && (d->underflow || d->cursor != d->replay_len)) rc = ORC_EDRAWS;
@@ -401,6 +451,34 @@ int orc_simulate_from(const orc_race* r, const orc_comp* comps, int64_t tick, co
     else { mt_seed_u64(&mt, seed); d.mt = &mt; }
     d.rec = rec;
     d.rec_cap = rec_cap;
+    double pos[ORC_MAXN], prev[ORC_MAXN];
+    int64_t fin[ORC_MAXN];
+    memcpy(pos, pos0, sizeof(double) * n);
+    memcpy(prev, prev0, sizeof(double) * n);
+    memcpy(fin, fin0, sizeof(int64_t) * n);
+    orc_state st = {tick, pos, prev, fin, 0};
+    return run_core(r, comps, &d, &st, 0, out);
+}
+
+/* run_race / simulate_from on the NATIVE64 Philox stream (key, global sim index gs) instead of MT. */
+int orc_run_race_px(const orc_race* r, const orc_comp* comps, uint64_t key, uint64_t gs, orc_out* out) {
+    int n = r->n;
+    if (n < 1 || n > ORC_MAXN) return ORC_EINVAL;
+    orc_draws d = {0};
+    d.philox = 1; d.key = key; d.gs = gs; d.rt = -1;
+    double pos[ORC_MAXN], prev[ORC_MAXN];
+    int64_t fin[ORC_MAXN];
+    orc_state st = {0, pos, prev, fin, 0};
+    initial_state(r, comps, &d, &st);
+    return run_core(r, comps, &d, &st, 1, out);
+}
+
+int orc_simulate_from_px(const orc_race* r, const orc_comp* comps, int64_t tick, const double* pos0,
+                         const double* prev0, const int64_t* fin0, uint64_t key, uint64_t gs, orc_out* out) {
+    int n = r->n;
+    if (n < 1 || n > ORC_MAXN) return ORC_EINVAL;
+    orc_draws d = {0};
+    d.philox = 1; d.key = key; d.gs = gs;
     double pos[ORC_MAXN], prev[ORC_MAXN];
     int64_t fin[ORC_MAXN];
     memcpy(pos, pos0, sizeof(double) * n);
@@ -471,6 +549,12 @@ typedef struct {
     const int64_t* fin0;
     const uint64_t* seeds; /* per-sim seeds, or NULL -> derive_seed(master, "run", i) */
     uint64_t master;
+    int px;              /* 1: NATIVE64 Philox stream (key = master, global index sim_offset + s) */
+    int64_t sim_offset;
+    int32_t* order_out;  /* optional per-sim records [n_sims*n] / [n_sims] */
+    int64_t* fin_out;
+    double* fpos_out;
+    int64_t* blk_out;
     int64_t lo, hi;
     int32_t* winners;
     uint64_t wins[ORC_MAXN];
@@ -484,13 +568,26 @@ static void* batch_worker(void* arg) {
     int n = j->r->n;
     int64_t fin[ORC_MAXN];
     int32_t order[ORC_MAXN];
+    double fpos[ORC_MAXN];
     j->first_diverged = -1;
     for (int64_t s = j->lo; s < j->hi; s++) {
-        uint64_t seed = j->seeds ? j->seeds[s] : orc_derive_seed_run(j->master, (uint64_t)s);
-        orc_out out = {fin, order, NULL, 0, 0, 0, 0};
-        int rc = j->from_start ? orc_run_race(j->r, j->comps, seed, NULL, 0, NULL, 0, &out)
+        orc_out out = {fin, order, fpos, 0, 0, 0, 0};
+        int rc;
+        if (j->px) {
+            uint64_t gs = (uint64_t)(j->sim_offset + s);
+            rc = j->from_start ? orc_run_race_px(j->r, j->comps, j->master, gs, &out)
+                               : orc_simulate_from_px(j->r, j->comps, j->tick, j->pos0, j->prev0, j->fin0, j->master,
+                                                      gs, &out);
+        } else {
+            uint64_t seed = j->seeds ? j->seeds[s] : orc_derive_seed_run(j->master, (uint64_t)s);
+            rc = j->from_start ? orc_run_race(j->r, j->comps, seed, NULL, 0, NULL, 0, &out)
                                : orc_simulate_from(j->r, j->comps, j->tick, j->pos0, j->prev0, j->fin0, seed,
                                                    NULL, 0, NULL, 0, &out);
+        }
+        if (j->order_out) memcpy(j->order_out + s * n, order, sizeof(int32_t) * n);
+        if (j->fin_out) memcpy(j->fin_out + s * n, fin, sizeof(int64_t) * n);
+        if (j->fpos_out) memcpy(j->fpos_out + s * n, fpos, sizeof(double) * n);
+        if (j->blk_out) j->blk_out[s] = out.blocked;
         if (rc != ORC_OK) {
             if (j->first_diverged < 0) j->first_diverged = s;
             j->rc = rc;
@@ -506,10 +603,11 @@ static void* batch_worker(void* arg) {
     return NULL;
 }
 
-int orc_batch(const orc_race* r, const orc_comp* comps, int from_start, int64_t tick, const double* pos0,
-              const double* prev0, const int64_t* fin0, int64_t n_sims, const uint64_t* seeds, uint64_t master,
-              int nthreads, uint64_t* wins, uint64_t* ranks, int32_t* winners, int64_t* ct, int64_t* blocked,
-              int64_t* first_diverged) {
+static int batch_run(const orc_race* r, const orc_comp* comps, int from_start, int64_t tick, const double* pos0,
+                     const double* prev0, const int64_t* fin0, int64_t n_sims, const uint64_t* seeds, uint64_t master,
+                     int px, int64_t sim_offset, int32_t* order_out, int64_t* fin_out, double* fpos_out,
+                     int64_t* blk_out, int nthreads, uint64_t* wins, uint64_t* ranks, int32_t* winners, int64_t* ct,
+                     int64_t* blocked, int64_t* first_diverged) {
     int n = r->n;
     if (n < 1 || n > ORC_MAXN || nthreads < 1) return ORC_EINVAL;
     if (nthreads > 256) nthreads = 256;
@@ -519,6 +617,8 @@ int orc_batch(const orc_race* r, const orc_comp* comps, int from_start, int64_t 
         orc_job* j = &jobs[t];
         j->r = r; j->comps = comps; j->from_start = from_start; j->tick = tick;
         j->pos0 = pos0; j->prev0 = prev0; j->fin0 = fin0; j->seeds = seeds; j->master = master;
+        j->px = px; j->sim_offset = sim_offset;
+        j->order_out = order_out; j->fin_out = fin_out; j->fpos_out = fpos_out; j->blk_out = blk_out;
         j->lo = n_sims * t / nthreads; j->hi = n_sims * (t + 1) / nthreads;
         j->winners = winners;
         j->ranks = ranks ? (uint64_t*)calloc((size_t)n * n, sizeof(uint64_t)) : NULL;
@@ -539,4 +639,22 @@ int orc_batch(const orc_race* r, const orc_comp* comps, int from_start, int64_t 
     }
     free(jobs);
     return rc;
+}
+
+int orc_batch(const orc_race* r, const orc_comp* comps, int from_start, int64_t tick, const double* pos0,
+              const double* prev0, const int64_t* fin0, int64_t n_sims, const uint64_t* seeds, uint64_t master,
+              int nthreads, uint64_t* wins, uint64_t* ranks, int32_t* winners, int64_t* ct, int64_t* blocked,
+              int64_t* first_diverged) {
+    return batch_run(r, comps, from_start, tick, pos0, prev0, fin0, n_sims, seeds, master, 0, 0, NULL, NULL, NULL,
+                     NULL, nthreads, wins, ranks, winners, ct, blocked, first_diverged);
+}
+
+/* The NATIVE64 stream: sim s = global index sim_offset + s of the Philox stream keyed by `key`;
+ * optional per-sim finish orders, finish ticks, final positions and blocked counts. */
+int orc_batch_px(const orc_race* r, const orc_comp* comps, int from_start, int64_t tick, const double* pos0,
+                 const double* prev0, const int64_t* fin0, int64_t n_sims, int64_t sim_offset, uint64_t key,
+                 int nthreads, uint64_t* wins, uint64_t* ranks, int32_t* order_out, int64_t* fin_out,
+                 double* fpos_out, int64_t* blk_out, int64_t* ct, int64_t* blocked, int64_t* first_diverged) {
+    return batch_run(r, comps, from_start, tick, pos0, prev0, fin0, n_sims, NULL, key, 1, sim_offset, order_out,
+                     fin_out, fpos_out, blk_out, nthreads, wins, ranks, NULL, ct, blocked, first_diverged);
 }

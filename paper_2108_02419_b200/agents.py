@@ -138,8 +138,10 @@ def rp_predict(state, config, d: int, rng, *, mode: str = "mt") -> tuple[float, 
 
     mode="mt" (default): every continuation replays the reference's own MT19937 stream from its
     dry-run seed, so the probabilities equal the reference's exactly (a true drop-in).
-    mode="native": Philox stream keyed by the first dry-run seed -- statistically equal to the
-    reference (binomial bounds, tests/test_gpu_native.py) and the fastest path.
+    mode="native64": Philox stream keyed by the first dry-run seed with the reference's FP64 race
+    arithmetic (only the word generator differs; tests/test_gpu_native64.py) -- statistically equal.
+    mode="native": the same stream with FP32 race state -- the fastest path (binomial bounds,
+    tests/test_gpu_native.py).
     """
     n = len(config.competitors)
     if d <= 0:

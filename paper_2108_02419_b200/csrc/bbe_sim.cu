@@ -233,8 +233,8 @@ int validate(const bbe_race* race, const bbe_competitor* comps, const bbe_state*
     }
     if (!st->from_start && (!st->positions || !st->prev_steps || !st->finish_ticks))
         return fail(BBE_EINVAL, "continuation state needs positions, prev_steps and finish_ticks");
-    if (rq->mode == BBE_MODE_NATIVE) {
-        // the FP32 front-runner frame (native_frame) needs finite positions and track length
+    if (rq->mode == BBE_MODE_NATIVE || rq->mode == BBE_MODE_NATIVE64) {
+        // the front-runner frames (native_frame) need finite positions and track length
         if (!std::isfinite(race->track_length)) return fail(BBE_EINVAL, "mode native needs a finite track_length");
         for (int c = 0; !st->from_start && c < n; ++c)
             if (!std::isfinite(st->positions[c])) return fail(BBE_EINVAL, "mode native needs finite positions");
@@ -243,7 +243,7 @@ int validate(const bbe_race* race, const bbe_competitor* comps, const bbe_state*
     if (rq->group_size < 0) return fail(BBE_EINVAL, "group_size must be >= 0");
     if (rq->mode == BBE_MODE_INJECT) {
         if (!rq->draws || !rq->draw_offsets) return fail(BBE_EINVAL, "inject mode needs draws and draw_offsets");
-    } else if (rq->mode != BBE_MODE_MT && rq->mode != BBE_MODE_NATIVE) {
+    } else if (rq->mode != BBE_MODE_MT && rq->mode != BBE_MODE_NATIVE && rq->mode != BBE_MODE_NATIVE64) {
         return fail(BBE_EINVAL, "unknown mode");
     }
     return BBE_OK;
@@ -341,7 +341,34 @@ struct NativeFrame {
     float shift;
     uint32_t key_base;
     int key_bits;
+    double c64;      // NATIVE64: key of pos = mantissa bits 51..26 of pos + c64 (native64_frame)
+    uint32_t sub64;  // NATIVE64: the exponent bit the key window drags in, << 31
 };
+
+// NATIVE64 coarse front-runner key (native64_kernel.cuh): every racing position p -- from the
+// smallest racing start position `base` up to hi = max(L, largest racing start position) -- maps to
+// y = fl(p + c64) inside one binade (2^E, 2^(E+1)), so the 26 mantissa bits below the top are a
+// monotone key of p with cells 2^(E-26) wide.  c64 = 2^E + 2^(E-20) - base: the 2^(E-20) margin keeps
+// y above 2^E (and every racing key >= 2^6 > 0, the value of a finished lane) despite the rounding of
+// c64 itself; 2^E >= (1 + 2^-10) (hi - base) keeps y below 2^(E+1).
+void native64_frame(const bbe_race* race, const bbe_state* st, NativeFrame* fr) {
+    const int n = race->n;
+    double lo = INFINITY, hi = race->track_length;
+    for (int c = 0; c < n; ++c) {
+        if (!st->from_start && st->finish_ticks[c] >= 0) continue;
+        const double p = st->from_start ? 0.0 : st->positions[c];
+        lo = std::min(lo, p);
+        hi = std::max(hi, p);
+    }
+    if (!(lo < INFINITY)) lo = 0.0;  // nobody racing: the scan never runs on a live key
+    const double R = std::max(hi - lo, 1e-300) * (1.0 + 1.0 / 1024.0);
+    int e = 0;
+    std::frexp(R, &e);  // R < 2^e
+    const double two_e = std::ldexp(1.0, e);
+    fr->c64 = two_e + std::ldexp(1.0, e - 20) - lo;
+    const int biased = e + 1023;  // exponent field of y
+    fr->sub64 = (uint32_t)(biased & 1) << 31;
+}
 
 uint32_t f32_bits(float f) {
     uint32_t u;
@@ -387,6 +414,12 @@ NativeFrame native_frame(const bbe_race* race, const bbe_state* st, int W) {
         }
     }
     fr.shift = NAN;  // unreachable for finite inputs (validate() rejects non-finite ones)
+    return fr;
+}
+
+NativeFrame native_frames(const bbe_race* race, const bbe_state* st, int W) {
+    NativeFrame fr = native_frame(race, st, W);
+    native64_frame(race, st, &fr);
     return fr;
 }
 
@@ -468,6 +501,23 @@ int pick_ticks(int K, bool scan, double T) {
     return 4;
 }
 
+// NATIVE64 ticks per block: scan-free fields 16 from ~43 expected ticks (the FP32 K = 1 threshold),
+// else 8; with a scan 8 (the only build).
+int pick_ticks64(bool scan, double T) {
+    static const int env = [] {
+        const char* e = std::getenv("BBE_TICKS64");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (scan) return 8;
+    if (env == 8 || env == 16) return env;
+    return T >= 43.0 ? 16 : 8;
+}
+
+KernelFn pick_native64_scan(int k, int ch, bool ln) {
+    if (k == 1) return ln ? pick_native64_scan_k1_ln1(k, ch) : pick_native64_scan_k1_ln0(k, ch);
+    return ln ? pick_native64_scan_kn_ln1(k, ch) : pick_native64_scan_kn_ln0(k, ch);
+}
+
 KernelFn pick_native(int k, int ch, bool scan, int vec, int nt) {
     if (k == 1) return nt == 16 ? pick_native_k1_nt16(ch, scan, vec) : pick_native_k1_nt8(ch, scan, vec);
     if (vec != 4) return nullptr;
@@ -476,10 +526,10 @@ KernelFn pick_native(int k, int ch, bool scan, int vec, int nt) {
 
 int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, const bbe_state* st,
               const bbe_request* rq, int want_perms, Plan* pl) {
-    bool scan = false;  // any theta > 0: the front-runner scan is needed
+    bool scan = false;  // any theta > 0 (or NaN: `gap > NaN` is false, race.py:271): the scan is needed
     bool ln = false;    // any lognormal competitor (MT: speculative draw rounds)
     for (int c = 0; c < race->n; ++c) {
-        scan = scan || comps[c].theta > 0.0;
+        scan = scan || !(comps[c].theta <= 0.0);
         ln = ln || comps[c].family == BBE_FAMILY_LOGNORMAL;
     }
     const int n = race->n;
@@ -488,7 +538,8 @@ int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, co
     // exact modes: the fewest slots that fit a warp (an MT slot adds a speculative word window per
     // lane); NATIVE: the measured layout rule
     const int k_min = (n + kWarp - 1) / kWarp;
-    if (rq->mode == BBE_MODE_NATIVE) pl->K = choose_k(n, scan, rq->lanes_per_slot_hint);
+    const bool native = rq->mode == BBE_MODE_NATIVE || rq->mode == BBE_MODE_NATIVE64;
+    if (native) pl->K = choose_k(n, scan, rq->lanes_per_slot_hint);
     else pl->K = (rq->lanes_per_slot_hint >= k_min && rq->lanes_per_slot_hint <= 4) ? rq->lanes_per_slot_hint : k_min;
     if (pl->K > 4) pl->K = -1;
     if (pl->K < 0) return fail(BBE_EINVAL, "field too large for one warp");
@@ -498,16 +549,22 @@ int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, co
     // NATIVE K = 1 with a scan: 2-word key loads when that avoids padding keys (W % 4 in {1, 2})
     const bool vec2 = BBE_NATIVE_VEC2 && rq->mode == BBE_MODE_NATIVE && pl->K == 1 && scan &&
                       ((pl->W + 1) & ~1) < ((pl->W + 3) & ~3);
-    pl->CH = vec2 ? (pl->W + 1) / 2 : (pl->W + 3) / 4;
+    pl->CH = vec2 ? (pl->W + 1) / 2 : (pl->W + 3) / 4;  // NATIVE64: always 4-word chunks
     pl->WP = (vec2 ? 2 : 4) * pl->CH;
     pl->nperm = want_perms ? nperm_for(n) : 0;
     TallyLayout TL{n, pl->nperm};
     pl->tally_len = TL.len();
-    const int kmode = rq->mode == BBE_MODE_NATIVE ? NATIVE : (rq->mode == BBE_MODE_MT ? MT : INJECT);
+    const int kmode = rq->mode == BBE_MODE_NATIVE ? NATIVE
+                      : rq->mode == BBE_MODE_NATIVE64 ? NATIVE64 : (rq->mode == BBE_MODE_MT ? MT : INJECT);
     pl->smem = smem_bytes(kmode, (TL.hist_len() + 1) & ~1, pl->K, pl->S, pl->WP);
-    pl->NT = rq->mode == BBE_MODE_NATIVE ? pick_ticks(pl->K, scan, expected_ticks(race, comps, st)) : 4;
-    pl->fn = rq->mode == BBE_MODE_NATIVE ? pick_native(pl->K, pl->CH, scan, vec2 ? 2 : 4, pl->NT)
-                                         : pick_exact(rq->mode == BBE_MODE_MT ? MT : INJECT, pl->K, ln);
+    if (rq->mode == BBE_MODE_NATIVE64) {
+        pl->NT = pick_ticks64(scan, expected_ticks(race, comps, st));
+        pl->fn = scan ? pick_native64_scan(pl->K, pl->CH, ln) : pick_native64_free(pl->K, ln, pl->NT);
+    } else {
+        pl->NT = rq->mode == BBE_MODE_NATIVE ? pick_ticks(pl->K, scan, expected_ticks(race, comps, st)) : 4;
+        pl->fn = rq->mode == BBE_MODE_NATIVE ? pick_native(pl->K, pl->CH, scan, vec2 ? 2 : 4, pl->NT)
+                                             : pick_exact(rq->mode == BBE_MODE_MT ? MT : INJECT, pl->K, ln);
+    }
     if (!pl->fn && rq->mode == BBE_MODE_NATIVE && pl->NT != 4) {
         pl->NT = 4;  // that block length is not built for this layout
         pl->fn = pick_native(pl->K, pl->CH, scan, vec2 ? 2 : 4, 4);
@@ -612,8 +669,20 @@ int bbe_mt_advance64_many(int64_t n_gen, uint32_t* const* states, int32_t* const
     for (int64_t g = 0; g < n_gen; ++g) words += counts[g];
     // below ~64k draws the thread start-up costs more than it saves
     threads = (int)std::min<int64_t>(threads, std::max<int64_t>(1, std::min<int64_t>(n_gen, words / 65536 + 1)));
+    // a generator listed more than once is advanced by one thread, in list order (its owner: the
+    // thread of its first occurrence), so no two threads ever write the same state
+    std::vector<int> owner(n_gen);
+    {
+        std::map<const uint32_t*, int> first;
+        for (int64_t g = 0; g < n_gen; ++g) {
+            auto it = first.find(states[g]);
+            owner[g] = it == first.end() ? (int)(g % threads) : it->second;
+            if (it == first.end()) first.emplace(states[g], owner[g]);
+        }
+    }
     auto work = [&](int t) {
-        for (int64_t g = t; g < n_gen; g += threads) {
+        for (int64_t g = 0; g < n_gen; ++g) {
+            if (owner[g] != t) continue;
             uint64_t* o = outs ? outs[g] : nullptr;
             const int64_t ol = (o && out_lens) ? out_lens[g] : 0;
             *pos[g] = (int32_t)bbe_host_mt_getrandbits64(states[g], (uint32_t)*pos[g], counts[g], o, o ? ol : 0);
@@ -834,7 +903,7 @@ static int launch_all(DevCtx* ctx, const Plan& pl, LaunchArgs a, const bbe_compe
                       uint64_t seed_master, cudaStream_t stream) {
     a.scan = 0;
     for (int c = 0; c < a.n; ++c)
-        if (comps[c].theta > 0.0) a.scan = 1;
+        if (!(comps[c].theta <= 0.0)) a.scan = 1;  // theta > 0 or NaN (see make_plan)
     if (pl.mode != BBE_MODE_MT) return launch_one(ctx, pl, a, stream);
 
     if (!ctx->mt_table) {
@@ -875,6 +944,8 @@ static int build_args(const Plan& pl, const bbe_race* race, const bbe_state* st,
     a.key_bits = fr.key_bits;
     a.key_mul = 1u << fr.key_bits;
     a.key_nmul = 0u - a.key_mul;
+    a.key_c64 = fr.c64;
+    a.key_sub64 = fr.sub64;
     philox_round_keys(rq->seed, a.rk);
     a.n = race->n;
     a.W = pl.W;
@@ -938,7 +1009,7 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
     BBE_CK(ctx->d_params.ensure(pbytes + tbytes + gbytes));
     BBE_CK(ctx->h_tally.ensure(tbytes));
     pack_params(race, comps, st, (double*)ctx->h_params.p);
-    const NativeFrame fr = native_frame(race, st, pl.W);
+    const NativeFrame fr = native_frames(race, st, pl.W);
     pack_params_f32(race, comps, st, (double*)ctx->h_params.p, fr);
     std::memset((char*)ctx->h_params.p + pbytes, 0, tbytes + gbytes);
     uint64_t* const d_tally = (uint64_t*)((char*)ctx->d_params.p + pbytes);
@@ -981,7 +1052,8 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
     }
     size_t traj_elems = 0;
     if (out->traj_cap > 0 && out->traj_positions && out->traj_prev_steps) {
-        if (rq->mode == BBE_MODE_NATIVE) return fail(BBE_EINVAL, "trajectories are recorded by the exact modes (mt, inject)");
+        if (rq->mode == BBE_MODE_NATIVE || rq->mode == BBE_MODE_NATIVE64)
+            return fail(BBE_EINVAL, "trajectories are recorded by the exact modes (mt, inject)");
         traj_elems = (size_t)ns * ((size_t)out->traj_cap + 1) * n;
         BBE_CK(ctx->d_traj.ensure(2 * traj_elems * sizeof(double)));
         dev.traj_positions = (double*)ctx->d_traj.p;
@@ -1156,7 +1228,7 @@ static int enqueue_tally(DevCtx* ctx, const bbe_race* race, const bbe_competitor
     BBE_CK(ctx->d_params.ensure(pbytes + tbytes));
     BBE_CK(ctx->h_tally.ensure(tbytes));
     pack_params(race, comps, st, (double*)ctx->h_params.p);
-    const NativeFrame fr = native_frame(race, st, pl.W);
+    const NativeFrame fr = native_frames(race, st, pl.W);
     pack_params_f32(race, comps, st, (double*)ctx->h_params.p, fr);
     std::memset((char*)ctx->h_params.p + pbytes, 0, tbytes);
     uint64_t* const d_tally = (uint64_t*)((char*)ctx->d_params.p + pbytes);
@@ -1165,7 +1237,7 @@ static int enqueue_tally(DevCtx* ctx, const bbe_race* race, const bbe_competitor
     // the graph is kept per context and re-captured when its grid changes, so it is used only for
     // calls that fill the persistent grid (their grid is the same from call to call)
     const int64_t sims_per_block = (int64_t)kWarpsPerBlock * pl.S;
-    if (pl.mode == BBE_MODE_NATIVE && rq.n_sims <= kMaxLaunchSims &&
+    if ((pl.mode == BBE_MODE_NATIVE || pl.mode == BBE_MODE_NATIVE64) && rq.n_sims <= kMaxLaunchSims &&
         (rq.n_sims + sims_per_block - 1) / sims_per_block >= pl.grid)
         return launch_graph(ctx, pl, a, pbytes + tbytes, tbytes, d_tally);
     BBE_CK(cudaMemcpyAsync(ctx->d_params.p, ctx->h_params.p, pbytes + tbytes, cudaMemcpyHostToDevice, s));
@@ -1208,13 +1280,59 @@ static int finish_tally(DevCtx* ctx, const Plan& pl, int n, int64_t limit, uint6
     return BBE_OK;
 }
 
+// The entry points that write a CPython random.Random in place (bbe_rp_predict, bbe_mt_advance64*)
+// are bound through ctypes.PyDLL, so they run with the GIL held and no other Python thread can touch
+// the generator mid-write.  bbe_rp_predict then drops the GIL for its GPU wait, once every write to
+// the generator is done (and takes it back before returning).  The CPython symbols are looked up in
+// the running process; in a process without Python, or a caller without the GIL, nothing happens.
+class GilRelease {
+  public:
+    void release() {
+        const Fns& f = fns();
+        if (!ts_ && f.check && f.save && f.restore && f.check()) ts_ = f.save();
+    }
+    void reacquire() {
+        if (ts_) fns().restore(ts_);
+        ts_ = nullptr;
+    }
+    ~GilRelease() { reacquire(); }
+
+  private:
+    struct Fns {
+        int (*check)() = nullptr;
+        void* (*save)() = nullptr;
+        void (*restore)(void*) = nullptr;
+    };
+    static const Fns& fns() {
+        static const Fns f = [] {
+            Fns g;
+            g.check = (int (*)())dlsym(RTLD_DEFAULT, "PyGILState_Check");
+            g.save = (void* (*)())dlsym(RTLD_DEFAULT, "PyEval_SaveThread");
+            g.restore = (void (*)(void*))dlsym(RTLD_DEFAULT, "PyEval_RestoreThread");
+            return g;
+        }();
+        return f;
+    }
+    void* ts_ = nullptr;
+};
+
+// On a diverged dry run the reference has drawn only the seeds up to and including the failing one
+// (agents.py:164 raises inside that simulate_from): put the bettor's stream back there.
+static void rewind_stream(const uint32_t* saved624, int32_t saved_pos, int64_t first_div, uint32_t* state624,
+                          int32_t* pos) {
+    if (first_div < 0) return;
+    std::memcpy(state624, saved624, 624 * sizeof(uint32_t));
+    *pos = (int32_t)bbe_host_mt_getrandbits64(state624, (uint32_t)saved_pos, first_div + 1, nullptr, 0);
+}
+
 extern "C" {
 
 int bbe_rp_predict(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, int64_t d, int32_t mode,
                    uint32_t* state624, int32_t* pos, uint64_t* wins, int64_t* first_diverged) {
     NvtxRange nvtx_range("bbe_rp_predict");
     if (!state624 || !pos || !wins || *pos < 0 || *pos > 624 || d < 0) return fail(BBE_EINVAL, "bad arguments");
-    if (mode != BBE_MODE_NATIVE && mode != BBE_MODE_MT) return fail(BBE_EINVAL, "rp_predict modes: native, mt");
+    if (mode != BBE_MODE_NATIVE && mode != BBE_MODE_NATIVE64 && mode != BBE_MODE_MT)
+        return fail(BBE_EINVAL, "rp_predict modes: native, native64, mt");
     bbe_request rq{};
     rq.n_sims = d;
     rq.mode = mode;
@@ -1227,7 +1345,13 @@ int bbe_rp_predict(const bbe_race* race, const bbe_competitor* comps, const bbe_
     Lease lease;
     if ((rc = acquire_ctx(lease))) return rc;
     DevCtx* const ctx = lease.c;
-    if (mode == BBE_MODE_NATIVE) {
+    uint32_t saved[624];
+    std::memcpy(saved, state624, sizeof(saved));
+    const int32_t saved_pos = *pos;
+    int64_t fd_local = -1;
+    int64_t* const fd = first_diverged ? first_diverged : &fd_local;
+    GilRelease gil;
+    if (mode == BBE_MODE_NATIVE || mode == BBE_MODE_NATIVE64) {
         // the first dry-run seed keys the Philox stream; the other d-1 draws advance the bettor's
         // stream on the host while the kernel runs
         uint64_t key = 0;
@@ -1237,7 +1361,11 @@ int bbe_rp_predict(const bbe_race* race, const bbe_competitor* comps, const bbe_
         if ((rc = make_plan(ctx, race, comps, st, &rq, 0, &pl))) return rc;
         if ((rc = enqueue_tally(ctx, race, comps, st, rq, nullptr, pl))) return rc;
         *pos = (int32_t)bbe_host_mt_getrandbits64(state624, (uint32_t)*pos, d - 1, nullptr, 0);
-        return finish_tally(ctx, pl, n, race->tick_limit, wins, first_diverged);
+        gil.release();
+        rc = finish_tally(ctx, pl, n, race->tick_limit, wins, fd);
+        gil.reacquire();
+        if (rc == BBE_EDIVERGED) rewind_stream(saved, saved_pos, *fd, state624, pos);
+        return rc;
     }
     // MT: every dry run replays random.Random(getrandbits(64)).  Large calls run as P parts on P
     // streams (P = d / kRpSplitMin, at most BBE_RP_PARTS): the host draws part p+1's seeds while the
@@ -1264,11 +1392,14 @@ int bbe_rp_predict(const bbe_race* race, const bbe_competitor* comps, const bbe_
         if ((rc = enqueue_mt_part(cx[p], race, comps, st, a0, a1 - a0, state624, pos, &pp[p]))) break;
         enq = p + 1;
     }
+    gil.release();  // every seed has been drawn
     int first_rc = BBE_OK;
     for (int p = 0; p < enq; ++p) {
-        rcs[p] = finish_tally(cx[p], pp[p], n, race->tick_limit, wins, first_diverged);
+        rcs[p] = finish_tally(cx[p], pp[p], n, race->tick_limit, wins, fd);
         if (rcs[p] && !first_rc) first_rc = rcs[p];
     }
+    gil.reacquire();
+    if (!rc && first_rc == BBE_EDIVERGED) rewind_stream(saved, saved_pos, *fd, state624, pos);
     return rc ? rc : first_rc;
 }
 
@@ -1414,7 +1545,7 @@ int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const 
     BBE_CK(ctx->d_params.ensure(pbytes));
     BBE_CK(cudaEventSynchronize(ctx->ev1));  // previous async launch on this ctx has read its params
     pack_params(race, comps, st, (double*)ctx->h_params.p);
-    const NativeFrame fr = native_frame(race, st, pl.W);
+    const NativeFrame fr = native_frames(race, st, pl.W);
     pack_params_f32(race, comps, st, (double*)ctx->h_params.p, fr);
     BBE_CK(cudaMemcpyAsync(ctx->d_params.p, ctx->h_params.p, pbytes, cudaMemcpyHostToDevice, s));
     LaunchArgs a;
@@ -1454,14 +1585,15 @@ static void free_prepared(bbe_prepared* p) {
 
 extern "C" {
 
-int bbe_prepare(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, int32_t lanes_per_slot_hint,
-                bbe_prepared** out) {
+int bbe_prepare(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, int32_t mode,
+                int32_t lanes_per_slot_hint, bbe_prepared** out) {
     NvtxRange nvtx_range("bbe_prepare");
     if (!out) return fail(BBE_EINVAL, "out is NULL");
     *out = nullptr;
     bbe_request rq{};
     rq.n_sims = INT64_MAX / 2;  // plan for a full persistent grid; each launch trims it
-    rq.mode = BBE_MODE_NATIVE;
+    if (mode != BBE_MODE_NATIVE && mode != BBE_MODE_NATIVE64) return fail(BBE_EINVAL, "prepared races: native, native64");
+    rq.mode = mode;
     rq.lanes_per_slot_hint = lanes_per_slot_hint;
     int rc = validate(race, comps, st, &rq);
     if (rc) return rc;
@@ -1477,7 +1609,7 @@ int bbe_prepare(const bbe_race* race, const bbe_competitor* comps, const bbe_sta
     p->race = *race;
     p->tick = st->from_start ? 0 : st->tick;
     p->from_start = st->from_start;
-    p->fr = native_frame(race, st, p->pl.W);
+    p->fr = native_frames(race, st, p->pl.W);
     const size_t pbytes = param_bytes(race->n);
     std::vector<double> h(pbytes / sizeof(double) + 1);
     pack_params(race, comps, st, h.data());
@@ -1508,7 +1640,7 @@ int bbe_launch_prepared(bbe_prepared* p, int64_t n_sims, int64_t sim_offset, uin
     rq.n_sims = n_sims;
     rq.sim_offset = sim_offset;
     rq.seed = seed;
-    rq.mode = BBE_MODE_NATIVE;
+    rq.mode = p->pl.mode;
     bbe_state st{};
     st.tick = p->tick;
     st.from_start = p->from_start;

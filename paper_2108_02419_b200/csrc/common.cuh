@@ -31,7 +31,7 @@ enum FieldF {
     NF_RP_EARLY, NF_RP_LATE, NF_EARLY, NF_LATE, NF_BP, NF_THETA, NF_POS0, NF_PREV0, NF_COUNT
 };
 
-enum Mode { NATIVE = 0, INJECT = 1, MT = 2 };
+enum Mode { NATIVE = 0, INJECT = 1, MT = 2, NATIVE64 = 3 };
 
 // "First failing sim" tally fields hold (2^63 - 1) - index (0 = none): a MAX reduction -- atomicMax
 // in a kernel, or a signed int64 all-reduce across ranks -- then keeps the smallest index.
@@ -65,6 +65,8 @@ struct LaunchArgs {
     float shift;      // NATIVE: positions, L and breakpoints are offset by this (the front-runner frame)
     uint32_t key_base;  // NATIVE: front-runner key = float bits of a position - key_base
     int key_bits;       // NATIVE: index bits packed under the key
+    double key_c64;       // NATIVE64: coarse front-runner key = mantissa bits 51..26 of (pos + key_c64)
+    uint32_t key_sub64;   //   (the constant exponent bit the 32-bit key window drags in, subtracted)
     uint32_t key_mul, key_nmul;  // NATIVE: 2^key_bits and -2^key_bits (runtime values: IMAD, not shifts)
     int n, W, S, WP, from_start, scan, perms;
     double L;
@@ -112,12 +114,12 @@ __host__ __device__ constexpr int mt_seg_words(int K) { return kMtWords + mt_sid
 constexpr int kXSlot = 66;         // exact modes: doubles per position row (S*round_up(W,2) <= 64, + pad)
 __host__ __device__ inline size_t smem_bytes(int mode, int hist_len_even, int K, int S, int WP) {
     size_t b = (size_t)hist_len_even * 8;
-    if (mode == NATIVE) {
+    if (mode == NATIVE || mode == NATIVE64) {
         const int vec = (WP % 4) ? 2 : 4;  // the host rounds W up to 2 (VEC 2) or 4 (VEC 4)
         b += (size_t)kWarpsPerBlock * native_warp_words(K, vec, WP / vec) * 4;
     }
     if (mode == MT) b += (size_t)kWarpsPerBlock * S * mt_seg_words(K) * 4;
-    if (mode != NATIVE) b += (size_t)kWarpsPerBlock * 2 * K * kXSlot * 8;
+    if (mode == INJECT || mode == MT) b += (size_t)kWarpsPerBlock * 2 * K * kXSlot * 8;
     if (mode == MT) b += (size_t)kWarpsPerBlock * kWarp * 4;  // per-warp lognormal offsets (trial pass)
     return b;
 }
@@ -135,8 +137,26 @@ __device__ __forceinline__ U4 philox_rk(U4 c, const uint32_t* rk) {
     return c;
 }
 
+// random_random(): m * 2^-53 with m = a*2^26 + b, a = w0>>5, b = w1>>6 -- an exact 53-bit fraction.
+// Built from bits, without integer->double conversions: D = 2^52 + (m mod 2^52) is m's low 52 bits
+// under the exponent of 2^52, E = D - 2^52 is exact, and m * 2^-53 = E * 2^-53 + (m >= 2^52 ? 0.5 : 0)
+// is one FMA whose result is exact (53 significant bits).  Checked against the integer formula on
+// 2e8 random word pairs and the edge words.
+__device__ __forceinline__ double random53(uint32_t w0, uint32_t w1) {
+    const uint32_t lo = ((w0 << 21) & 0xFC000000u) | (w1 >> 6);  // m bits 0..31
+    const uint32_t hi = w0 >> 11;                                  // m bits 32..52
+    const double E = __dsub_rn(__hiloint2double((int)(0x43300000u | (hi & 0xFFFFFu)), (int)lo), 4503599627370496.0);
+    const double top = __hiloint2double((hi >> 20) ? 0x3FE00000 : 0, 0);
+    return __fma_rn(E, 1.0 / 9007199254740992.0, top);
+}
+
 template <typename T>
 __device__ __forceinline__ T shfl(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+
+// Finish-tick sentinels of the NATIVE kernels (int32 finish ticks relative to the state's tick).
+constexpr int32_t kRacing = 0x7fffffff;
+constexpr int32_t kDiverged = 0x7ffffffe;
+constexpr int32_t kIdle = 0x7ffffffd;  // slot without a competitor / segment without a sim
 
 // ---- dynamic sim assignment (persistent kernels) ----
 // Every segment starts on sim `slot` (< segs_total); later sims are claimed from work[0], so a

@@ -204,7 +204,7 @@ exact_kernel(const LaunchArgs a) {
                 const int off = slot_base + 2 * __popc(m & lt_mask);
                 slot_base += 2 * __popc(m);
                 const uint32_t w0 = mt_temper(mt_word(off)), w1 = mt_temper(mt_word(off + 1));
-                d[k] = want[k] ? __dadd_rn(lo[k], __dmul_rn(span[k], mt_random53(w0, w1))) : 1.0;
+                d[k] = want[k] ? __dadd_rn(lo[k], __dmul_rn(span[k], random53(w0, w1))) : 1.0;
             }
             if (lane_on && running) mt_consume(slot_base);
             return;
@@ -261,11 +261,11 @@ exact_kernel(const LaunchArgs a) {
                 __syncwarp();  // ln_off reads precede the next round's writes
                 if (pend && lane < fail_lane) {
                     const int at = off + 4 * (lognorm[0] ? my_grid : my_shift);
-                    const double r = mt_random53(mt_temper(mt_word(at)), mt_temper(mt_word(at + 1)));
+                    const double r = random53(mt_temper(mt_word(at)), mt_temper(mt_word(at + 1)));
                     if (lognorm[0]) {
                         got_ln = true;
                         u1a = r;
-                        u2a = __dsub_rn(1.0, mt_random53(mt_temper(mt_word(at + 2)), mt_temper(mt_word(at + 3))));
+                        u2a = __dsub_rn(1.0, random53(mt_temper(mt_word(at + 2)), mt_temper(mt_word(at + 3))));
                     } else {
                         d[0] = __dadd_rn(lo[0], __dmul_rn(span[0], r));
                     }
@@ -314,13 +314,13 @@ exact_kernel(const LaunchArgs a) {
             uint32_t w23[K][2];
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                r01[k] = mt_random53(mt_temper(mt_word(off[k])), mt_temper(mt_word(off[k] + 1)));
+                r01[k] = random53(mt_temper(mt_word(off[k])), mt_temper(mt_word(off[k] + 1)));
                 w23[k][0] = mt_temper(mt_word(off[k] + 2));
                 w23[k][1] = mt_temper(mt_word(off[k] + 3));
                 ok[k] = true;
                 if (pend[k] && lognorm[k]) {
                     const double u1 = r01[k];
-                    const double u2 = __dsub_rn(1.0, mt_random53(w23[k][0], w23[k][1]));
+                    const double u2 = __dsub_rn(1.0, random53(w23[k][0], w23[k][1]));
                     // accept iff z*z/4 <= -log(u2) (Lib/random.py normalvariate).  Decide in FP32 when
                     // the two sides are far apart (relative 1e-4, absolute 1e-5: >25x the FP32 error of
                     // either side), else in FP64 exactly as CPython does -- the same decision either way.
@@ -598,7 +598,9 @@ exact_kernel(const LaunchArgs a) {
             bool any_blocked = false, need_exact = false;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                fr[k] = racing[k] && gap[k] > th[k];
+                // race.py:271: free when nobody is strictly ahead (front is None) -- tested explicitly, as
+                // gap = inf > theta fails for theta = inf or NaN -- or when gap > theta
+                fr[k] = racing[k] && (!(best[k] < CUDART_INF) || gap[k] > th[k]);
                 bl[k] = racing[k] && !fr[k];
                 any_blocked |= bl[k];
                 need_exact |= bl[k] && !(best[k] > __dmul_rn(2.0, gap[k]));

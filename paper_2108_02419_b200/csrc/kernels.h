@@ -23,6 +23,14 @@ KernelFn pick_native_k1_nt8(int ch, bool scan, int vec);
 KernelFn pick_native_k1_nt16(int ch, bool scan, int vec);
 KernelFn pick_native_kn_nt4(int k, int ch, bool scan);
 KernelFn pick_native_kn_nt16(int k, int ch, bool scan);
+// NATIVE64 (FP64 state): with a front-runner scan (8-tick blocks), or scan-free (NT = 8 or 16);
+// LN = some lognormal competitor
+KernelFn pick_native64_scan(int k, int ch, bool ln);  // bbe_sim.cu: dispatches to the four parts
+KernelFn pick_native64_scan_k1_ln0(int k, int ch);
+KernelFn pick_native64_scan_k1_ln1(int k, int ch);
+KernelFn pick_native64_scan_kn_ln0(int k, int ch);
+KernelFn pick_native64_scan_kn_ln1(int k, int ch);
+KernelFn pick_native64_free(int k, bool ln, int nt);
 // INJECT / MT (mode: INJECT or MT), K competitors per lane, LN = some lognormal competitor (MT)
 KernelFn pick_exact(int mode, int k, bool ln);
 // c_mt_init (init_genrand(19650218)), and the host libm's exp table for MT lognormal steps

@@ -82,19 +82,6 @@ __device__ __forceinline__ uint32_t mt_mix(uint32_t a, uint32_t b, uint32_t m) {
     return m ^ (y >> 1) ^ ((0u - (y & 1u)) & 0x9908b0dfu);
 }
 
-// random_random(): m * 2^-53 with m = a*2^26 + b, a = w0>>5, b = w1>>6 -- an exact 53-bit fraction.
-// Built from bits, without integer->double conversions: D = 2^52 + (m mod 2^52) is m's low 52 bits
-// under the exponent of 2^52, E = D - 2^52 is exact, and m * 2^-53 = E * 2^-53 + (m >= 2^52 ? 0.5 : 0)
-// is one FMA whose result is exact (53 significant bits).  Checked against the integer formula on
-// 2e8 random word pairs and the edge words.
-__device__ __forceinline__ double mt_random53(uint32_t w0, uint32_t w1) {
-    const uint32_t lo = ((w0 << 21) & 0xFC000000u) | (w1 >> 6);  // m bits 0..31
-    const uint32_t hi = w0 >> 11;                                  // m bits 32..52
-    const double E = __dsub_rn(__hiloint2double((int)(0x43300000u | (hi & 0xFFFFFu)), (int)lo), 4503599627370496.0);
-    const double top = __hiloint2double((hi >> 20) ? 0x3FE00000 : 0, 0);
-    return __fma_rn(E, 1.0 / 9007199254740992.0, top);
-}
-
 // Kinderman-Monahan acceptance of one normalvariate trial (Lib/random.py): u1 = random(), u2 =
 // 1 - random() from the tempered words (w0, w1), (w2, w3); z = NV_MAGICCONST * (u1 - 0.5) / u2;
 // accept iff z*z/4 <= -log(u2).  Decided in FP32 when the two sides are apart by more than 4x a
@@ -116,8 +103,8 @@ __device__ __forceinline__ bool km_accept(uint32_t w0, uint32_t w1_raw, uint32_t
     const float gap = zz - lg;
     const float aa = fabsf(a);
     if (c >= 2u && fabsf(gap) * aa > zz * (5.4e-7f + 5.6e-6f * aa) + (2.4e-6f + 1.5e-6f * lg) * aa) return gap < 0.0f;
-    const double u1 = mt_random53(w0, mt_temper(w1_raw));
-    const double u2d = __dsub_rn(1.0, mt_random53(w2, w3));
+    const double u1 = random53(w0, mt_temper(w1_raw));
+    const double u2d = __dsub_rn(1.0, random53(w2, w3));
     const double zx = __ddiv_rn(__dmul_rn(nv, __dsub_rn(u1, 0.5)), u2d);
     return __dmul_rn(__dmul_rn(zx, zx), 0.25) <= -log(u2d);  // z*z/4.0 (exact scaling)
 }

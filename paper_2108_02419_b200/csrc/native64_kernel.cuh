@@ -1,0 +1,451 @@
+// native64_kernel.cuh -- the throughput kernel at the reference's precision (BBE_MODE_NATIVE64):
+// Philox4x32-10 draws, FP64 race state, the reference's FP64 operations in the reference's order.
+//
+// Semantics (all /root/reference/pkg/src/racemarket/race.py):
+//   :46-47   uniform step  lo + (hi - lo) * random()            (random.py uniform, no FMA)
+//   :68-69   lognormal     scale * exp(mu + z * sigma)          (random.py lognormvariate/normalvariate)
+//   :93-96   responsiveness: early_mult if pos < breakpoint*L else late_mult
+//   :233-241 initial_state: prev[c] = (resp(0)*pref)*draw         [from_start]
+//   :244-264 _front_runner: nearest STILL-RACING rival STRICTLY ahead, gap = p_i - p_c, equal gaps ->
+//            lowest index; finished rivals never block
+//   :267-274 _resolve_step: free (no front, or gap > theta): (resp*pref)*draw; else resp*min(prev_c, prev_f)
+//   :287-320 advance_race: synchronous; p = pos + step; p == pos -> nextafter(p, +inf); finish at p >= L
+//   :323-332 _finish_order: sort by (finish_tick, L - pos, index)
+// Every race operation is an explicit IEEE double operation (__dadd_rn/__dmul_rn/__dsub_rn: no FMA
+// contraction), so given the same draws the kernel reproduces the reference's positions, finish ticks,
+// order and blocked counts bit for bit (tests/test_gpu_native64.py against the C oracle's Philox
+// draw source).  Only the word generator differs from the reference: Philox4x32-10 keyed by the
+// request seed with counter (tick / 2, competitor, global sim index), instead of a per-sim MT19937.
+//
+// Draws.  One Philox call per competitor per two ticks gives words (x, y, z, w).  A uniform step takes
+// random() = ((x >> 5) * 2^26 + (y >> 6)) * 2^-53 for the even tick and (z, w) for the odd one --
+// CPython's random_random() formula on Philox words, 53-bit resolution as the reference's.  A
+// lognormal step takes a Box-Muller normal from u1 = 1 - random(x, y), u2 = random(z, w) (the cosine
+// branch for the even tick, the sine branch for the odd one): the reference's Kinderman-Monahan loop
+// needs a variable number of words, which a counter-based stream replaces by the same N(0, 1) law.
+// Priming draws (run_race) use counter word 0 = 0xFFFFFFFF.
+//
+// Front runner.  A coarse 26-bit key per racing competitor: mantissa bits 51..26 of y = pos + C, where
+// the host picks C (bbe_sim.cu native64_frame) so that every racing position maps into one binade
+// [2^E, 2^(E+1)); the key is then a monotone (non-decreasing) function of the position.  Lanes publish
+// v = (key << 5) | lane to a shared-memory row and keep one wrapped minimum of v_r + ~v_c per rival
+// (one VIADDMNMX): the nearest rival in (key, index) order after c.  When all racing keys of a
+// segment are distinct, that rival is exactly the reference's front (keys order like positions).  Two
+// racing competitors sharing a key always show up: the lower of the two in (key, index) order finds
+// the other as its nearest, with an equal key.  Such a tick -- or a blocked lane whose front could be
+// a gap-rounding tie (p_f <= 2 gap, see exact_kernel.cuh) -- reruns the reference's own loop over
+// the segment's FP64 positions for the whole warp (rare: the key cell is (L - min pos) / 2^26 wide).
+//
+// Layout, sims, tallies: as native_kernel.cuh (segments of W lanes, K competitors per lane, persistent
+// grid with a claimed-sim counter, NT-tick blocks, shared-memory histograms flushed once per block).
+#pragma once
+
+#include "common.cuh"
+
+namespace bbe {
+
+#ifndef BBE_N64_MINBLOCKS_K1
+#define BBE_N64_MINBLOCKS_K1 5
+#endif
+#ifndef BBE_N64_MINBLOCKS_KN
+#define BBE_N64_MINBLOCKS_KN 4
+#endif
+
+// Box-Muller: two independent N(0, 1) from four words; u1 in (0, 1], u2 in [0, 1).
+__device__ __forceinline__ void normal_pair64(const U4& w, double& n0, double& n1) {
+    const double u1 = __dsub_rn(1.0, random53(w.x, w.y));
+    const double u2 = random53(w.z, w.w);
+    const double r = sqrt(__dmul_rn(-2.0, log(u1)));
+    double s, c;
+    sincospi(__dmul_rn(2.0, u2), &s, &c);
+    n0 = __dmul_rn(r, c);
+    n1 = __dmul_rn(r, s);
+}
+
+// K: competitors per lane; CH: key-row chunks of 4 words (SCAN only); SCAN: some theta > 0 (else
+// nobody can be blocked and the scan is omitted); LN: some lognormal competitor; NT: ticks per block.
+template <int K, int CH, bool SCAN, bool LN, int NT>
+__global__ void __launch_bounds__(kBlockThreads, K == 1 ? BBE_N64_MINBLOCKS_K1 : BBE_N64_MINBLOCKS_KN)
+native64_kernel(const LaunchArgs a) {
+    static_assert(NT % 2 == 0 && NT >= 2 && NT <= 16, "an even number of ticks per block");
+    extern __shared__ __align__(16) unsigned long long s_dyn[];
+    const TallyLayout TL{a.n, a.perms};
+    const int hist_len = TL.hist_len();
+    uint32_t* s_hist = reinterpret_cast<uint32_t*>(s_dyn);
+    for (int i = threadIdx.x; i < hist_len; i += blockDim.x) s_hist[i] = 0u;
+
+    constexpr int WP = 4 * CH;
+    constexpr int SLOT = native_slot_words(4, CH);
+    constexpr int PAR = K * SLOT;
+    const int n = a.n, W = a.W, S = a.S;
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int warp = threadIdx.x >> 5;
+    const int seg = lane / W;
+    const bool lane_on = seg < S;
+    const int base = lane_on ? seg * W : 0;
+    const int l = lane - seg * W;
+    const unsigned segmask = lane_on ? ((W == 32 ? 0xffffffffu : ((1u << W) - 1u)) << base) : 0u;
+
+    uint32_t* rows = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) + warp * native_warp_words(K, 4, CH);
+    if (SCAN)
+        for (int i = lane; i < native_warp_words(K, 4, CH); i += kWarp) rows[i] = 0u;
+    uint32_t* const wr = rows + (lane_on ? seg * WP + l : SLOT - 1);
+    const uint32_t* const rd = rows + (lane_on ? seg * WP : 0);
+    __syncthreads();
+
+    // ---- per-slot constants, FP64 (the host's double parameter block) ----
+    int cidx[K];
+    bool has[K], lognorm[K];
+    double lo[K], span[K], mu[K], sigma[K], scale[K], rpE[K], rpL[K], eE[K], eL[K], bp[K], th[K];
+    const double* P = a.P;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int c = k * W + l;
+        cidx[k] = c;
+        has[k] = lane_on && c < n;
+        const int cc = has[k] ? c : 0;
+        lo[k] = P[F_LO * n + cc];
+        span[k] = P[F_SPAN * n + cc];
+        mu[k] = P[F_MU * n + cc];
+        sigma[k] = P[F_SIGMA * n + cc];
+        scale[k] = P[F_SCALE * n + cc];
+        rpE[k] = P[F_RP_EARLY * n + cc];
+        rpL[k] = P[F_RP_LATE * n + cc];
+        eE[k] = P[F_EARLY * n + cc];
+        eL[k] = P[F_LATE * n + cc];
+        bp[k] = P[F_BP * n + cc];
+        th[k] = P[F_THETA * n + cc];
+        lognorm[k] = LN && has[k] && P[F_FAMILY * n + cc] != 0.0;
+    }
+    const double L = a.L;
+    const double C64 = a.key_c64;
+    const uint32_t cl = (uint32_t)l - a.key_sub64;  // v = funnel * 32 + cl = (key << 5) | l
+
+    // ---- segment bookkeeping ----
+    const int64_t segs_total = (int64_t)gridDim.x * kWarpsPerBlock * S;
+    const int64_t slot = (int64_t)(warp * S + seg) * gridDim.x + blockIdx.x;  // block-fastest (spread tail)
+    int64_t s = lane_on ? slot : a.n_sims;
+    int32_t rt = 0;
+    bool running = false;
+
+    double pos[K], prev[K];
+    int32_t fin[K];
+    bool started[K];
+    uint32_t blk_sim = 0;
+    unsigned long long ct_tot = 0, blk_tot = 0, n_div = 0;
+    int64_t first_div = INT64_MAX;
+
+    // the step draw of slot k for ticks 2h and 2h + 1 of the sim (counter word 0 = h)
+    auto draw_pair = [&](int k, uint32_t h, uint64_t gs, double& d0, double& d1) {
+        const U4 w = philox_rk(U4{h, (uint32_t)cidx[k], (uint32_t)gs, (uint32_t)(gs >> 32)}, a.rk);
+        d0 = __dadd_rn(lo[k], __dmul_rn(span[k], random53(w.x, w.y)));
+        d1 = __dadd_rn(lo[k], __dmul_rn(span[k], random53(w.z, w.w)));
+        if constexpr (LN) {
+            if (lognorm[k]) {
+                double z0, z1;
+                normal_pair64(w, z0, z1);
+                d0 = __dmul_rn(scale[k], exp(__dadd_rn(mu[k], __dmul_rn(z0, sigma[k]))));
+                d1 = __dmul_rn(scale[k], exp(__dadd_rn(mu[k], __dmul_rn(z1, sigma[k]))));
+            }
+        }
+    };
+
+    auto load_sim = [&](bool do_it) {
+        if (!do_it) return;
+        running = lane_on && s < a.n_sims;
+        rt = 0;
+        blk_sim = 0;
+        const uint64_t gs = (uint64_t)(a.sim_offset + s);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int cc = has[k] ? cidx[k] : 0;
+            pos[k] = P[F_POS0 * n + cc];
+            prev[k] = P[F_PREV0 * n + cc];
+            const bool pre_finished = P[F_FIN0 * n + cc] >= 0.0;
+            fin[k] = !(running && has[k]) ? kIdle : (pre_finished ? (int32_t)P[F_FINREL * n + cc] : kRacing);
+            started[k] = fin[k] == kRacing;
+            if (a.from_start && running && has[k]) {
+                // race.py:233-241: one free draw per competitor, resp at position 0
+                double d, d1;
+                draw_pair(k, 0xFFFFFFFFu, gs, d, d1);
+                prev[k] = __dmul_rn((0.0 < bp[k]) ? rpE[k] : rpL[k], d);
+            }
+        }
+    };
+    load_sim(true);
+
+    while (true) {
+        // ---------------- block boundary (as native_kernel.cuh) ----------------
+        if (rt >= a.limit) {
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                if (started[k] && fin[k] > a.limit) fin[k] = kDiverged;
+        }
+        bool live = false, dv = false;
+#pragma unroll
+        for (int k = 0; k < K; ++k) { live |= fin[k] == kRacing; dv |= fin[k] == kDiverged; }
+        const unsigned live_mask = __ballot_sync(0xffffffffu, live);
+        const bool seg_done = running && ((live_mask & segmask) == 0u);
+        if (__any_sync(0xffffffffu, seg_done)) {
+            const bool diverged = (__ballot_sync(0xffffffffu, dv) & segmask) != 0u;
+            // _finish_order (race.py:323-332): rank = #{i : (fin_i, L - pos_i, i) < (fin_c, L - pos_c, c)}
+            double lp[K];
+            int rank[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) { lp[k] = __dsub_rn(L, pos[k]); rank[k] = 0; }
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) {
+                for (int j = 0; j < W; ++j) {
+                    const int32_t fr = shfl(fin[kk], base + j);
+                    const double dr = shfl(lp[kk], base + j);
+                    const int i = kk * W + j;
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const bool less = (fr < fin[k]) | ((fr == fin[k]) & ((dr < lp[k]) | ((dr == lp[k]) & (i < cidx[k]))));
+                        rank[k] += (i < n && less) ? 1 : 0;
+                    }
+                }
+            }
+            uint32_t seg_blk = 0;
+            if (a.blocked)
+                for (int j = 0; j < W; ++j) seg_blk += shfl(blk_sim, base + j);
+            int64_t lehmer = 0;
+            if (a.perms) {
+                int cnt[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) cnt[k] = 0;
+#pragma unroll
+                for (int kk = 0; kk < K; ++kk)
+                    for (int j = 0; j < W; ++j) {
+                        const int rr = shfl(rank[kk], base + j);
+                        const int i = kk * W + j;
+#pragma unroll
+                        for (int k = 0; k < K; ++k) cnt[k] += (i < n && i < cidx[k] && rr > rank[k]) ? 1 : 0;
+                    }
+                int64_t term = 0;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    if (!has[k]) continue;
+                    int64_t f = 1;
+                    for (int q = 2; q <= n - 1 - rank[k]; ++q) f *= q;
+                    term += cnt[k] * f;
+                }
+                for (int j = 0; j < W; ++j) lehmer += shfl(term, base + j);
+            }
+            if (seg_done) {
+                const int64_t gs = a.sim_offset + s;
+                if (diverged) {
+                    if (l == 0) { n_div++; first_div = min(first_div, gs); }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        if (!has[k]) continue;
+                        if (rank[k] == 0) atomicAdd(&s_hist[TL.wins() + cidx[k]], 1u);
+                        atomicAdd(&s_hist[TL.ranks() + cidx[k] * n + rank[k]], 1u);
+                        if (a.group_wins && rank[k] == 0)
+                            atomicAdd(&a.group_wins[((a.group_base + s) / a.group_size) * n + cidx[k]], 1ull);
+                    }
+                    if (a.perms && l == 0) atomicAdd(&s_hist[TL.perms() + lehmer], 1u);
+                }
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    if (!has[k]) continue;
+                    if (started[k]) ct_tot += (fin[k] >= kDiverged) ? (uint32_t)min(rt, a.limit) : (uint32_t)fin[k];
+                    const int64_t o = s * n + cidx[k];
+                    if (a.winner && rank[k] == 0) a.winner[s] = diverged ? -1 : cidx[k];
+                    if (a.order) a.order[s * n + rank[k]] = cidx[k];
+                    if (a.finish_ticks) {
+                        const double f0 = P[F_FIN0 * n + cidx[k]];
+                        a.finish_ticks[o] = f0 >= 0.0 ? (int64_t)f0
+                                                      : (fin[k] >= kDiverged ? -1 : a.tick0 + (int64_t)fin[k]);
+                    }
+                    if (a.final_pos) a.final_pos[o] = pos[k];
+                }
+                if (l == 0 && a.blocked) a.blocked[s] = seg_blk;
+                blk_tot += blk_sim;
+            }
+            const int64_t next = claim_next_sim(seg_done, l == 0, base, segs_total, a.work);
+            if (seg_done) s = next;
+            load_sim(seg_done);
+        }
+        if (!__any_sync(0xffffffffu, running)) break;
+
+        const uint64_t gs = (uint64_t)(a.sim_offset + s);
+        double dr[K][2];
+
+        auto tick = [&](const int tj) {
+            bool racing[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) racing[k] = fin[k] == kRacing;
+
+            // ---- front runner (race.py:244-264) ----
+            double gap[K], pfpos[K];
+            bool ahead[K];
+            int fj[K], fk[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) { gap[k] = CUDART_INF; pfpos[k] = CUDART_INF; ahead[k] = false; fj[k] = 0; fk[k] = 0; }
+            if constexpr (SCAN) {
+                uint32_t v[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const double y = __dadd_rn(pos[k], C64);
+                    const uint32_t key = __funnelshift_r((uint32_t)__double2loint(y), (uint32_t)__double2hiint(y), 26);
+                    v[k] = key * 32u + cl;
+                    wr[(tj & 1) * PAR + k * SLOT] = racing[k] ? v[k] : 0u;
+                }
+                __syncwarp();
+                // per (own slot k, row kk) offset: t = v_r + nk is < 2^31 iff rival r follows c in
+                // (key, index) order -- rows below c's slot need a strictly larger key, c's own row a
+                // larger (key, lane), rows above a key at least as large
+                bool coll = false;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    uint32_t bestv = 0xffffffffu;
+                    int bestkk = 0;
+                    bool any = false;
+#pragma unroll
+                    for (int kk = 0; kk < K; ++kk) {
+                        const uint32_t nk = kk < k ? ~(v[k] | 31u) : (kk == k ? ~v[k] : 0u - (v[k] & ~31u));
+                        uint32_t b0 = 0xffffffffu, b1 = 0xffffffffu;
+                        const uint4* r4 = reinterpret_cast<const uint4*>(rd + (tj & 1) * PAR + kk * SLOT);
+#pragma unroll
+                        for (int c = 0; c < CH; ++c) {
+                            const uint4 q = r4[c];
+                            b0 = min(b0, q.x + nk);
+                            b1 = min(b1, q.y + nk);
+                            b0 = min(b0, q.z + nk);
+                            b1 = min(b1, q.w + nk);
+                        }
+                        const uint32_t t = min(b0, b1);
+                        const uint32_t vf = t - nk;  // the rival's own published value
+                        // rows in slot order; a later row replaces only with a strictly smaller key
+                        if (t < 0x80000000u && (!any || (vf >> 5) < (bestv >> 5))) { bestv = vf; bestkk = kk; any = true; }
+                    }
+                    ahead[k] = any;
+                    fk[k] = bestkk;
+                    fj[k] = (int)(bestv & 31u);
+                    coll |= racing[k] && any && (bestv >> 5) == (v[k] >> 5);
+                }
+                // the front's FP64 position
+#pragma unroll
+                for (int kk = 0; kk < K; ++kk) {
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const double pr = shfl(pos[kk], base + fj[k]);
+                        pfpos[k] = (K == 1 || fk[k] == kk) ? pr : pfpos[k];
+                    }
+                }
+                bool need_exact = coll;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    gap[k] = ahead[k] ? __dsub_rn(pfpos[k], pos[k]) : CUDART_INF;
+                    // a blocked lane whose front could be a gap-rounding tie (exact_kernel.cuh)
+                    need_exact |= racing[k] && ahead[k] && !(gap[k] > th[k]) && !(pfpos[k] > __dmul_rn(2.0, gap[k]));
+                }
+                if (__any_sync(0xffffffffu, need_exact)) {
+                    // the reference's loop (race.py:244-264) over the segment's start-of-tick positions
+                    double bg[K];
+#pragma unroll
+                    for (int k = 0; k < K; ++k) { bg[k] = CUDART_INF; ahead[k] = false; }
+#pragma unroll
+                    for (int kk = 0; kk < K; ++kk) {
+                        for (int j = 0; j < W; ++j) {
+                            const double pr = shfl(pos[kk], base + j);
+                            const bool rr = shfl((int)racing[kk], base + j) != 0;
+#pragma unroll
+                            for (int k = 0; k < K; ++k) {
+                                if (rr && pr > pos[k]) {
+                                    const double g = __dsub_rn(pr, pos[k]);
+                                    if (!ahead[k] || g < bg[k]) { bg[k] = g; ahead[k] = true; fk[k] = kk; fj[k] = j; }
+                                }
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int k = 0; k < K; ++k) gap[k] = bg[k];
+                }
+            }
+
+            // ---- step resolution (race.py:267-274) ----
+            bool fr[K], bl[K], any_bl = false;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                fr[k] = !SCAN || !ahead[k] || gap[k] > th[k];
+                bl[k] = racing[k] && !fr[k];
+                any_bl |= bl[k];
+            }
+            double pf[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) pf[k] = 0.0;
+            if constexpr (SCAN) {
+                if (__any_sync(0xffffffffu, any_bl)) {
+#pragma unroll
+                    for (int kk = 0; kk < K; ++kk) {
+#pragma unroll
+                        for (int k = 0; k < K; ++k) {
+                            const double pv = shfl(prev[kk], base + fj[k]);
+                            pf[k] = (K == 1 || fk[k] == kk) ? pv : pf[k];
+                        }
+                    }
+                }
+            }
+
+            // ---- synchronous update (race.py:299-320) ----
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const bool early = pos[k] < bp[k];
+                double step;
+                if (!SCAN || fr[k]) {
+                    step = __dmul_rn(early ? rpE[k] : rpL[k], dr[k][tj & 1]);
+                } else {
+                    const double m = (pf[k] < prev[k]) ? pf[k] : prev[k];  // Python min(prev_c, prev_front)
+                    step = __dmul_rn(early ? eE[k] : eL[k], m);
+                }
+                double p = __dadd_rn(pos[k], step);
+                if (p == pos[k]) p = nextafter(p, CUDART_INF);
+                const bool done = racing[k] && p >= L;
+                pos[k] = racing[k] ? p : pos[k];
+                prev[k] = step;  // a finished competitor's previous step is never read again
+                blk_sim += bl[k] ? 1u : 0u;
+                fin[k] = done ? rt + 1 : fin[k];
+            }
+            rt += 1;
+        };
+
+        if (SCAN) __syncwarp();  // key rows: the previous block's reads precede this block's writes
+#pragma unroll
+        for (int tj = 0; tj < NT; ++tj) {
+            if ((tj & 1) == 0) {
+#pragma unroll
+                for (int k = 0; k < K; ++k) draw_pair(k, (uint32_t)rt >> 1, gs, dr[k][0], dr[k][1]);
+            }
+            tick(tj);
+        }
+    }
+
+    // ---------------- flush ----------------
+    unsigned long long v_ct = ct_tot, v_blk = blk_tot, v_div = n_div;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        v_ct += __shfl_xor_sync(0xffffffffu, v_ct, off);
+        v_blk += __shfl_xor_sync(0xffffffffu, v_blk, off);
+        v_div += __shfl_xor_sync(0xffffffffu, v_div, off);
+        first_div = min(first_div, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)first_div, off));
+    }
+    const int ct_at = TL.ct();
+    if (lane == 0) {
+        if (v_ct) atomicAdd((unsigned long long*)&a.tally[ct_at + 0], v_ct);
+        if (v_blk) atomicAdd((unsigned long long*)&a.tally[ct_at + 1], v_blk);
+        if (v_div) atomicAdd((unsigned long long*)&a.tally[ct_at + 2], v_div);
+        if (first_div != INT64_MAX)
+            atomicMax((unsigned long long*)&a.tally[ct_at + 4], encode_first(first_div));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) release_work(a.work);
+    for (int i = threadIdx.x; i < hist_len; i += blockDim.x) {
+        const uint32_t v = s_hist[i];
+        if (v) atomicAdd((unsigned long long*)&a.tally[i], (unsigned long long)v);
+    }
+}
+
+}  // namespace bbe

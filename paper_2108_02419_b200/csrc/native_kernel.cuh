@@ -40,10 +40,6 @@ namespace bbe {
 #define BBE_NATIVE_MINBLOCKS_K1 7  // 64 registers -> 8 resident blocks of 4 warps
 #endif
 
-constexpr int32_t kRacing = 0x7fffffff;
-constexpr int32_t kDiverged = 0x7ffffffe;
-constexpr int32_t kIdle = 0x7ffffffd;  // slot without a competitor / segment without a sim
-
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -32,12 +32,12 @@ _LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
 LIB_PATH = os.environ.get("BBE_LIB") or os.path.join(_LIB_DIR, "libbbe_sim.so")  # BBE_LIB: A/B builds
 
 BBE_OK, BBE_EINVAL, BBE_EDIVERGED, BBE_EDRAWS, BBE_ECUDA, BBE_ENODEV = range(6)
-MODES = {"native": 0, "inject": 1, "mt": 2}
+MODES = {"native": 0, "inject": 1, "mt": 2, "native64": 3}
 MAX_COMPETITORS = 128
 MAX_PERM_COMPETITORS = 6
 M64 = (1 << 64) - 1
 
-ABI_VERSION = 4  # include/bbe_sim.h BBE_ABI_VERSION
+ABI_VERSION = 5  # include/bbe_sim.h BBE_ABI_VERSION
 
 EXPORTED_SYMBOLS = (
     "bbe_simulate",
@@ -169,7 +169,7 @@ def lib():
         L.bbe_rp_predict.argtypes = [_P(BbeRace), _P(BbeCompetitor), _P(BbeState), ctypes.c_int64, ctypes.c_int32,
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         L.bbe_rp_predict.restype = ctypes.c_int
-        L.bbe_prepare.argtypes = [_P(BbeRace), _P(BbeCompetitor), _P(BbeState), ctypes.c_int32,
+        L.bbe_prepare.argtypes = [_P(BbeRace), _P(BbeCompetitor), _P(BbeState), ctypes.c_int32, ctypes.c_int32,
                                   _P(ctypes.c_void_p)]
         L.bbe_prepare.restype = ctypes.c_int
         L.bbe_launch_prepared.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64,
@@ -186,10 +186,50 @@ def lib():
         L.bbe_device_count.restype = ctypes.c_int
         L.bbe_device_info.argtypes = [ctypes.c_int, ctypes.c_char_p, _P(ctypes.c_int32), _P(ctypes.c_int32)]
         L.bbe_device_info.restype = ctypes.c_int
+        # The entry points that write a CPython random.Random in place (bbe_rp_predict,
+        # bbe_mt_advance64, bbe_mt_advance64_many) go through a PyDLL handle: they run with the GIL
+        # held, so no other thread can use the generator mid-write (bbe_rp_predict drops the GIL in C
+        # for its GPU wait once all its writes are done).
+        G = ctypes.PyDLL(LIB_PATH)
+        for name in ("bbe_rp_predict", "bbe_mt_advance64", "bbe_mt_advance64_many"):
+            f = getattr(G, name)
+            f.argtypes, f.restype = getattr(L, name).argtypes, getattr(L, name).restype
+            setattr(L, name, f)
         if L.bbe_version() != ABI_VERSION:
             raise BackendUnavailable(f"{LIB_PATH} has ABI {L.bbe_version()}, expected {ABI_VERSION}: rebuild (make)")
         _lib = L
     return _lib
+
+
+_EXP_EXACT: bool | None = None
+
+
+def mt_exp_exact() -> bool:
+    """Whether MT mode reproduces the host libm's exp() bit for bit (bbe_mt_exp_exact): the library
+    found glibc's exp table in the loaded libm and verified it.  When False, lognormal steps in MT
+    mode may differ from the reference's in the last bit."""
+    global _EXP_EXACT
+    if _EXP_EXACT is None:
+        _EXP_EXACT = bool(lib().bbe_mt_exp_exact())
+    return _EXP_EXACT
+
+
+def check_mt_exact(config) -> None:
+    """Warn (once per config object) when an MT-mode call on a field with a lognormal runner cannot
+    be bit-exact because the libm exp table was not found."""
+    if mt_exp_exact() or not any(not hasattr(c.steps, "lo") for c in config.competitors):
+        return
+    if id(config) in _warned:
+        return
+    _warned.add(id(config))
+    import warnings
+
+    warnings.warn("mode='mt': glibc's exp table was not found in this process's libm, so lognormal steps "
+                  "use CUDA's exp and may differ from the reference in the last bit (bbe_mt_exp_exact() == 0)",
+                  RuntimeWarning, stacklevel=3)
+
+
+_warned: set = set()
 
 
 def last_error() -> str:
@@ -366,6 +406,8 @@ def simulate_batch(
     if mode not in MODES:
         raise ValueError(f"unknown mode {mode!r}")
     pk = pack_config(config)
+    if mode == "mt":
+        check_mt_exact(config)
     n = pk.n
     st, keep = pack_state(state, n)
     n_sims = int(n_sims)
@@ -462,6 +504,8 @@ def rp_predict_counts(state, config, d: int, state624_addr: int, pos_addr: int, 
     state at ``state624_addr`` (624 uint32) / ``pos_addr`` (int32), advanced in place (a CPython
     random.Random's own fields, agents.py); returns the counts as a list of ints."""
     pk = pack_config(config)
+    if mode == "mt":
+        check_mt_exact(config)
     st, keep = pack_state(state, pk.n)
     b = _pbufs
     rc = lib().bbe_rp_predict(ctypes.byref(pk.race), pk.comps, ctypes.byref(st), int(d), MODES[mode], state624_addr,
@@ -537,12 +581,15 @@ class DeviceLauncher:
     """Pre-packed race for repeated device-resident launches.
 
     Tallies are added into a caller-owned device buffer (e.g. a torch int64 CUDA tensor, passed by
-    ``data_ptr()``) on a caller stream (``torch.cuda.current_stream().cuda_stream``).  NATIVE launches
-    use a prepared race (``bbe_prepare``: parameters uploaded once, nothing copied per launch); MT
-    launches go through ``bbe_simulate_async``.
+    ``data_ptr()``) on a caller stream (``torch.cuda.current_stream().cuda_stream``).  NATIVE and
+    NATIVE64 launches use a prepared race (``bbe_prepare``: parameters uploaded once, nothing copied
+    per launch; ``native_mode`` picks which); MT launches go through ``bbe_simulate_async``.
     """
 
-    def __init__(self, state, config, *, lanes_per_slot: int = 0):
+    def __init__(self, state, config, *, lanes_per_slot: int = 0, native_mode: str = "native"):
+        if native_mode not in ("native", "native64"):
+            raise ValueError("native_mode: 'native' (FP32 state) or 'native64' (FP64 state)")
+        self.native_mode = native_mode
         self.pk = pack_config(config)
         self.st, self._keep = pack_state(state, self.pk.n)
         self.lanes_per_slot = int(lanes_per_slot)
@@ -557,7 +604,7 @@ class DeviceLauncher:
         if self._prep is None:
             h = ctypes.c_void_p()
             rc = lib().bbe_prepare(ctypes.byref(self.pk.race), self.pk.comps, ctypes.byref(self.st),
-                                   self.lanes_per_slot, ctypes.byref(h))
+                                   MODES[self.native_mode], self.lanes_per_slot, ctypes.byref(h))
             if rc != BBE_OK:
                 _raise(rc, BbeResult())
             self._prep = h
@@ -570,7 +617,9 @@ class DeviceLauncher:
 
     def launch(self, d_tally_ptr: int, n_sims: int, seed: int, *, sim_offset: int = 0, stream: int = 0,
                mode: str = "native") -> None:
-        if mode == "native":
+        if mode in ("native", "native64"):
+            if mode != self.native_mode:
+                raise ValueError(f"this launcher was prepared for {self.native_mode!r}")
             rc = lib().bbe_launch_prepared(self._prepared(), int(n_sims), int(sim_offset), int(seed) & M64,
                                            d_tally_ptr, stream)
             if rc != BBE_OK:

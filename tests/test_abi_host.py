@@ -28,7 +28,7 @@ def test_library_exports_every_header_symbol():
     assert declared and set(declared) == set(sim.EXPORTED_SYMBOLS)
     for name in declared:
         assert hasattr(L, name), name
-    assert L.bbe_version() == sim.ABI_VERSION == 4
+    assert L.bbe_version() == sim.ABI_VERSION == 5
 
 
 def test_tally_layout():
@@ -130,3 +130,48 @@ def test_batched_stream_advance_matches_sequential_getrandbits():
         else:
             assert o is None
     assert all(x.getstate() == y.getstate() for x, y in zip(a, b))
+
+
+def test_generator_writes_hold_the_gil():
+    """bbe_mt_advance64 writes a random.Random in place; bound through ctypes.PyDLL it holds the GIL,
+    so a second thread using the same generator never sees (or makes) a half-written state.  Every
+    operation consumes whole MT words, so whatever the interleaving the final state is the start
+    advanced by the total number of words drawn."""
+    import threading
+
+    rng = random.Random(2021)
+    calls_a, calls_b = 300, 20000
+    d = 3000
+
+    def a():
+        for _ in range(calls_a):
+            dry_run_seeds(rng, d, want=False)
+
+    def b():
+        for _ in range(calls_b):
+            rng.random()
+
+    ta, tb = threading.Thread(target=a), threading.Thread(target=b)
+    ta.start(), tb.start()
+    ta.join(), tb.join()
+    ref = random.Random(2021)
+    for _ in range(calls_a * d * 2 + calls_b * 2):
+        ref.getrandbits(32)
+    assert rng.getstate() == ref.getstate()
+
+
+def test_duplicate_generators_advance_in_list_order():
+    """bbe_mt_advance64_many with one generator listed several times: advanced once per listing, in
+    order, by a single thread (no two threads write the same state)."""
+    from paper_2108_02419_b200.agents import dry_run_seeds_many
+
+    g1, g2 = random.Random(5), random.Random(6)
+    rngs = [g1, g2, g1, g1, g2] * 8
+    ds = [70000, 3, 70000, 5, 70000] * 8
+    outs = dry_run_seeds_many(rngs, ds, [2] * len(rngs))
+    r1, r2 = random.Random(5), random.Random(6)
+    for r, d, o in zip(rngs, ds, outs):
+        ref = r1 if r is g1 else r2
+        vals = [ref.getrandbits(64) for _ in range(d)]
+        assert [int(x) for x in o] == vals[:2]
+    assert g1.getstate() == r1.getstate() and g2.getstate() == r2.getstate()
