@@ -3,25 +3,33 @@
 In the reference every RP/RB wake runs ``rp_predict`` on its own: d sequential ``simulate_from``
 calls (session.py:240-267 -> agents.py:345-362 -> agents.py:153-166).  Predictions depend only on
 the live race state (never on the order book), and each bettor's dry-run seeds come from its own
-private stream.  So all predictions a tick needs can run as ONE launch:
+private stream.  So all predictions a wake round needs can run as ONE launch:
 concatenate every requesting bettor's d seeds -- drawn from each bettor's stream in its own order,
 exactly as ``rp_predict`` would -- simulate them together, and split the per-sim winners back per
 bettor.  In MT mode every bettor then gets exactly the probabilities (and the stream position) the
-reference would have produced; the exchange loop stays on the host and unchanged.
+reference would have produced.
 
-``run_dry_run_session`` drives the C4 workload without the exchange: the live race (the reference's
-own race for ``derive_seed(master, "race")``, recorded tick by tick on the GPU in MT mode), the
-jittered wake schedule of session.py:104-121, and one batched prediction launch per tick.
+``run_session`` / ``GpuSession`` is the full BBE session (C4): the reference's own session loop,
+exchange, matching and settlement (racemarket.session._Session, session.py:124-340) with the
+RP/RB predictions of every ``_process_wakes`` call served from batched launches.  The event log is
+the reference's, byte for byte, in MT mode (tests/test_session_exchange.py).
+
+``run_dry_run_session`` drives the prediction side of C4 alone (no exchange): the live race, the
+jittered wake schedule of session.py:104-121, and one batched prediction launch per wake round.
 """
 
 from __future__ import annotations
 
+import os
+import random
+import sys
 import time
+from collections import deque
 from dataclasses import dataclass
 
 import numpy as np
 
-from .agents import dry_run_seeds_many
+from .agents import dry_run_seeds, dry_run_seeds_many, rb_bettor_predict, rb_weighted, rp_bettor_predict
 from .race import RaceState
 from .seeding import derive_seed, spawn_rng
 from .sim import run_race, simulate_batch_begin
@@ -158,9 +166,11 @@ def run_dry_run_session(config, n_agents: int, d: int, master_seed: int, *, open
     each race tick advances the clock by dt and processes the wakes due by then (one launch per
     batch of wakes that share a race state).  Returns every prediction and the end-to-end rate.
 
-    ``on_batch(predictions)`` -- the host's use of a batch (the exchange loop's decisions and order
-    book in a full session) -- runs while the NEXT batch is already on the GPU: the race never depends
-    on the market (session.py:282), so predictions run one batch ahead of the host.
+    Every bettor is an RP bettor whose decision draws from its stream only on an exact probability
+    tie (``_pick``'s randrange, agents.py:304-310); that draw is made after each batch, so every
+    stream stays where the reference's session leaves it.  ``on_batch(predictions)`` is called after
+    each batch (it must not draw from the bettors' streams).  ``run_session`` is the full session
+    with the exchange.
     """
     states = live_states(config, master_seed)
     n_ticks = len(states) - 1
@@ -176,9 +186,8 @@ def run_dry_run_session(config, n_agents: int, d: int, master_seed: int, *, open
                 due.append((next_wake[i], i))
                 next_wake[i] += reevaluate_every
         due.sort()
-        # a bettor waking k times in one batch needs its k-th prediction after its (k-1)-th decision;
-        # RP decisions draw from the stream only on ties (agents.py:304-310), which this driver does
-        # not model, so rounds are batched: round r = every bettor's r-th due wake.
+        # a bettor waking k times in one batch needs its k-th prediction after its (k-1)-th decision,
+        # so rounds are batched: round r = every bettor's r-th due wake.
         rounds: list[list[tuple[float, int]]] = []
         seen: dict[int, int] = {}
         for t, i in due:
@@ -190,28 +199,195 @@ def run_dry_run_session(config, n_agents: int, d: int, master_seed: int, *, open
         return [(state, rnd) for rnd in rounds]
 
     # the live race is fixed in advance (session.py:282 uses only rng_race), so the whole sequence of
-    # (race state, wake round) batches is known: prepare batch i+1 on the host while batch i runs
+    # (race state, wake round) batches is known up front.  Wakes stop once betting closes: at
+    # close_rank finishers (session.py:294-311).
+    close_rank = config.betting_close.close_rank(len(config.competitors))
     work = batches(opening_period, states[0])
     for tick in range(1, n_ticks + 1):
-        if all(f is not None for f in states[tick].finish_ticks):
-            break  # betting closes when the last runner finishes (BettingClose.last, session.py:294-311)
+        if sum(f is not None for f in states[tick].finish_ticks) >= close_rank:
+            break
         work.extend(batches(opening_period + tick * config.dt, states[tick]))
 
     t0 = time.perf_counter()
-    prev = None  # (batch, prepared, pending) in flight
     for state, rnd in work:
+        # a bettor's next seeds are drawn only after its previous decision's draws (the RP tie-break
+        # randrange, agents.py:304-310), so a batch is prepared once the one before it is decided
         prep = disp.prepare([DryRunRequest(rngs[i], d) for _, i in rnd])
-        done = None
-        if prev is not None:
-            done = [(t, i, p) for (t, i), p in zip(prev[0], disp.finish(prev[2], prev[1]))]
-            preds.extend(done)
-        prev = (rnd, prep, disp.launch(state, prep))
-        if done is not None and on_batch is not None:
-            on_batch(done)  # overlaps the batch just launched
-    if prev is not None:
-        done = [(t, i, p) for (t, i), p in zip(prev[0], disp.finish(prev[2], prev[1]))]
+        done = [(t, i, p) for (t, i), p in zip(rnd, disp.finish(disp.launch(state, prep), prep))]
+        for _, i, p in done:
+            decide_draws(rngs[i], p, None)
         preds.extend(done)
         if on_batch is not None:
             on_batch(done)
     seconds = time.perf_counter() - t0
     return DryRunSessionResult(preds, disp.launches, disp.sims, seconds, n_ticks)
+
+
+def decide_draws(rng, probs, max_stake: int | None) -> None:
+    """The draws ``Bettor.decide`` makes from the bettor's stream after its prediction
+    (agents.py:334-342): ``_pick``'s ``randrange`` over exactly tied maxima (agents.py:304-310), then
+    for an RB bettor the stake ``randint(1, max_stake)`` (agents.py:406-408).  Neither depends on
+    the order book, so the stream position after a decision is a function of the prediction alone.
+    """
+    best = max(probs)
+    k = sum(1 for p in probs if p == best)
+    if k > 1:
+        rng.randrange(k)
+    if max_stake is not None:
+        rng.randint(1, max_stake)
+
+
+# -- the full session: the reference's exchange loop with batched GPU predictions --------------------
+
+
+def import_racemarket():
+    """The reference package, whose session loop, exchange and agents run on the host unchanged.
+
+    Imported as installed; else from ``$RACEMARKET_PATH`` or this checkout's ``baseline/_ref`` (the
+    offline install of /root/reference)."""
+    try:
+        import racemarket.session  # noqa: F401
+    except ImportError:
+        here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        for p in (os.environ.get("RACEMARKET_PATH"), os.path.join(here, "baseline", "_ref")):
+            if p and os.path.isdir(os.path.join(p, "racemarket")) and p not in sys.path:
+                sys.path.append(p)
+        import racemarket.session  # noqa: F401
+    import racemarket
+
+    return racemarket
+
+
+@dataclass
+class SessionStats:
+    launches: int = 0          # batched prediction launches
+    sims: int = 0              # dry runs simulated
+    predictions: int = 0       # RP/RB predictions served from a batch
+    fallbacks: int = 0         # predictions computed on their own (stream not where planned)
+    rounds: int = 0            # wake rounds
+    predict_seconds: float = 0.0  # host wall time inside the batched predictions (seeds + GPU + tally)
+    seconds: float = 0.0          # wall time of the whole session run
+
+
+def make_gpu_session(config, *, mode: str = "mt", predictor=None):
+    """A ``racemarket.session._Session`` whose RP/RB bettors' predictions come from batched launches.
+
+    ``predictor.predict_many(state, requests)`` serves a round (default: ``DryRunDispatcher(race,
+    mode)``).  Everything else -- wake schedule, observations, ``decide``, the exchange, matching,
+    close, settlement, the event log -- is the reference's own code (session.py:124-340).
+    """
+    rm = import_racemarket()
+    from racemarket.agents import RBBettor, RPBettor
+
+    class GpuSession(rm.session._Session):
+        """session.py:_Session with ``_process_wakes`` (session.py:258-267) prefetching predictions.
+
+        For one ``_process_wakes(until)`` call the due wakes are computed exactly as the reference
+        computes them (on a copy of ``next_wake``).  RP/RB wakes are grouped into rounds -- round r
+        holds every bettor's r-th due wake -- and each round is ONE batched launch from the race state
+        of this call (the race does not move inside a call).  Round r's seeds come from a clone of
+        the bettor's stream advanced past its earlier predictions and decisions (``decide_draws``).
+        Then the reference's own loop runs the wakes in (time, index) order; each RP/RB ``predict``
+        pops its planned probabilities after checking that the bettor's real stream is exactly
+        where the plan drew the seeds, and advances it by d ``getrandbits(64)`` as ``rp_predict``
+        does (agents.py:164).  A stream found anywhere else is predicted on its own (GPU, same
+        mode), so the result never depends on the plan being right.
+        """
+
+        def __init__(self, cfg):
+            super().__init__(cfg)
+            self.bbe_mode = mode
+            self.predictor = predictor if predictor is not None else DryRunDispatcher(cfg.race, mode)
+            self.stats = SessionStats()
+            self._plans: dict[int, deque] = {}
+            self._batched: dict[int, object] = {}
+            for i, a in enumerate(self.agents):
+                if type(a) in (RPBettor, RBBettor) and type(a.rng) is random.Random:
+                    self._batched[i] = a
+                    self._plans[i] = deque()
+                    a.predict = self._hook(i, a)  # instance attribute: shadows the class method
+
+        def _hook(self, i, agent):
+            rb = isinstance(agent, RBBettor)
+            d = agent.params.d
+
+            def predict(obs):
+                q = self._plans[i]
+                if q:
+                    expect, probs = q.popleft()
+                    if agent.rng.getstate() == expect:
+                        dry_run_seeds(agent.rng, d, want=False)
+                        return probs
+                    q.clear()  # the stream moved off the plan: later planned wakes are void too
+                self.stats.fallbacks += 1
+                if rb:
+                    return rb_bettor_predict(obs, self.race_cfg, d, agent.params.gamma, agent.rng, mode=self.bbe_mode)
+                return rp_bettor_predict(obs, self.race_cfg, d, agent.rng, mode=self.bbe_mode)
+
+            return predict
+
+        def _process_wakes(self, until: float) -> None:
+            nw = list(self.next_wake)
+            due = []
+            for i, agent in enumerate(self.agents):  # session.py:259-264, on a copy
+                period = agent.params.reevaluate_every
+                while nw[i] <= until:
+                    due.append((nw[i], i))
+                    nw[i] += period
+            due.sort()
+            self._prefetch(due)
+            super()._process_wakes(until)
+
+        def _prefetch(self, due) -> None:
+            count: dict[int, int] = {}
+            for _, i in due:
+                if i in self._batched:
+                    count[i] = count.get(i, 0) + 1
+            if not count:
+                return
+            positions, finish_ticks, history = self._race_view()
+            state = RaceState(self.state.tick, list(positions), [h[-1] if h else 0.0 for h in history],
+                              list(finish_ticks))
+            virt = {}
+            for i in count:
+                v = random.Random()
+                v.setstate(self._batched[i].rng.getstate())
+                virt[i] = v
+            t0 = time.perf_counter()
+            for r in range(max(count.values())):
+                members = [i for i in count if count[i] > r]
+                expects = [virt[i].getstate() for i in members]
+                reqs = [DryRunRequest(virt[i], self._batched[i].params.d) for i in members]
+                before = (getattr(self.predictor, "launches", 0), getattr(self.predictor, "sims", 0))
+                probs = self.predictor.predict_many(state, reqs)
+                self.stats.launches += getattr(self.predictor, "launches", 0) - before[0]
+                self.stats.sims += getattr(self.predictor, "sims", 0) - before[1]
+                self.stats.rounds += 1
+                for i, e, p in zip(members, expects, probs):
+                    a = self._batched[i]
+                    rb = isinstance(a, RBBettor)
+                    out = rb_weighted(p, a.params.gamma) if rb else tuple(p)
+                    self._plans[i].append((e, out))
+                    decide_draws(virt[i], out, a.params.max_stake if rb else None)
+                self.stats.predictions += len(members)
+            self.stats.predict_seconds += time.perf_counter() - t0
+
+    return GpuSession(config)
+
+
+def run_session(config, *, mode: str = "mt", predictor=None):
+    """``racemarket.session.run_session`` (session.py:345-347) with batched GPU predictions.
+
+    mode="mt": every prediction, and so the whole event log, settlement and balances, equals the
+    reference's; "native64"/"native": Philox dry runs (statistically equal predictions).  Returns
+    the reference's ``SessionResult``."""
+    return run_session_with_stats(config, mode=mode, predictor=predictor)[0]
+
+
+def run_session_with_stats(config, *, mode: str = "mt", predictor=None):
+    """``run_session`` plus the dispatch counters (``SessionStats``) and the wall time of ``run``."""
+    s = make_gpu_session(config, mode=mode, predictor=predictor)
+    t0 = time.perf_counter()
+    res = s.run()
+    s.stats.seconds = time.perf_counter() - t0
+    return res, s.stats

@@ -308,7 +308,9 @@ def test_extreme_step_laws_terminate_or_diverge_cleanly(mode):
 @pytest.mark.parametrize("mode", ["mt", "native"])
 def test_rp_predict_c_entry_errors(mode):
     """bbe_rp_predict: a dry run past tick_limit raises with the first failing dry-run index (both MT
-    halves included) and still advances the bettor's stream by d; bad arguments are rejected."""
+    halves included) and leaves the bettor's stream where the reference leaves it -- advanced by
+    first_diverged + 1 draws, as rp_predict raises inside that dry run (agents.py:164); bad arguments
+    are rejected."""
     import ctypes
     import random
 
@@ -322,7 +324,7 @@ def test_rp_predict_c_entry_errors(mode):
     with pytest.raises(sim.SimDivergedError) as e:
         rp_predict(st, cfg, d, rng, mode=mode)
     assert e.value.sim_index == 0
-    for _ in range(d):
+    for _ in range(e.value.sim_index + 1):
         twin.getrandbits(64)
     assert rng.getstate() == twin.getstate()
     pk = sim.pack_config(cfg)

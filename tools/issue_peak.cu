@@ -16,11 +16,14 @@ template <int OP>
 __global__ void __launch_bounds__(256) chains(uint32_t* out, uint32_t seed) {
     uint32_t a[8];
     float f[8];
+    double g[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         a[i] = seed * (threadIdx.x + 1) + i;
         f[i] = (float)a[i] * 1e-9f;
+        g[i] = (double)a[i] * 1e-9;
     }
+    const double gb = 1.0000000001, gc = 1e-12;
     const uint32_t b = seed ^ 0x9E3779B9u, c = seed * 3u + 7u;
     const float fb = 1.0000001f, fc = 1e-7f;
     for (int it = 0; it < kIters; ++it) {
@@ -31,11 +34,15 @@ __global__ void __launch_bounds__(256) chains(uint32_t* out, uint32_t seed) {
             if constexpr (OP == 2) a[i] = (a[i] ^ b) & (c | a[i]);               // LOP3
             if constexpr (OP == 3) a[i] = min(a[i] + b, c + (uint32_t)i);        // VIADDMNMX
             if constexpr (OP == 4) a[i] = a[i] < b + (uint32_t)i ? a[i] + 1u : a[i] - c;  // ISETP+SEL
+            if constexpr (OP == 5) g[i] = fma(g[i], gb, gc);                     // DFMA
+            if constexpr (OP == 6) g[i] = __dadd_rn(g[i], gc);                   // DADD
+            if constexpr (OP == 7) g[i] = __dmul_rn(g[i], gb);                   // DMUL
+            if constexpr (OP == 8) g[i] = g[i] < gb ? __dadd_rn(g[i], gc) : __dmul_rn(g[i], gc);  // DSETP+DADD/DMUL
         }
     }
     uint32_t s = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) s += a[i] + __float_as_uint(f[i]);
+    for (int i = 0; i < 8; ++i) s += a[i] + __float_as_uint(f[i]) + (uint32_t)__double2loint(g[i]);
     if (s == 0x12345678u) out[0] = s;  // keep the chains alive
 }
 
@@ -74,5 +81,9 @@ int main() {
     run<2>("LOP3 (alu pipe)", sms, mhz, 1);
     run<3>("VIADDMNMX (alu pipe)", sms, mhz, 1);
     run<4>("ISETP + SEL (alu pipe)", sms, mhz, 2);
+    run<5>("DFMA (fp64)", sms, mhz, 1);
+    run<6>("DADD (fp64)", sms, mhz, 1);
+    run<7>("DMUL (fp64)", sms, mhz, 1);
+    run<8>("DSETP + DADD|DMUL (fp64)", sms, mhz, 2);
     return 0;
 }
