@@ -343,7 +343,42 @@ struct NativeFrame {
     int key_bits;
     double c64;      // NATIVE64: key of pos = mantissa bits 51..26 of pos + c64 (native64_frame)
     uint32_t sub64;  // NATIVE64: the exponent bit the key window drags in, << 31
+    int flags64;     // NATIVE64: kN64RespVar | kN64Guard (native64_flags)
 };
+
+// NATIVE64 host flags (native64_kernel.cuh).  kN64RespVar: some competitor has early != late
+// multiplier (so the per-tick breakpoint test matters).  kN64Guard: unless every step the race can
+// take provably exceeds 2^-52 * B, B = the largest |position| a racing competitor can start a tick
+// at (max(L, |initial positions|)), fl(pos + step) == pos is possible and the nextafter guard
+// (race.py:310-313) stays.  Step lower bounds: free steps (resp * pref) * draw with draw >= lo
+// (uniform: lo + span * r, r >= 0) or >= scale * exp(mu - 8.58 sigma) (Box-Muller |z| <= 8.572 for
+// u1 >= 2^-53), halved for rounding; blocked steps resp * min(prev_c, prev_front) can shrink without
+// bound when a multiplier is < 1, else stay >= the smallest free step and initial previous step.
+int native64_flags(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st) {
+    const int n = race->n;
+    int fl = 0;
+    bool scan = false, small_mult = false;
+    double min_free = INFINITY, min_prev = INFINITY, B = std::fabs(race->track_length);
+    for (int c = 0; c < n; ++c) {
+        const bbe_competitor& p = comps[c];
+        const double rpE = p.early_mult * p.pref_factor, rpL = p.late_mult * p.pref_factor;
+        if (!(rpE == rpL) || !(p.early_mult == p.late_mult)) fl |= kN64RespVar;
+        const bool racing = st->from_start || st->finish_ticks[c] < 0;
+        if (!racing) continue;
+        scan = scan || !(p.theta <= 0.0);
+        small_mult = small_mult || !(p.early_mult >= 1.0) || !(p.late_mult >= 1.0);
+        const double dmin = p.family == BBE_FAMILY_LOGNORMAL ? p.scale * std::exp(p.mu - 8.58 * p.sigma) : p.lo;
+        min_free = std::min(min_free, 0.5 * std::min(rpE, rpL) * dmin);
+        if (!st->from_start) {
+            min_prev = std::min(min_prev, st->prev_steps[c]);
+            B = std::max(B, std::fabs(st->positions[c]));
+        }
+    }
+    double step_min = min_free;
+    if (scan) step_min = small_mult ? 0.0 : std::min(min_free, min_prev);
+    if (!(step_min > std::ldexp(B, -52))) fl |= kN64Guard;
+    return fl;
+}
 
 // NATIVE64 coarse front-runner key (native64_kernel.cuh): every racing position p -- from the
 // smallest racing start position `base` up to hi = max(L, largest racing start position) -- maps to
@@ -417,9 +452,10 @@ NativeFrame native_frame(const bbe_race* race, const bbe_state* st, int W) {
     return fr;
 }
 
-NativeFrame native_frames(const bbe_race* race, const bbe_state* st, int W) {
+NativeFrame native_frames(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, int W) {
     NativeFrame fr = native_frame(race, st, W);
     native64_frame(race, st, &fr);
+    fr.flags64 = native64_flags(race, comps, st);
     return fr;
 }
 
@@ -559,6 +595,7 @@ int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, co
     pl->smem = smem_bytes(kmode, (TL.hist_len() + 1) & ~1, pl->K, pl->S, pl->WP);
     if (rq->mode == BBE_MODE_NATIVE64) {
         pl->NT = pick_ticks64(scan, expected_ticks(race, comps, st));
+        pl->smem = smem_bytes(kmode, (TL.hist_len() + 1) & ~1, pl->K, pl->S, scan ? pl->WP : 0, pl->NT);
         pl->fn = scan ? pick_native64_scan(pl->K, pl->CH, ln) : pick_native64_free(pl->K, ln, pl->NT);
     } else {
         pl->NT = rq->mode == BBE_MODE_NATIVE ? pick_ticks(pl->K, scan, expected_ticks(race, comps, st)) : 4;
@@ -946,6 +983,7 @@ static int build_args(const Plan& pl, const bbe_race* race, const bbe_state* st,
     a.key_nmul = 0u - a.key_mul;
     a.key_c64 = fr.c64;
     a.key_sub64 = fr.sub64;
+    a.n64_flags = fr.flags64;
     philox_round_keys(rq->seed, a.rk);
     a.n = race->n;
     a.W = pl.W;
@@ -1009,7 +1047,7 @@ int bbe_simulate_begin(const bbe_race* race, const bbe_competitor* comps, const 
     BBE_CK(ctx->d_params.ensure(pbytes + tbytes + gbytes));
     BBE_CK(ctx->h_tally.ensure(tbytes));
     pack_params(race, comps, st, (double*)ctx->h_params.p);
-    const NativeFrame fr = native_frames(race, st, pl.W);
+    const NativeFrame fr = native_frames(race, comps, st, pl.W);
     pack_params_f32(race, comps, st, (double*)ctx->h_params.p, fr);
     std::memset((char*)ctx->h_params.p + pbytes, 0, tbytes + gbytes);
     uint64_t* const d_tally = (uint64_t*)((char*)ctx->d_params.p + pbytes);
@@ -1228,7 +1266,7 @@ static int enqueue_tally(DevCtx* ctx, const bbe_race* race, const bbe_competitor
     BBE_CK(ctx->d_params.ensure(pbytes + tbytes));
     BBE_CK(ctx->h_tally.ensure(tbytes));
     pack_params(race, comps, st, (double*)ctx->h_params.p);
-    const NativeFrame fr = native_frames(race, st, pl.W);
+    const NativeFrame fr = native_frames(race, comps, st, pl.W);
     pack_params_f32(race, comps, st, (double*)ctx->h_params.p, fr);
     std::memset((char*)ctx->h_params.p + pbytes, 0, tbytes);
     uint64_t* const d_tally = (uint64_t*)((char*)ctx->d_params.p + pbytes);
@@ -1545,7 +1583,7 @@ int bbe_simulate_async(const bbe_race* race, const bbe_competitor* comps, const 
     BBE_CK(ctx->d_params.ensure(pbytes));
     BBE_CK(cudaEventSynchronize(ctx->ev1));  // previous async launch on this ctx has read its params
     pack_params(race, comps, st, (double*)ctx->h_params.p);
-    const NativeFrame fr = native_frames(race, st, pl.W);
+    const NativeFrame fr = native_frames(race, comps, st, pl.W);
     pack_params_f32(race, comps, st, (double*)ctx->h_params.p, fr);
     BBE_CK(cudaMemcpyAsync(ctx->d_params.p, ctx->h_params.p, pbytes, cudaMemcpyHostToDevice, s));
     LaunchArgs a;
@@ -1609,7 +1647,7 @@ int bbe_prepare(const bbe_race* race, const bbe_competitor* comps, const bbe_sta
     p->race = *race;
     p->tick = st->from_start ? 0 : st->tick;
     p->from_start = st->from_start;
-    p->fr = native_frames(race, st, p->pl.W);
+    p->fr = native_frames(race, comps, st, p->pl.W);
     const size_t pbytes = param_bytes(race->n);
     std::vector<double> h(pbytes / sizeof(double) + 1);
     pack_params(race, comps, st, h.data());

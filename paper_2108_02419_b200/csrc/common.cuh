@@ -67,6 +67,7 @@ struct LaunchArgs {
     int key_bits;       // NATIVE: index bits packed under the key
     double key_c64;       // NATIVE64: coarse front-runner key = mantissa bits 51..26 of (pos + key_c64)
     uint32_t key_sub64;   //   (the constant exponent bit the 32-bit key window drags in, subtracted)
+    int n64_flags;        // NATIVE64: kN64RespVar | kN64Guard (bbe_sim.cu native64_flags)
     uint32_t key_mul, key_nmul;  // NATIVE: 2^key_bits and -2^key_bits (runtime values: IMAD, not shifts)
     int n, W, S, WP, from_start, scan, perms;
     double L;
@@ -112,12 +113,16 @@ constexpr int kMtMaxTrials = 8;
 __host__ __device__ constexpr int mt_side_words(int K) { return 128 * K + 4 * kMtMaxTrials; }
 __host__ __device__ constexpr int mt_seg_words(int K) { return kMtWords + mt_side_words(K); }
 constexpr int kXSlot = 66;         // exact modes: doubles per position row (S*round_up(W,2) <= 64, + pad)
-__host__ __device__ inline size_t smem_bytes(int mode, int hist_len_even, int K, int S, int WP) {
+// NATIVE64 host flags
+constexpr int kN64RespVar = 1;  // some competitor's early and late multipliers differ
+constexpr int kN64Guard = 2;    // fl(pos + step) == pos is possible: keep the nextafter guard
+__host__ __device__ inline size_t smem_bytes(int mode, int hist_len_even, int K, int S, int WP, int nt64 = 0) {
     size_t b = (size_t)hist_len_even * 8;
-    if (mode == NATIVE || mode == NATIVE64) {
+    if (mode == NATIVE || (mode == NATIVE64 && WP > 0)) {  // NATIVE64 scan-free kernels: no key rows (WP 0)
         const int vec = (WP % 4) ? 2 : 4;  // the host rounds W up to 2 (VEC 2) or 4 (VEC 4)
         b += (size_t)kWarpsPerBlock * native_warp_words(K, vec, WP / vec) * 4;
     }
+    if (mode == NATIVE64) b += (size_t)kWarpsPerBlock * K * nt64 * kWarp * 8;  // staged draws
     if (mode == MT) b += (size_t)kWarpsPerBlock * S * mt_seg_words(K) * 4;
     if (mode == INJECT || mode == MT) b += (size_t)kWarpsPerBlock * 2 * K * kXSlot * 8;
     if (mode == MT) b += (size_t)kWarpsPerBlock * kWarp * 4;  // per-warp lognormal offsets (trial pass)

@@ -36,6 +36,18 @@
 // a gap-rounding tie (p_f <= 2 gap, see exact_kernel.cuh) -- reruns the reference's own loop over
 // the segment's FP64 positions for the whole warp (rare: the key cell is (L - min pos) / 2^26 wide).
 //
+// Draw staging.  At every NT-tick block boundary each lane computes its slots' NT step draws (Philox,
+// the uniform/lognormal transform) in a rolled loop and parks them in a per-lane shared-memory column;
+// the tick loop then reads one double per slot per tick.  The transcendental lognormal code and the
+// Philox rounds thus appear once in the binary instead of once per unrolled tick (ncu round 2: with
+// them inlined per tick the derby20 kernel spent 76 % of its stall samples on instruction fetch).
+//
+// Host flags (bbe_sim.cu native64_flags): kN64RespVar -- some competitor's early and late multipliers
+// differ, so the responsiveness test `pos < breakpoint*L` (race.py:93-96) runs per tick; without it the
+// early value is used (bit-identical, the two are equal).  kN64Guard -- the `p == pos -> nextafter`
+// guard (race.py:310-313) can fire: off when every possible step exceeds 2^-52 of the largest
+// |position|, where fl(pos + step) == pos is impossible.
+//
 // Layout, sims, tallies: as native_kernel.cuh (segments of W lanes, K competitors per lane, persistent
 // grid with a claimed-sim counter, NT-tick blocks, shared-memory histograms flushed once per block).
 #pragma once
@@ -43,6 +55,11 @@
 #include "common.cuh"
 
 namespace bbe {
+
+template <bool B>
+struct CBool {
+    static constexpr bool value = B;
+};
 
 #ifndef BBE_N64_MINBLOCKS_K1
 #define BBE_N64_MINBLOCKS_K1 5
@@ -86,11 +103,16 @@ native64_kernel(const LaunchArgs a) {
     const int l = lane - seg * W;
     const unsigned segmask = lane_on ? ((W == 32 ? 0xffffffffu : ((1u << W) - 1u)) << base) : 0u;
 
-    uint32_t* rows = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) + warp * native_warp_words(K, 4, CH);
+    // key rows (SCAN only: the scan-free kernels have none -- host smem_bytes with WP = 0)
+    constexpr int ROWW = SCAN ? native_warp_words(K, 4, CH) : 0;
+    uint32_t* rows = reinterpret_cast<uint32_t*>(s_dyn + ((hist_len + 1) & ~1)) + warp * ROWW;
     if (SCAN)
-        for (int i = lane; i < native_warp_words(K, 4, CH); i += kWarp) rows[i] = 0u;
+        for (int i = lane; i < ROWW; i += kWarp) rows[i] = 0u;
     uint32_t* const wr = rows + (lane_on ? seg * WP + l : SLOT - 1);
     const uint32_t* const rd = rows + (lane_on ? seg * WP : 0);
+    // this lane's staged draws: [k][tick] doubles, lane-interleaved (conflict-free LDS.64/STS.64)
+    double* const s_draw = reinterpret_cast<double*>(s_dyn + ((hist_len + 1) & ~1) + kWarpsPerBlock * ROWW / 2) +
+                           warp * (K * NT * kWarp) + lane;
     __syncthreads();
 
     // ---- per-slot constants, FP64 (the host's double parameter block) ----
@@ -270,10 +292,22 @@ native64_kernel(const LaunchArgs a) {
         }
         if (!__any_sync(0xffffffffu, running)) break;
 
-        const uint64_t gs = (uint64_t)(a.sim_offset + s);
-        double dr[K][2];
+        // ---- the block's draws: NT per slot, into this lane's shared-memory column ----
+        {
+            const uint64_t gs = (uint64_t)(a.sim_offset + s);
+#pragma unroll 1
+            for (int h = 0; h < NT / 2; ++h) {
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    double d0, d1;
+                    draw_pair(k, ((uint32_t)rt >> 1) + (uint32_t)h, gs, d0, d1);
+                    s_draw[(k * NT + 2 * h) * kWarp] = d0;
+                    s_draw[(k * NT + 2 * h + 1) * kWarp] = d1;
+                }
+            }
+        }
 
-        auto tick = [&](const int tj) {
+        auto tick = [&](const int tj, const int par, auto resp_var, auto guard) {
             bool racing[K];
 #pragma unroll
             for (int k = 0; k < K; ++k) racing[k] = fin[k] == kRacing;
@@ -291,7 +325,7 @@ native64_kernel(const LaunchArgs a) {
                     const double y = __dadd_rn(pos[k], C64);
                     const uint32_t key = __funnelshift_r((uint32_t)__double2loint(y), (uint32_t)__double2hiint(y), 26);
                     v[k] = key * 32u + cl;
-                    wr[(tj & 1) * PAR + k * SLOT] = racing[k] ? v[k] : 0u;
+                    wr[par * PAR + k * SLOT] = racing[k] ? v[k] : 0u;
                 }
                 __syncwarp();
                 // per (own slot k, row kk) offset: t = v_r + nk is < 2^31 iff rival r follows c in
@@ -307,7 +341,7 @@ native64_kernel(const LaunchArgs a) {
                     for (int kk = 0; kk < K; ++kk) {
                         const uint32_t nk = kk < k ? ~(v[k] | 31u) : (kk == k ? ~v[k] : 0u - (v[k] & ~31u));
                         uint32_t b0 = 0xffffffffu, b1 = 0xffffffffu;
-                        const uint4* r4 = reinterpret_cast<const uint4*>(rd + (tj & 1) * PAR + kk * SLOT);
+                        const uint4* r4 = reinterpret_cast<const uint4*>(rd + par * PAR + kk * SLOT);
 #pragma unroll
                         for (int c = 0; c < CH; ++c) {
                             const uint4 q = r4[c];
@@ -391,36 +425,54 @@ native64_kernel(const LaunchArgs a) {
             }
 
             // ---- synchronous update (race.py:299-320) ----
+            bool eq_any = false;
+            double pnew[K];
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                const bool early = pos[k] < bp[k];
+                const bool early = decltype(resp_var)::value ? pos[k] < bp[k] : true;
                 double step;
+                const double dk = s_draw[(k * NT + tj) * kWarp];
                 if (!SCAN || fr[k]) {
-                    step = __dmul_rn(early ? rpE[k] : rpL[k], dr[k][tj & 1]);
+                    step = __dmul_rn(early ? rpE[k] : rpL[k], dk);
                 } else {
                     const double m = (pf[k] < prev[k]) ? pf[k] : prev[k];  // Python min(prev_c, prev_front)
                     step = __dmul_rn(early ? eE[k] : eL[k], m);
                 }
-                double p = __dadd_rn(pos[k], step);
-                if (p == pos[k]) p = nextafter(p, CUDART_INF);
-                const bool done = racing[k] && p >= L;
-                pos[k] = racing[k] ? p : pos[k];
+                pnew[k] = __dadd_rn(pos[k], step);
+                if constexpr (decltype(guard)::value) eq_any |= racing[k] && pnew[k] == pos[k];
                 prev[k] = step;  // a finished competitor's previous step is never read again
+            }
+            if constexpr (decltype(guard)::value) {
+                if (__any_sync(0xffffffffu, eq_any)) {
+#pragma unroll
+                    for (int k = 0; k < K; ++k)
+                        if (pnew[k] == pos[k]) pnew[k] = nextafter(pnew[k], CUDART_INF);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const bool done = racing[k] && pnew[k] >= L;
+                pos[k] = racing[k] ? pnew[k] : pos[k];
                 blk_sim += bl[k] ? 1u : 0u;
                 fin[k] = done ? rt + 1 : fin[k];
             }
             rt += 1;
         };
 
-        if (SCAN) __syncwarp();  // key rows: the previous block's reads precede this block's writes
-#pragma unroll
-        for (int tj = 0; tj < NT; ++tj) {
-            if ((tj & 1) == 0) {
-#pragma unroll
-                for (int k = 0; k < K; ++k) draw_pair(k, (uint32_t)rt >> 1, gs, dr[k][0], dr[k][1]);
+        // the block's NT ticks, in pairs (the key rows alternate by tick parity), under the host flags
+        auto run_block = [&](auto resp_var, auto guard) {
+#pragma unroll 1
+            for (int tp = 0; tp < NT; tp += 2) {
+                tick(tp, 0, resp_var, guard);
+                tick(tp + 1, 1, resp_var, guard);
             }
-            tick(tj);
-        }
+        };
+        if (SCAN) __syncwarp();  // key rows: the previous block's reads precede this block's writes
+        const int fl = a.n64_flags;
+        if (fl == (kN64RespVar | kN64Guard)) run_block(CBool<true>{}, CBool<true>{});
+        else if (fl == kN64RespVar) run_block(CBool<true>{}, CBool<false>{});
+        else if (fl == kN64Guard) run_block(CBool<false>{}, CBool<true>{});
+        else run_block(CBool<false>{}, CBool<false>{});
     }
 
     // ---------------- flush ----------------

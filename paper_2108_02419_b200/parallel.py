@@ -6,9 +6,11 @@ index (NATIVE: Philox counter; MT: the sim's own seed; INJECT: its CSR draw rang
 tallies are bit-identical for any number of ranks -- the GPU analogue of run_batch's worker-count
 invariance (batch.py:110-124, tests/test_batch.py:38-42).
 
-The only collective is the reduction of the tally vector (``bbe_tally_len(n)`` u64 counters,
-< 1 KB for n = 10): SUM over the counters, MAX over the two complement-encoded "first failing
-sim" fields (include/bbe_sim.h).  On NCCL it is enqueued on the same stream right after the kernel.
+The only collective on the success path is ONE SUM all-reduce of the tally vector
+(``bbe_tally_len(n)`` u64 counters, < 1 KB for n = 10), enqueued on the kernel's stream right after
+it.  The two complement-encoded "first failing sim" fields (include/bbe_sim.h) need a MAX, not a
+SUM: each rank keeps its own values, and only when the summed failure counts are non-zero -- the
+same on every rank after the SUM -- does ``settle_first_fields`` run a second (MAX) all-reduce.
 """
 
 from __future__ import annotations
@@ -52,12 +54,31 @@ class TallyLayout:
         return self.ct + 4
 
 
-def reduce_tally(tally, layout: TallyLayout, group=None) -> None:
-    """In-place all-reduce of one rank's tally tensor (torch int64; CUDA for NCCL, CPU for gloo)."""
+def reduce_tally(tally, layout: TallyLayout, group=None):
+    """One in-place SUM all-reduce of a rank's tally tensor (torch int64; CUDA for NCCL, CPU for gloo).
+
+    Returns this rank's own "first failing sim" fields (a copy taken before the SUM, which garbles
+    them in ``tally``); pass it to ``settle_first_fields`` once the tally has been read."""
     import torch.distributed as dist
 
-    dist.all_reduce(tally[: layout.sum_len], op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(tally[layout.sum_len:], op=dist.ReduceOp.MAX, group=group)
+    own_first = tally[layout.sum_len:].clone()
+    dist.all_reduce(tally, op=dist.ReduceOp.SUM, group=group)
+    return own_first
+
+
+def settle_first_fields(tally, own_first, layout: TallyLayout, group=None) -> None:
+    """Restore the MAX-reduced "first failing sim" fields after ``reduce_tally``.
+
+    No collective when no rank failed (the summed n_div / n_bad are zero -- identical on every rank,
+    so every rank takes the same branch); else one MAX all-reduce of the saved fields."""
+    import torch.distributed as dist
+
+    fails = int(tally[layout.ct + 2]) + int(tally[layout.ct + 3])
+    if fails == 0:
+        tally[layout.sum_len:] = 0
+        return
+    dist.all_reduce(own_first, op=dist.ReduceOp.MAX, group=group)
+    tally[layout.sum_len:] = own_first.to(tally.device)
 
 
 @dataclass
@@ -123,8 +144,12 @@ def simulate_sharded(state, config, n_sims: int, seed: int = 0, *, group=None, l
     launcher.launch(tally.data_ptr(), hi - lo, seed, sim_offset=lo,
                     stream=torch.cuda.current_stream().cuda_stream, mode=mode)
     if world > 1:
-        reduce_tally(tally, layout, group)
-    out = decode_tally(tally.cpu().numpy().view(np.uint64), layout)
+        own_first = reduce_tally(tally, layout, group)
+        host = tally.cpu()
+        settle_first_fields(host, own_first, layout, group)  # own_first stays on the collective's device
+        out = decode_tally(host.numpy().view(np.uint64), layout)
+    else:
+        out = decode_tally(tally.cpu().numpy().view(np.uint64), layout)
     if out.n_diverged:
         raise SimDivergedError(out.first_diverged, f"race exceeded tick_limit in sim {out.first_diverged}")
     return out

@@ -103,15 +103,17 @@ def test_dry_run_session_c4_shape():
     out = run_dry_run_session(base, n_agents=20, d=50, master_seed=7, opening_period=3.0)
     assert out.launches >= 3 and out.sims == sum(50 for _ in out.predictions)
     assert all(abs(sum(p) - 1.0) < 1e-12 for _, _, p in out.predictions)
-    # every prediction equals the bettor's own sequential rp_predict on the same live-race state
+    # every prediction equals the bettor's own sequential rp_predict on the same live-race state, the
+    # bettor's decision (its tie-break draw) made between its predictions as in the reference
     from paper_2108_02419_b200.seeding import spawn_rng
-    from paper_2108_02419_b200.session import live_states
+    from paper_2108_02419_b200.session import decide_draws, live_states
 
     states = live_states(base, 7)
     rngs = [spawn_rng(7, "agent", i) for i in range(20)]
-    for t, i, p in out.predictions[:60]:
+    for t, i, p in out.predictions:
         tick = 0 if t <= 3.0 else int(np.ceil(t - 3.0 - 1e-9))
         assert rp_predict(states[tick], base, 50, rngs[i], mode="mt") == p
+        decide_draws(rngs[i], p, None)
 
 
 def test_cli_products(tmp_path):
@@ -155,9 +157,9 @@ def oracle_seed_race():
     return derive_seed(20260818, "race")
 
 
-def test_session_host_work_overlaps_the_next_batch():
-    """on_batch (the exchange loop's share of a tick) runs while the next batch is on the GPU: the
-    predictions are unchanged and each batch reaches the callback exactly once, in order."""
+def test_session_on_batch_sees_every_batch_in_order():
+    """on_batch (the host's use of a batch) reaches every batch exactly once, in order, and does not
+    change the predictions."""
     base = RaceConfig(300.0, tuple(Competitor(f"c{i + 1}", UniformSteps(10.0, 20.0)) for i in range(5)))
     ref = run_dry_run_session(base, n_agents=20, d=50, master_seed=7, opening_period=3.0)
     seen = []
