@@ -79,6 +79,27 @@ __device__ __forceinline__ void normal_pair64(const U4& w, double& n0, double& n
     n1 = __dmul_rn(r, s);
 }
 
+// The lognormal step draws of competitor c for ticks 2h and 2h + 1 of global sim gs (counter word 0 =
+// h): scale * exp(mu + z * sigma) (random.py lognormvariate / normalvariate) with the Box-Muller pair
+// of the same Philox words a uniform competitor would use.  Parameters are read from the parameter
+// block (L1-resident), not held in registers.
+static __device__ __noinline__ double2 ln_pair(const double* P, int n, int c, uint32_t h, uint64_t gs, uint32_t k0, uint32_t k1) {
+    U4 x{h, (uint32_t)c, (uint32_t)gs, (uint32_t)(gs >> 32)};
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {  // philox_rk with the key schedule computed in place
+        const uint32_t hi0 = __umulhi(0xD2511F53u, x.x), lo0 = 0xD2511F53u * x.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, x.z), lo1 = 0xCD9E8D57u * x.z;
+        x = U4{hi1 ^ x.y ^ k0, lo1, hi0 ^ x.w ^ k1, lo0};
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    double z0, z1;
+    normal_pair64(x, z0, z1);
+    const double mu = P[F_MU * n + c], sigma = P[F_SIGMA * n + c], scale = P[F_SCALE * n + c];
+    return make_double2(__dmul_rn(scale, exp(__dadd_rn(mu, __dmul_rn(z0, sigma)))),
+                        __dmul_rn(scale, exp(__dadd_rn(mu, __dmul_rn(z1, sigma)))));
+}
+
 // K: competitors per lane; CH: key-row chunks of 4 words (SCAN only); SCAN: some theta > 0 (else
 // nobody can be blocked and the scan is omitted); LN: some lognormal competitor; NT: ticks per block.
 template <int K, int CH, bool SCAN, bool LN, int NT>
@@ -90,6 +111,20 @@ native64_kernel(const LaunchArgs a) {
     const int hist_len = TL.hist_len();
     uint32_t* s_hist = reinterpret_cast<uint32_t*>(s_dyn);
     for (int i = threadIdx.x; i < hist_len; i += blockDim.x) s_hist[i] = 0u;
+    // the lognormal competitors, in index order (their draws are computed lane-compacted, below)
+    __shared__ uint8_t s_lnc[128];  // BBE_MAX_COMPETITORS
+    __shared__ int s_nln;
+    if (LN && threadIdx.x < kWarp) {
+        int m = 0;
+        for (int c0 = 0; c0 < a.n; c0 += kWarp) {
+            const int c = c0 + (int)threadIdx.x;
+            const bool is_ln = c < a.n && a.P[F_FAMILY * a.n + c] != 0.0;
+            const unsigned b = __ballot_sync(0xffffffffu, is_ln);
+            if (is_ln) s_lnc[m + __popc(b & ((1u << threadIdx.x) - 1u))] = (uint8_t)c;
+            m += __popc(b);
+        }
+        if (threadIdx.x == 0) s_nln = m;
+    }
 
     constexpr int WP = 4 * CH;
     constexpr int SLOT = native_slot_words(4, CH);
@@ -118,7 +153,7 @@ native64_kernel(const LaunchArgs a) {
     // ---- per-slot constants, FP64 (the host's double parameter block) ----
     int cidx[K];
     bool has[K], lognorm[K];
-    double lo[K], span[K], mu[K], sigma[K], scale[K], rpE[K], rpL[K], eE[K], eL[K], bp[K], th[K];
+    double lo[K], span[K], rpE[K], rpL[K], eE[K], eL[K], bp[K], th[K];
     const double* P = a.P;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -128,9 +163,6 @@ native64_kernel(const LaunchArgs a) {
         const int cc = has[k] ? c : 0;
         lo[k] = P[F_LO * n + cc];
         span[k] = P[F_SPAN * n + cc];
-        mu[k] = P[F_MU * n + cc];
-        sigma[k] = P[F_SIGMA * n + cc];
-        scale[k] = P[F_SCALE * n + cc];
         rpE[k] = P[F_RP_EARLY * n + cc];
         rpL[k] = P[F_RP_LATE * n + cc];
         eE[k] = P[F_EARLY * n + cc];
@@ -157,19 +189,11 @@ native64_kernel(const LaunchArgs a) {
     unsigned long long ct_tot = 0, blk_tot = 0, n_div = 0;
     int64_t first_div = INT64_MAX;
 
-    // the step draw of slot k for ticks 2h and 2h + 1 of the sim (counter word 0 = h)
+    // the uniform step draws of slot k for ticks 2h and 2h + 1 of the sim (counter word 0 = h)
     auto draw_pair = [&](int k, uint32_t h, uint64_t gs, double& d0, double& d1) {
         const U4 w = philox_rk(U4{h, (uint32_t)cidx[k], (uint32_t)gs, (uint32_t)(gs >> 32)}, a.rk);
         d0 = __dadd_rn(lo[k], __dmul_rn(span[k], random53(w.x, w.y)));
         d1 = __dadd_rn(lo[k], __dmul_rn(span[k], random53(w.z, w.w)));
-        if constexpr (LN) {
-            if (lognorm[k]) {
-                double z0, z1;
-                normal_pair64(w, z0, z1);
-                d0 = __dmul_rn(scale[k], exp(__dadd_rn(mu[k], __dmul_rn(z0, sigma[k]))));
-                d1 = __dmul_rn(scale[k], exp(__dadd_rn(mu[k], __dmul_rn(z1, sigma[k]))));
-            }
-        }
     };
 
     auto load_sim = [&](bool do_it) {
@@ -189,7 +213,8 @@ native64_kernel(const LaunchArgs a) {
             if (a.from_start && running && has[k]) {
                 // race.py:233-241: one free draw per competitor, resp at position 0
                 double d, d1;
-                draw_pair(k, 0xFFFFFFFFu, gs, d, d1);
+                if (LN && lognorm[k]) d = ln_pair(P, n, cidx[k], 0xFFFFFFFFu, gs, a.rk[0], a.rk[1]).x;
+                else draw_pair(k, 0xFFFFFFFFu, gs, d, d1);
                 prev[k] = __dmul_rn((0.0 < bp[k]) ? rpE[k] : rpL[k], d);
             }
         }
@@ -304,6 +329,34 @@ native64_kernel(const LaunchArgs a) {
                     s_draw[(k * NT + 2 * h) * kWarp] = d0;
                     s_draw[(k * NT + 2 * h + 1) * kWarp] = d1;
                 }
+            }
+            if constexpr (LN) {
+                // lognormal draws, lane-compacted: item j = (segment, lognormal competitor, tick pair)
+                // runs on lane j % 32 and overwrites the owner lane's two staged draws (the owner's
+                // own pass above wrote uniform values there).  C2 (2 lognormal of 10, 3 segments, 8
+                // ticks): 24 items, one pass, instead of 4 pairs x (6 of 32 lanes active).
+                const int m = s_nln;
+                const int per_seg = m * (NT / 2);
+                const int items = S * per_seg;
+                __syncwarp();
+                for (int j0 = 0; j0 < items; j0 += kWarp) {
+                    const int j = j0 + lane;
+                    const int sg = min(j, items - 1) / per_seg;
+                    const int r = min(j, items - 1) - sg * per_seg;
+                    const int i = r / (NT / 2), h = r - i * (NT / 2);
+                    const int64_t s_item = shfl(s, sg * W);
+                    const int32_t rt_item = shfl(rt, sg * W);
+                    if (j < items && s_item < a.n_sims) {
+                        const int c = s_lnc[i];
+                        const int kk = c / W, owner = sg * W + (c - kk * W);
+                        const double2 d = ln_pair(P, n, c, ((uint32_t)rt_item >> 1) + (uint32_t)h,
+                                                  (uint64_t)(a.sim_offset + s_item), a.rk[0], a.rk[1]);
+                        double* col = s_draw - lane + owner;
+                        col[(kk * NT + 2 * h) * kWarp] = d.x;
+                        col[(kk * NT + 2 * h + 1) * kWarp] = d.y;
+                    }
+                }
+                __syncwarp();
             }
         }
 
