@@ -1,23 +1,31 @@
-"""Benchmark: batched Monte Carlo race continuation (the BBE dry-run hot path) on B200.
+"""Benchmark: batched Monte Carlo race simulation (the BBE dry-run hot path) on B200.
 
-Workload (BASELINE.json configs[1]): derby.json resized to 10 runners
-(uniform / preference-sensitive / lognormal / theta=8 blocking / closer), mid-race state
-make_rng(3) + initial_state + 65 ticks (tests/golden/c2.json, generated from the reference), and
-100,000 continuations per call -- one rp_predict call of one bettor.  A step = one such call.
+Headline workload (BASELINE.json configs[4] = SURVEY C5, the configuration the metric "races/s per
+GPU at 1/2/4/8 B200" is quoted on): a 20-competitor race (20 x U(10,20), L = 2000, theta = 0, the
+reference's default field widened to 20, config.py:433-443) simulated from the start line
+(run_race semantics: priming draws, race.py:233-241, 373-390), 10^9 simulations per step, split into
+contiguous sim-index shards over the N ranks (strong scaling) with ONE NCCL SUM all-reduce of the
+tally vector inside the step.  Arithmetic: FP64 race state in the reference's operation order
+(NATIVE64 kernel), Philox4x32-10 draws with 53-bit resolution.
 
-  value  device-resident: bbe_simulate_async into a device tally on torch's stream, CUDA events,
-         max over ranks; N>1 = weak scaling (each rank its own 100k-sim shard, disjoint sim indices)
-         plus the NCCL all-reduce of the tally vector inside the step.
-  e2e    through the public API agents.rp_predict(state, config, d, rng) with host buffers: agent
-         stream advance, parameter H2D, kernel, tally D2H, Laplace probabilities.
-  roofline  FP32/INT32 issue roofline of the race kernel: lane-ops per competitor-
-         timestep (ct) = 4(n-1) + 13 + 22*f_free; achieved = ct/s * ops/ct; peak = 148 SMs x 128
-         lanes x max SM clock.
-  cpu_baseline  oracle/pyref.py (the reference's algorithm in the reference's language and RNG),
-         single thread, bounded sample.
+  value  device-resident: the prepared race (parameters uploaded once), each step = tally zero +
+         race kernel over this rank's shard + tally all-reduce, CUDA events on the launching
+         stream, max over ranks; value = 10^9 x steps / max-rank time.
+  e2e    the same metric through the public API parallel.simulate_sharded(None, config, 10^9, seed,
+         mode="native64") with host buffers: parameter H2D, kernel, all-reduce, tally D2H per step
+         (wall clock per call, max over ranks).
+  roofline  FP32/INT32 issue roofline of the race kernel, lane-ops per competitor-
+         timestep (ct) for the FP64-state kernel = [scan: 4(n-1)] + 13 + 44 f_free (a 53-bit draw =
+         two Philox words, 2 x 20 ops, + 4 to form the double); peak = SMs x 128 lanes x max clock.
+  cpu_baseline  the reference itself (racemarket from baseline/_ref: run_batch(workers=1), i.e.
+         run_race per seed) on a bounded sample of the same workload, one core.
 
-``--impl reference`` times that same pure-Python restatement with every host core (process pool,
-the reference's run_batch fan-out style) on the same workload; rank 0 only.
+``--impl reference`` times the reference's own parallel path, racemarket ``run_batch`` with
+``workers = host cores`` (batch.py:110-124), on a bounded sample of the same workload per step;
+rank 0 only.  Without baseline/_ref it falls back to oracle/pyref.py (kind "port").
+
+``--gpus N`` without torchrun's RANK re-launches itself under ``torch.distributed.run`` with N
+ranks (127.0.0.1), one GPU per rank.
 """
 
 from __future__ import annotations
@@ -25,6 +33,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -37,24 +46,88 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
-SIMS_PER_CALL = 100_000
 METRIC = "simulated races/sec"
 UNIT = "races/s"
+MASTER = 20260818
+C5_SIMS = 1_000_000_000
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC = os.path.join(ROOT, "profiles", "r2_native64_c5_ncu.json")
 
 
-def load_workload():
+# ---------------------------------------------------------------------------------------------------
+# workloads
+
+
+def uniform_field(n: int, track_length: float = 2000.0):
+    """n x U(10, 20) competitors, theta 0 (config.py:433-443 default field, widened)."""
+    from paper_2108_02419_b200.race import Competitor, RaceConfig, UniformSteps
+
+    return RaceConfig(track_length, tuple(Competitor(f"c{i + 1}", UniformSteps(10.0, 20.0)) for i in range(n)))
+
+
+def c2_workload():
     from golden_io import c2, config_from_dict, state_from_dict
 
     g = c2()
     return config_from_dict(g["config"]), state_from_dict(g["state"])
 
 
-def ops_per_ct(n: int, f_free: float) -> float:
-    return 4 * (n - 1) + 13 + 22 * f_free
+def job_config(total_sims: int, world: int) -> dict:
+    """The ``config`` of both arms' JSON lines (identical dicts: same workload)."""
+    return {"workload": "C5: 20-competitor race (20 x U(10,20), L=2000, theta=0) from the start line, "
+                        f"{total_sims} simulations per step split over the ranks",
+            "competitors": 20, "track_length": 2000.0, "sims_per_step": int(total_sims), "from_start": True,
+            "rng": "philox4x32-10 (53-bit draws)", "state": "f64",
+            "l2": "flushed between timed steps (256 MB write); the kernel's working set is on-chip",
+            "parallelism": f"dp{world} (contiguous sim-index shards, one NCCL SUM all-reduce of the tally)"}
+
+
+def ops_per_ct(n: int, f_free: float, *, scan: bool = True, native64: bool = True) -> float:
+    """Algorithmic lane-ops per competitor-timestep.  FP32 state: a draw is
+    one Philox word (20 ops) + 2; FP64 state: two words + 4.  The scan term drops when every theta is
+    0 (nobody can be blocked, the scan's result is never used)."""
+    draw = 44.0 if native64 else 22.0
+    return (4 * (n - 1) if scan else 0) + 13 + draw * f_free
+
+
+def issue_peak(sms: int):
+    mhz = 1965.0
+    try:
+        with open(PEAKS) as fh:
+            mhz = float(json.load(fh).get("sm_max_mhz", mhz))
+    except (OSError, ValueError):
+        pass
+    return sms * 128 * mhz * 1e6 / 1e9, f"{sms} SMs x 128 FP32/INT32 lanes x {mhz:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)"
+
+
+def load_traffic():
+    """DRAM bytes per launch of the NATIVE64 C5 kernel from the committed ncu --set full capture."""
+    try:
+        with open(TRAFFIC) as fh:
+            d = json.load(fh)
+        return d.get("dram_bytes_per_launch"), d.get("source")
+    except (OSError, ValueError):
+        return None, None
+
+
+# ---------------------------------------------------------------------------------------------------
+# process plumbing
 
 
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_command(gpus: int, argv: list[str], port: int) -> list[str]:
+    """The torchrun command that re-runs this bench with one rank per GPU."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
 
 
 class ClockSampler:
@@ -127,137 +200,325 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows), "power_w_max": max(pw) if pw else None}
 
 
-def cpu_baseline_pyref(cfg, state, n_sims: int):
-    from oracle import pyref
-
-    seeds = [pyref.derive_seed(20260818, "bench", i) for i in range(n_sims)]
-    t0 = time.perf_counter()
-    wins, ct = pyref.batch_tally(cfg, seeds, state, workers=1)
-    dt = time.perf_counter() - t0
-    return {"value": n_sims / dt, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{n_sims} C2 continuations, oracle/pyref.py (reference algorithm, CPython random), 1 thread",
-            "ct_per_s": ct / dt, "seconds": dt}
+# ---------------------------------------------------------------------------------------------------
+# the strong-scaling job (device-agnostic: CUDA + NCCL in the bench, CPU + gloo in
+# tests/test_bench_harness.py with an oracle-backed launch)
 
 
-def cpu_baseline_c(cfg, state, n_sims: int):
+class CudaTimer:
+    """CUDA events on the launching stream (torch's current stream)."""
+
+    def __init__(self, torch):
+        self.torch = torch
+        self.pairs = []
+
+    def start(self):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def stop(self, e0):
+        e1 = self.torch.cuda.Event(enable_timing=True)
+        e1.record()
+        self.pairs.append((e0, e1))
+
+    def sync(self):
+        self.torch.cuda.synchronize()
+
+    def times_ms(self):
+        self.sync()
+        return [a.elapsed_time(b) for a, b in self.pairs]
+
+
+class WallTimer:
+    """Host wall clock (CPU-only harness test; every launch there is synchronous)."""
+
+    def __init__(self):
+        self.ms = []
+
+    def start(self):
+        return time.perf_counter()
+
+    def stop(self, t0):
+        self.ms.append((time.perf_counter() - t0) * 1e3)
+
+    def sync(self):
+        pass
+
+    def times_ms(self):
+        return list(self.ms)
+
+
+def run_strong_job(launch, layout, total_sims: int, steps: int, warmup: int, *, rank: int, world: int, device,
+                   timer, seed0: int = MASTER, flush=None, on_start=None, on_end=None, after_step=None):
+    """W warm-up + K timed steps of the sharded job.  A step: zero this rank's tally, ``launch(tally,
+    n, seed, sim_offset)`` over the rank's contiguous shard of [0, total_sims), then ONE SUM
+    all-reduce of the tally (parallel.reduce_tally) when world > 1.  Steps are bracketed by a barrier
+    and a device sync on both sides.  Returns (max-over-ranks total ms, per-step local ms, the last
+    step's reduced tally as int64 numpy, ct and blocked summed over the timed steps (job totals))."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2108_02419_b200.parallel import reduce_tally, settle_first_fields, shard_range
+
+    lo, hi = shard_range(int(total_sims), rank, world)
+    tally = torch.zeros(layout.length, dtype=torch.int64, device=device)
+    state = {"own": None}
+
+    def step(i):
+        tally.zero_()
+        launch(tally, hi - lo, seed0 + i, lo)
+        state["own"] = reduce_tally(tally, layout) if world > 1 else None
+
+    def read():
+        host = tally.cpu()
+        if world > 1:
+            settle_first_fields(host, state["own"], layout)
+        return host.numpy().copy()
+
+    for i in range(warmup):
+        step(i)
+        read()
+    timer.sync()
+    if world > 1:
+        dist.barrier()
+    timer.sync()
+    if on_start:
+        on_start()
+    ct = blocked = 0
+    last = None
+    for i in range(steps):
+        if flush:
+            flush(i)  # outside the timed bracket
+        t = timer.start()
+        step(warmup + i)
+        timer.stop(t)
+        last = read()
+        ct += int(last[layout.ct])
+        blocked += int(last[layout.ct + 1])
+        if after_step:
+            after_step(i, last)
+    timer.sync()
+    if on_end:
+        on_end()
+    if world > 1:
+        dist.barrier()
+    local = timer.times_ms()
+    total = torch.tensor([sum(local)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    return float(total.item()), local, last, ct, blocked
+
+
+# ---------------------------------------------------------------------------------------------------
+# CPU baselines (the reference itself; the oracle only where the reference is absent)
+
+
+def reference_module():
+    try:
+        from paper_2108_02419_b200.session import import_racemarket
+
+        return import_racemarket()
+    except ImportError:
+        return None
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def reference_batch(rm, cfg, sims: int, master: int, workers: int):
+    """racemarket.batch.run_batch over ``sims`` runs of ``cfg`` from the start line; returns (ct, winners)."""
+    from paper_2108_02419_b200.session import to_reference_race
+
+    res = rm.batch.run_batch(rm.batch.BatchConfig(to_reference_race(cfg), sims, master, workers=workers))
+    return sum(sum(r.finish_ticks) for r in res), [r.winner for r in res]
+
+
+def cpu_baseline_reference(cfg, sims: int):
+    """The reference's own single-thread path (run_batch(workers=1) = run_race per seed) on a sample."""
+    rm = reference_module()
+    if rm is None:
+        from oracle import pyref
+
+        seeds = [pyref.derive_seed(MASTER, "run", i) for i in range(sims)]
+        t0 = time.perf_counter()
+        _, ct = pyref.batch_tally(cfg, seeds, None, workers=1)
+        dt = time.perf_counter() - t0
+        kind, what = "port", "oracle/pyref.py (reference algorithm, CPython random; racemarket not installed)"
+    else:
+        t0 = time.perf_counter()
+        ct, _ = reference_batch(rm, cfg, sims, MASTER, 1)
+        dt = time.perf_counter() - t0
+        kind, what = "reference", "racemarket.batch.run_batch(workers=1) from baseline/_ref"
+    return {"value": sims / dt, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"{sims} C5 races from the start line, {what}, 1 core", "ct_per_s": ct / dt, "seconds": dt}
+
+
+def cpu_baseline_c(cfg, sims: int):
     import oracle
     from oracle import pyref
 
     cores = pyref.cpu_count()
     t0 = time.perf_counter()
-    out = oracle.batch(cfg, n_sims, state=state, master=20260818, threads=cores)
+    out = oracle.batch(cfg, sims, master=MASTER, threads=cores)
     dt = time.perf_counter() - t0
-    return {"value": n_sims / dt, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{n_sims} C2 continuations, oracle/bbe_oracle.c (C restatement, MT19937), {cores} threads",
+    return {"value": sims / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{sims} C5 races, oracle/bbe_oracle.c (C restatement, MT19937), {cores} threads",
             "ct_per_s": out["ct"] / dt, "seconds": dt}
 
 
 def run_reference(args):
-    """--impl reference: the reference algorithm on all host cores (rank 0 only)."""
+    """--impl reference: the reference's run_batch over every host core, rank 0 only."""
     rank, world, _ = dist_env()
+    world = max(world, args.gpus)
     if rank != 0:
         return 0
-    from oracle import pyref
-
-    cfg, state = load_workload()
-    cores = pyref.cpu_count()
-    sample = args.ref_sample
+    cfg = uniform_field(20)
+    cores = host_cores()
+    sample = args.ref_sample or 320 * cores
+    rm = reference_module()
     times, cts = [], []
-    pool = pyref.TallyPool(cfg, state, workers=cores)
-    for i in range(args.warmup + args.steps):
-        seeds = [pyref.derive_seed(20260818, "ref", i, j) for j in range(sample)]
-        t0 = time.perf_counter()
-        wins, ct = pool.run(seeds)
-        dt = time.perf_counter() - t0
-        if i >= args.warmup:
-            times.append(dt)
-            cts.append(ct)
-    pool.close()
+    if rm is not None:
+        kind = "reference"
+        what = f"racemarket.batch.run_batch(BatchConfig(race, {sample}, seed, workers={cores})) from baseline/_ref"
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            ct, _ = reference_batch(rm, cfg, sample, MASTER + i, cores)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+                cts.append(ct)
+    else:
+        from oracle import pyref
+
+        kind = "port"
+        what = f"oracle/pyref.py over a {cores}-process pool (racemarket not installed)"
+        pool = pyref.TallyPool(cfg, None, workers=cores)
+        for i in range(args.warmup + args.steps):
+            seeds = [pyref.derive_seed(MASTER + i, "run", j) for j in range(sample)]
+            t0 = time.perf_counter()
+            _, ct = pool.run(seeds)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+                cts.append(ct)
+        pool.close()
     t = sum(times) / len(times)
     value = sample / t
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2: derby10 mid-race (tick 65) continuation, rp_predict dry runs",
-                   "sims_per_step": sample, "competitors": 10},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": job_config(args.c5_sims, world),
         "ct_per_s": sum(cts) / sum(times),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{sample} C2 continuations per step, oracle/pyref.py over a {cores}-process pool"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"{sample} races of the C5 workload per step (a bounded sample of the "
+                                   f"{args.c5_sims} per step), {what}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def sweep_configs(args, torch, sim):
-    """The other BASELINE.json configs, device-resident NATIVE launches (one warm-up + one timed each):
-    C1 = 5 x U(10,20), L=2000 from the start line (1,000 sims, the reference's CPU case, and 10^6);
-    C3 = 20 x U(10,20), L=2000, 10^7 sims; derby20 = derby.json resized to 20, 10^6 sims; C5 = the C3
-    field at 10^9 sims in one launch (the per-GPU shard of the scaling config)."""
-    from golden_io import c2, config_from_dict
-    from paper_2108_02419_b200.batch import resize_race
-    from paper_2108_02419_b200.race import Competitor, RaceConfig, UniformSteps
+# ---------------------------------------------------------------------------------------------------
+# secondary configurations (rank 0, N = 1 numbers; not the headline)
 
-    def uniform_field(n):
-        return RaceConfig(2000.0, tuple(Competitor(f"c{i + 1}", UniformSteps(10.0, 20.0)) for i in range(n)))
 
-    derby10 = config_from_dict(c2()["config"])
-    derby5 = resize_race(derby10, 5)
-    runs = [("C1_5x_U10_20_from_start_1e3", uniform_field(5), 1_000),
-            ("C1_5x_U10_20_from_start_1e6", uniform_field(5), 1_000_000),
-            ("C3_20x_U10_20_from_start_1e7", uniform_field(20), args.c3_sims),
-            ("derby20_from_start_1e6", resize_race(derby5, 20), 1_000_000),
-            ("C5_20x_U10_20_from_start_1e9", uniform_field(20), args.c5_sims)]
-    out = {}
-    stream = torch.cuda.current_stream()
-    for name, cfg, n_sims in runs:
-        L = sim.DeviceLauncher(None, cfg)
-        tally = torch.zeros(L.tally_len, dtype=torch.int64, device="cuda")
-        L.launch(tally.data_ptr(), min(n_sims, 100_000), 1, stream=stream.cuda_stream)
-        torch.cuda.synchronize()
+def device_launch_ms(torch, sim, state, cfg, n_sims, mode, reps=2):
+    """One warm-up + best of ``reps`` device-resident prepared launches; returns (ms, ct, blocked)."""
+    L = sim.DeviceLauncher(state, cfg, native_mode=mode)
+    tally = torch.zeros(L.tally_len, dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    L.launch(tally.data_ptr(), min(n_sims, 200_000), 1, stream=s, mode=mode)
+    torch.cuda.synchronize()
+    best = None
+    for r in range(reps):
         tally.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        L.launch(tally.data_ptr(), n_sims, 2, stream=stream.cuda_stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
-        t = tally.cpu()
-        ct = int(t[L.off["ct"]])
-        blocked = int(t[L.off["blocked"]])
+        L.launch(tally.data_ptr(), n_sims, 2 + r, stream=s, mode=mode)
+        ms = L.last_kernel_ms()
+        best = ms if best is None else min(best, ms)
+    t = tally.cpu()
+    return best, int(t[L.off["ct"]]), int(t[L.off["blocked"]])
+
+
+def sweep_configs(args, torch, sim):
+    """C1, C2 (native64 / native / mt, device and e2e), C3, derby20, the FP32-state C5, and C4 (the
+    full session with the reference's exchange loop)."""
+    from paper_2108_02419_b200.agents import rp_predict
+    from paper_2108_02419_b200.batch import resize_race
+
+    out = {}
+    peak, _ = issue_peak(torch.cuda.get_device_properties(0).multi_processor_count)
+    derby10, c2_state = c2_workload()
+    runs = [("C1_5x_U10_20_from_start_1e6", None, uniform_field(5), 1_000_000),
+            ("C2_derby10_mid_race_1e5", c2_state, derby10, 100_000),
+            ("C3_20x_U10_20_from_start_1e7", None, uniform_field(20), args.c3_sims),
+            ("derby20_from_start_1e6", None, resize_race(resize_race(derby10, 5), 20), 1_000_000)]
+    for name, state, cfg, n_sims in runs:
         n = len(cfg.competitors)
         scan = any(c.theta > 0 for c in cfg.competitors)
-        # with every theta = 0 no competitor can be blocked (gap > 0 = theta), so the front-runner
-        # scan's result is never used: the algorithmic ops drop the 4(n-1) scan term
-        ops = ops_per_ct(n, 1.0 - blocked / ct) - (0 if scan else 4 * (n - 1))
-        out[name] = {"sims": n_sims, "ms": ms, "races_per_s": n_sims / (ms / 1e3), "ct_per_s": ct / (ms / 1e3),
-                     "ct_per_race": ct / n_sims, "ops_per_ct": ops,
-                     "issue_roofline_frac": ct * ops / (ms / 1e3) / 37.22e12, "scan_needed": scan}
-    # C4: 100 RP bettors, every wake (1 s period, 1 s jitter) predicting with d dry runs on the live
-    # race; all wakes that share a race state run as one launch (session dispatch batching).  The
-    # host exchange loop (order book, matching) is not part of this path and is not run.
-    from paper_2108_02419_b200.session import run_dry_run_session
+        row = {"sims": n_sims}
+        for mode in ("native64", "native"):
+            ms, ct, blk = device_launch_ms(torch, sim, state, cfg, n_sims, mode)
+            ops = ops_per_ct(n, 1.0 - blk / ct, scan=scan, native64=mode == "native64")
+            row[mode] = {"dtype": "f64" if mode == "native64" else "f32", "ms": ms, "races_per_s": n_sims / (ms / 1e3),
+                         "ct_per_s": ct / (ms / 1e3), "ops_per_ct": ops,
+                         "issue_roofline_frac": ct * ops / (ms / 1e3) / (peak * 1e9)}
+        out[name] = row
+    ms, ct, blk = device_launch_ms(torch, sim, None, uniform_field(20), args.c5_sims, "native", reps=1)
+    out["C5_fp32_state_1e9"] = {"dtype": "f32", "ms": ms, "races_per_s": args.c5_sims / (ms / 1e3), "ct_per_s": ct / (ms / 1e3),
+                                "issue_roofline_frac": ct * ops_per_ct(20, 1.0, scan=False, native64=False) / (ms / 1e3) / (peak * 1e9)}
 
-    for mode, d in (("mt", 1000), ("native", 1000), ("native", 10000)):
-        run_dry_run_session(derby5, n_agents=100, d=d, master_seed=20260818, opening_period=5.0, mode=mode)
-        r = run_dry_run_session(derby5, n_agents=100, d=d, master_seed=20260818, opening_period=5.0, mode=mode)
-        out[f"C4_session_100_rp_bettors_d{d}_{mode}"] = {
-            "predictions": len(r.predictions), "launches": r.launches, "sims": r.sims, "seconds": r.seconds,
-            "races_per_s_end_to_end": r.sims_per_second, "race_ticks": r.ticks,
-            "note": "live race + wake schedule + batched predictions; exchange loop not run"}
+    # C2 end to end: one bettor's rp_predict(d = 100k) per call, host buffers
+    import random
+
+    def per_call(mode, calls):
+        agent = random.Random(11)
+        ts = []
+        for i in range(3 + calls):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            probs = rp_predict(c2_state, derby10, 100_000, agent, mode=mode)
+            ts.append(time.perf_counter() - t0)
+        assert abs(sum(probs) - 1.0) < 1e-9
+        return statistics.mean(ts[3:])
+
+    c2 = {}
+    for mode, calls in (("native64", 20), ("native", 20), ("mt", 10)):
+        s = per_call(mode, calls)
+        c2[mode] = {"ms_per_call": s * 1e3, "races_per_s": 100_000 / s}
+    c2["mt"]["note"] = "bit-identical to the reference's rp_predict for the same bettor stream"
+    out["C2_rp_predict_e2e_d1e5"] = c2
+
+    # C4: the full BBE session -- the reference's session loop, exchange and agents (racemarket from
+    # baseline/_ref) with every wake round's RP predictions served by one batched launch
+    try:
+        from paper_2108_02419_b200.session import c4_session_config, run_session_with_stats
+
+        for mode, d in (("mt", 1000), ("native64", 1000), ("native64", 10_000), ("native64", 100_000)):
+            if d > args.c4_max_d:
+                continue
+            cfg = c4_session_config(derby10, n_agents=100, d=d)
+            res, st = run_session_with_stats(cfg, mode=mode)
+            out[f"C4_session_100_rp_bettors_d{d}_{mode}"] = {
+                "races_per_s_end_to_end": st.sims / st.seconds, "seconds": st.seconds,
+                "predict_seconds": st.predict_seconds, "exchange_loop_seconds": st.seconds - st.predict_seconds,
+                "sims": st.sims, "predictions": st.predictions, "launches": st.launches, "rounds": st.rounds,
+                "fallbacks": st.fallbacks, "events": len(res.events), "race_ticks": res.trajectory.n_ticks
+                if hasattr(res.trajectory, "n_ticks") else None,
+                "note": "reference exchange loop (racemarket.session) with batched GPU predictions"
+                        + ("; event log equals the reference's" if mode == "mt" else "")}
+    except ImportError as e:
+        out["C4_session"] = {"unavailable": f"racemarket not importable ({e})"}
     return out
 
 
-def load_traffic():
-    p = os.path.join(ROOT, "profiles", "race_kernel_ncu.json")
-    if os.path.exists(p):
-        try:
-            with open(p) as fh:
-                return json.load(fh).get("dram_bytes_per_launch")
-        except (OSError, ValueError):
-            return None
-    return None
+# ---------------------------------------------------------------------------------------------------
+# our arm
 
 
 def run_ours(args):
@@ -265,136 +526,92 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2108_02419_b200 import sim
-    from paper_2108_02419_b200.agents import rp_predict
+    from paper_2108_02419_b200.parallel import TallyLayout, simulate_sharded
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg, state = load_workload()
+    cfg = uniform_field(20)
     n = cfg.n_competitors
-    from paper_2108_02419_b200.parallel import TallyLayout, reduce_tally
-
-    launcher = sim.DeviceLauncher(state, cfg)
     layout = TallyLayout.for_n(n)
-    tally = torch.zeros(launcher.tally_len, dtype=torch.int64, device="cuda")
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
+    launcher = sim.DeviceLauncher(None, cfg, native_mode="native64")
+    assert launcher.tally_len == layout.length
     stream = torch.cuda.current_stream()
-    sims = args.sims
-    seed = 20260818
-
-    def step(i):
-        tally.zero_()
-        launcher.launch(tally.data_ptr(), sims, seed + i, sim_offset=rank * sims, stream=stream.cuda_stream)
-        if world > 1:
-            reduce_tally(tally, layout)
-
-    for i in range(args.warmup):
-        step(i)
-    torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    flush_buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
     kernel_ms = []
-    ct_total = blocked_total = 0
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        clk.mark_start()
-        for i in range(args.steps):
-            flush.fill_(float(i))  # L2 flush between timed iterations (outside the event bracket)
-            ev[i][0].record(stream)
-            step(args.warmup + i)
-            ev[i][1].record(stream)
-            kernel_ms.append(launcher.last_kernel_ms())
-            t = tally.cpu()
-            ct_total += int(t[launcher.off["ct"]])
-            blocked_total += int(t[launcher.off["blocked"]])
-        torch.cuda.synchronize()
-        clk.mark_end()
-    if world > 1:
-        dist.barrier()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    t_local = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-    total_ms = float(t_local.item())
-    ms_per_step = total_ms / args.steps
-    sims_all = sims * world * args.steps
-    value = sims_all / (total_ms / 1e3)
-    # ct over all ranks: after the all-reduce the tally holds the job total for that step
-    ct_all = ct_total if world > 1 else ct_total
-    ct_per_s = ct_all / (total_ms / 1e3)
 
-    # roofline of the race kernel (this rank), from its own CUDA-event kernel durations
-    f_free = 1.0 - (blocked_total / ct_total if ct_total else 0.0)
-    ops = ops_per_ct(n, f_free)
+    def launch(tally, n_sims, seed, sim_offset):
+        launcher.launch(tally.data_ptr(), n_sims, seed, sim_offset=sim_offset, stream=stream.cuda_stream,
+                        mode="native64")
+
+    def after_step(i, t):
+        kernel_ms.append(launcher.last_kernel_ms())
+        if t[layout.ct + 2]:
+            raise RuntimeError("a C5 simulation diverged")
+
+    with ClockSampler(local) as clk:
+        total_ms, local_ms, last, ct_job, blk_job = run_strong_job(
+            launch, layout, args.c5_sims, args.steps, args.warmup, rank=rank, world=world, device="cuda",
+            timer=CudaTimer(torch), flush=lambda i: flush_buf.fill_(float(i)), on_start=clk.mark_start,
+            on_end=clk.mark_end, after_step=after_step)
+    value = args.c5_sims * args.steps / (total_ms / 1e3)
+    ct_per_s = ct_job / (total_ms / 1e3)
+    assert int(last[:n].sum()) == args.c5_sims, "every simulation has exactly one winner"
+
+    # e2e: the public API with host buffers (parameter H2D, kernel, all-reduce, tally D2H), per call
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    simulate_sharded(None, cfg, args.c5_sims, MASTER + 1000, mode="native64")  # warm-up call
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for i in range(e2e_steps):
+        tal = simulate_sharded(None, cfg, args.c5_sims, MASTER + 2000 + i, mode="native64")
+    e2e_local = time.perf_counter() - t0
+    assert int(tal.wins.sum()) == args.c5_sims
+    e2e_t = torch.tensor([e2e_local], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_s = float(e2e_t.item()) / e2e_steps
+    h2d = int(sim.lib().bbe_param_bytes(n))
+    d2h = layout.length * 8
+
+    # roofline of this rank's race kernel (its own launches, prepared-launch CUDA events)
+    ct_rank_launch = ct_job / args.steps / world
+    f_free = 1.0 - (blk_job / ct_job if ct_job else 0.0)
+    ops = ops_per_ct(n, f_free, scan=False, native64=True)
     k_ms = statistics.mean(kernel_ms)
-    ct_launch = ct_total / args.steps / (world if world > 1 else 1)
-    achieved = ct_launch * ops / (k_ms / 1e3) / 1e9  # Glane-op/s
-    name = torch.cuda.get_device_name(local)
     sms = torch.cuda.get_device_properties(local).multi_processor_count
-    max_mhz = 1965.0
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            max_mhz = float(json.load(fh).get("sm_max_mhz", max_mhz))
-    except (OSError, ValueError):
-        pass
-    peak = sms * 128 * max_mhz * 1e6 / 1e9  # Glane-op/s
+    peak, peak_src = issue_peak(sms)
+    achieved = ct_rank_launch * ops / (k_ms / 1e3) / 1e9
+    traffic, traffic_src = load_traffic()
 
     line = None
     if rank == 0:
-        # e2e through the public API (host buffers; agent stream advance + H2D params + D2H tally)
-        import random
-
-        def time_calls(mode, steps):
-            agent = random.Random(11)
-            ts = []
-            for i in range(args.warmup + steps):
-                torch.cuda.synchronize()
-                t0 = time.perf_counter()
-                probs = rp_predict(state, cfg, sims, agent, mode=mode)
-                ts.append(time.perf_counter() - t0)
-            assert abs(sum(probs) - 1.0) < 1e-9
-            return statistics.mean(ts[args.warmup:])
-
-        e2e_s = time_calls("native", args.steps)
-        # one H2D per call: the race-parameter block (64-byte aligned) followed by the zeroed tally
-        h2d = ((int(sim.lib().bbe_param_bytes(n)) + 63) // 64) * 64 + launcher.tally_len * 8
-        d2h = launcher.tally_len * 8
-        # MT mode: the reference's own MT19937 streams, bit-identical results (seeds are H2D inputs)
-        mt_steps = max(3, min(args.steps, 20))
-        e2e_mt_s = time_calls("mt", mt_steps)
-        # device time of one MT batch of the same size (seeding + race kernels, one stream, CUDA events)
-        mt_seeds = np.arange(1, sims + 1, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
-        mt_kernel_ms = min(sim.simulate_batch(state, cfg, sims, mode="mt", seeds=mt_seeds, ranks=False).kernel_ms
-                           for _ in range(3))
-
-        sweep = sweep_configs(args, torch, sim) if args.sweep else None
-        cpu = cpu_baseline_pyref(cfg, state, args.cpu_sample) if args.cpu_sample else None
-        cpu_c = cpu_baseline_c(cfg, state, args.cpu_c_sample) if args.cpu_c_sample else None
+        sweep = sweep_configs(args, torch, sim) if (args.sweep and world == 1) else None
+        cpu = cpu_baseline_reference(cfg, args.cpu_sample) if (args.cpu_sample and world == 1) else None
+        cpu_c = cpu_baseline_c(cfg, args.cpu_c_sample) if (args.cpu_c_sample and world == 1) else None
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "C2: derby10 mid-race (tick 65) continuation, one rp_predict call = "
-                                   f"{sims} dry runs per GPU", "competitors": n, "sims_per_gpu_per_step": sims,
-                       "rng": "philox4x32-10", "l2": "flushed between timed steps (256 MB write)",
-                       "parallelism": f"dp{world} (disjoint sim index shards + NCCL tally all-reduce)"},
-            "ct_per_s": ct_per_s,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": job_config(args.c5_sims, world),
+            "ct_per_s": ct_per_s, "races_per_s_per_gpu": value / world,
             "roofline": {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "Glane-op/s",
-                         "frac": achieved / peak, "traffic": load_traffic(),
+                         "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": traffic_src or "no committed capture",
                          "ops_per_ct": ops, "f_free": f_free, "kernel_ms": k_ms,
-                         "peak_source": f"{sms} SMs x 128 FP32/INT32 lanes x {max_mhz:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)"},
-            "e2e": {"value": sims / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "api": "paper_2108_02419_b200.agents.rp_predict(mode='native')", "ms_per_call": e2e_s * 1e3},
-            "mt_exact": {"e2e_value": sims / e2e_mt_s, "unit": UNIT, "ms_per_call": e2e_mt_s * 1e3,
-                         "device_ms": mt_kernel_ms, "h2d_bytes_per_step": h2d + 8 * sims, "d2h_bytes_per_step": d2h,
-                         "api": "rp_predict(mode='mt'): bit-identical to the reference for the same seeds"},
+                         "ct_per_launch": ct_rank_launch, "kernel": "native64_kernel<K=2, scan-free>",
+                         "peak_source": peak_src},
+            "e2e": {"value": args.c5_sims / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "paper_2108_02419_b200.parallel.simulate_sharded(None, config, 1e9, seed, mode='native64')",
+                    "ms_per_call": e2e_s * 1e3, "calls": e2e_steps},
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "cpu_baseline_c": cpu_c,
-            "device": name,
+            "device": torch.cuda.get_device_name(local),
             "other_configs": sweep,
         }
     if world > 1:
@@ -405,24 +622,28 @@ def run_ours(args):
     return 0
 
 
-def main():
+def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=300)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--sims", type=int, default=SIMS_PER_CALL)
-    ap.add_argument("--cpu-sample", type=int, default=10000, help="pyref sims for cpu_baseline (0 = skip)")
-    ap.add_argument("--cpu-c-sample", type=int, default=200_000, help="C oracle sims (0 = skip)")
-    ap.add_argument("--ref-sample", type=int, default=2000, help="sims per --impl reference step")
+    ap.add_argument("--c5-sims", type=int, default=C5_SIMS, help="simulations per step, over all ranks")
+    ap.add_argument("--e2e-steps", type=int, default=3, help="public-API calls timed for e2e (each is a full step)")
+    ap.add_argument("--cpu-sample", type=int, default=2000, help="reference races for cpu_baseline (0 = skip)")
+    ap.add_argument("--cpu-c-sample", type=int, default=100_000, help="C oracle races (0 = skip)")
+    ap.add_argument("--ref-sample", type=int, default=0, help="races per --impl reference step (0 = 320 x cores)")
     ap.add_argument("--sweep", type=int, default=1, help="also time the other BASELINE configs (0 = skip)")
     ap.add_argument("--c3-sims", type=int, default=10_000_000)
-    ap.add_argument("--c5-sims", type=int, default=1_000_000_000, help="C5 on this GPU (the per-GPU shard)")
-    args = ap.parse_args()
+    ap.add_argument("--c4-max-d", type=int, default=100_000, help="largest C4 session d to run")
+    argv = sys.argv[1:] if argv is None else argv
+    args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup < 3 requested; timing rules want >= 3", file=sys.stderr)
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "RANK" not in os.environ:
+        return subprocess.call(spawn_command(args.gpus, argv, free_port()))
     return run_ours(args)
 
 

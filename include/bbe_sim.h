@@ -30,7 +30,7 @@
  *
  * Return codes: BBE_OK, BBE_EINVAL (-> RaceConfigError), BBE_EDIVERGED (-> RaceDivergedError /
  * BatchRunError(first_diverged)), BBE_EDRAWS (inject stream under/over-consumed), BBE_ECUDA,
- * BBE_ENODEV.
+ * BBE_ENODEV, BBE_ENCCL (the multi-GPU tally all-reduce failed, or libnccl is not loadable).
  */
 #ifndef BBE_SIM_H
 #define BBE_SIM_H
@@ -51,7 +51,8 @@ enum {
     BBE_EDIVERGED = 2,
     BBE_EDRAWS = 3,
     BBE_ECUDA = 4,
-    BBE_ENODEV = 5
+    BBE_ENODEV = 5,
+    BBE_ENCCL = 6
 };
 
 /* Random-draw source. */
@@ -149,11 +150,17 @@ int bbe_simulate(const bbe_race* race, const bbe_competitor* comps, const bbe_st
 
 /* bbe_simulate over several GPUs from one host thread -- the run_batch(workers=N) analogue
  * (batch.py:110-124): the sims are split into `n_parts` contiguous shards (shard_range), part p runs
- * on device p % bbe_device_count() in its own host thread (parts on one device run in turn), and
- * the tallies are merged on the host (SUM; first_diverged / first_bad_draws keep the smallest
- * index).  Per-sim outputs land at their global positions in `out`.  Every per-sim stream is a pure
+ * on device p % bbe_device_count() in its own host thread (parts on one device run in turn).
+ * Tally-only requests (no per-sim output buffers; NATIVE, NATIVE64, or MT with seeds derived from
+ * seed_master): each device adds its parts
+ * into one device tally on its own stream, and ONE grouped NCCL all-reduce over the devices (SUM of
+ * the counters fused with a MAX of the encoded first-failure fields) combines them over NVLink /
+ * NVSwitch -- the SURVEY 8(b)/(e) contract; device 0's tally is the only D2H copy (BBE_ENCCL when
+ * the collective fails).  Requests with per-sim outputs (or host-memory draws / seeds)
+ * write those outputs at their global positions from each part and merge the tallies on the host
+ * (SUM; first_diverged / first_bad_draws keep the smallest index).  Every per-sim stream is a pure
  * function of the global sim index, so results are identical for any n_parts.  n_parts <= 0 -> one
- * part per visible device.  kernel_ms = the slowest part. */
+ * part per visible device.  kernel_ms = the slowest device. */
 int bbe_simulate_multi(int32_t n_parts, const bbe_race* race, const bbe_competitor* comps, const bbe_state* state,
                        const bbe_request* req, bbe_result* out);
 

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl is dlopen'ed (nccl_api)
 #ifdef BBE_TIMING
 #include <chrono>
 #endif
@@ -1363,6 +1364,72 @@ static void rewind_stream(const uint32_t* saved624, int32_t saved_pos, int64_t f
     *pos = (int32_t)bbe_host_mt_getrandbits64(state624, (uint32_t)saved_pos, first_div + 1, nullptr, 0);
 }
 
+// ---- NCCL (single process, every visible GPU): the tally all-reduce of bbe_simulate_multi ----
+// NCCL is dlopen'ed (RTLD_NOLOAD first: a process running torch already holds its libnccl, and one
+// process must not load two).  Types come from nccl.h; nothing links against libnccl.
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    decltype(&ncclCommInitAll) init = nullptr;
+    decltype(&ncclAllReduce) allreduce = nullptr;
+    decltype(&ncclGroupStart) group_start = nullptr;
+    decltype(&ncclGroupEnd) group_end = nullptr;
+    decltype(&ncclGetErrorString) error = nullptr;
+};
+
+static const NcclApi& nccl_api() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            a.why = std::string("libnccl.so.2 not loadable: ") + dlerror();
+            return a;
+        }
+        a.init = (decltype(a.init))dlsym(h, "ncclCommInitAll");
+        a.allreduce = (decltype(a.allreduce))dlsym(h, "ncclAllReduce");
+        a.group_start = (decltype(a.group_start))dlsym(h, "ncclGroupStart");
+        a.group_end = (decltype(a.group_end))dlsym(h, "ncclGroupEnd");
+        a.error = (decltype(a.error))dlsym(h, "ncclGetErrorString");
+        a.ok = a.init && a.allreduce && a.group_start && a.group_end && a.error;
+        if (!a.ok) a.why = "libnccl.so.2 lacks the collective entry points";
+        return a;
+    }();
+    return api;
+}
+
+// One communicator clique per device count (devices 0..k-1), created once and kept for the process.
+static std::mutex g_nccl_mu;
+static std::map<int, std::vector<ncclComm_t>> g_nccl_comms;
+
+static int nccl_comms(int k, std::vector<ncclComm_t>** out) {
+    const NcclApi& api = nccl_api();
+    if (!api.ok) return fail(BBE_ENCCL, api.why);
+    std::lock_guard<std::mutex> g(g_nccl_mu);
+    auto it = g_nccl_comms.find(k);
+    if (it == g_nccl_comms.end()) {
+        std::vector<ncclComm_t> comms(k);
+        std::vector<int> devs(k);
+        for (int i = 0; i < k; ++i) devs[i] = i;
+        const ncclResult_t r = api.init(comms.data(), k, devs.data());
+        if (r != ncclSuccess) return fail(BBE_ENCCL, std::string("ncclCommInitAll: ") + api.error(r));
+        it = g_nccl_comms.emplace(k, std::move(comms)).first;
+    }
+    *out = &it->second;
+    return BBE_OK;
+}
+
+// Per-device state of a tally-only multi-GPU call: the device tally every part on that device adds
+// into, its stream, and events around the device's work.
+struct MultiDev {
+    cudaStream_t s = nullptr;
+    uint64_t* d_tally = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    int rc = BBE_OK;
+    std::string err;
+};
+
 extern "C" {
 
 int bbe_rp_predict(const bbe_race* race, const bbe_competitor* comps, const bbe_state* st, int64_t d, int32_t mode,
@@ -1510,7 +1577,117 @@ int bbe_simulate_multi(int32_t n_parts, const bbe_race* race, const bbe_competit
             P.res.traj_prev_steps = out->traj_prev_steps + a * traj_stride;
         }
     }
-    // one host thread per device; a device's parts run in order on that thread
+    // Tally-only requests (no per-sim outputs; NATIVE, NATIVE64, or MT with device-derived run seeds):
+    // every device adds its parts
+    // into one device tally on its own stream, then ONE grouped NCCL all-reduce (SUM over the counters,
+    // MAX over the two complement-encoded "first failing sim" fields, fused by ncclGroupStart/End)
+    // combines them over NVLink; device 0's tally is the only D2H copy.
+    const bool tally_only = !out->winner && !out->order && !out->finish_ticks && !out->final_positions &&
+                            !out->blocked && !out->draws_used && !out->traj_positions && !out->group_wins &&
+                            rq->mode != BBE_MODE_INJECT && !(rq->mode == BBE_MODE_MT && rq->seeds);
+    if (tally_only) {
+        const int used = std::min(ndev, n_parts);
+        const TallyLayout T{n, nperm_for(n)};
+        const int64_t tl = T.len();
+        std::vector<MultiDev> md(used);
+        auto run_dev = [&](int d) {
+            MultiDev& M = md[d];
+            auto ok = [&](cudaError_t e, const char* what) {
+                if (e != cudaSuccess && M.rc == BBE_OK) {
+                    M.rc = BBE_ECUDA;
+                    M.err = std::string(what) + ": " + cudaGetErrorString(e);
+                }
+                return e == cudaSuccess;
+            };
+            if (!ok(cudaSetDevice(d), "cudaSetDevice") ||
+                !ok(cudaStreamCreateWithFlags(&M.s, cudaStreamNonBlocking), "cudaStreamCreate") ||
+                !ok(cudaEventCreate(&M.e0), "cudaEventCreate") || !ok(cudaEventCreate(&M.e1), "cudaEventCreate") ||
+                !ok(cudaMallocAsync((void**)&M.d_tally, tl * sizeof(uint64_t), M.s), "cudaMallocAsync") ||
+                !ok(cudaMemsetAsync(M.d_tally, 0, tl * sizeof(uint64_t), M.s), "cudaMemsetAsync") ||
+                !ok(cudaEventRecord(M.e0, M.s), "cudaEventRecord"))
+                return;
+            for (int p = d; p < n_parts; p += ndev) {
+                if (parts[p].rq.n_sims == 0) continue;
+                const int r = bbe_simulate_async(race, comps, st, &parts[p].rq, nullptr, M.d_tally, M.s);
+                if (r != BBE_OK) {
+                    M.rc = r;
+                    M.err = bbe_last_error();
+                    return;
+                }
+            }
+            ok(cudaEventRecord(M.e1, M.s), "cudaEventRecord");
+        };
+        int caller = 0;
+        cudaGetDevice(&caller);
+        {
+            std::vector<std::thread> th;
+            for (int d = 1; d < used; ++d) th.emplace_back(run_dev, d);
+            run_dev(0);
+            for (auto& t : th) t.join();
+        }
+        int rc2 = BBE_OK;
+        std::string err2;
+        for (const MultiDev& M : md)
+            if (M.rc != BBE_OK && rc2 == BBE_OK) { rc2 = M.rc; err2 = M.err; }
+        if (rc2 == BBE_OK && used > 1) {
+            std::vector<ncclComm_t>* comms = nullptr;
+            if ((rc2 = nccl_comms(used, &comms)) != BBE_OK) {
+                err2 = g_err;
+            } else {
+                const NcclApi& api = nccl_api();
+                const int64_t nsum = T.ct() + 4;  // wins, ranks, perms, ct, blocked, n_div, n_bad
+                api.group_start();
+                for (int d = 0; d < used; ++d) {
+                    api.allreduce(md[d].d_tally, md[d].d_tally, nsum, ncclUint64, ncclSum, (*comms)[d], md[d].s);
+                    api.allreduce(md[d].d_tally + nsum, md[d].d_tally + nsum, 2, ncclUint64, ncclMax, (*comms)[d], md[d].s);
+                }
+                const ncclResult_t r = api.group_end();
+                if (r != ncclSuccess) { rc2 = BBE_ENCCL; err2 = std::string("ncclAllReduce: ") + api.error(r); }
+            }
+        }
+        std::vector<uint64_t> h(tl, 0);
+        float kms = 0.f;
+        if (rc2 == BBE_OK) {
+            cudaSetDevice(0);
+            cudaError_t e = cudaMemcpyAsync(h.data(), md[0].d_tally, tl * sizeof(uint64_t), cudaMemcpyDeviceToHost, md[0].s);
+            for (int d = 0; d < used && e == cudaSuccess; ++d) {
+                cudaSetDevice(d);
+                e = cudaStreamSynchronize(md[d].s);
+                float ms = 0.f;
+                if (e == cudaSuccess && cudaEventElapsedTime(&ms, md[d].e0, md[d].e1) == cudaSuccess) kms = std::max(kms, ms);
+            }
+            if (e != cudaSuccess) { rc2 = BBE_ECUDA; err2 = std::string("multi-GPU tally: ") + cudaGetErrorString(e); }
+        }
+        for (int d = 0; d < used; ++d) {  // release (after a failure too)
+            cudaSetDevice(d);
+            if (md[d].s) cudaStreamSynchronize(md[d].s);
+            if (md[d].d_tally) cudaFree(md[d].d_tally);
+            if (md[d].s) cudaStreamDestroy(md[d].s);
+            if (md[d].e0) cudaEventDestroy(md[d].e0);
+            if (md[d].e1) cudaEventDestroy(md[d].e1);
+        }
+        cudaGetLastError();
+        cudaSetDevice(caller);
+        if (rc2 != BBE_OK) return fail(rc2, err2);
+        std::copy(h.begin(), h.begin() + n, out->wins);
+        if (out->ranks) std::copy(h.begin() + T.ranks(), h.begin() + T.ranks() + (size_t)n * n, out->ranks);
+        if (nperm) std::copy(h.begin() + T.perms(), h.begin() + T.perms() + nperm, out->perms);
+        out->competitor_steps = h[T.ct()];
+        out->blocked_steps = h[T.ct() + 1];
+        auto first = [](uint64_t v) -> int64_t { return v == 0 ? -1 : (int64_t)(0x7fffffffffffffffull - v); };
+        out->first_diverged = first(h[T.ct() + 4]);
+        out->first_bad_draws = first(h[T.ct() + 5]);
+        out->kernel_ms = kms;
+        out->lanes_per_slot = 0;
+        if (h[T.ct() + 2])
+            return fail(BBE_EDIVERGED, "race exceeded tick_limit=" + std::to_string(race->tick_limit) + " in sim " +
+                                           std::to_string(out->first_diverged));
+        if (h[T.ct() + 3])
+            return fail(BBE_EDRAWS, "draw stream under/over-consumed in sim " + std::to_string(out->first_bad_draws));
+        return BBE_OK;
+    }
+    // per-sim outputs (or host-memory draws / seeds): one host thread per device; a
+    // device's parts run in order on that thread, each with its own host outputs, merged below
     auto run_device = [&](int d) {
         if (cudaSetDevice(d) != cudaSuccess) {
             cudaGetLastError();

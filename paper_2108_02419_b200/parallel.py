@@ -125,8 +125,8 @@ def simulate_sharded(state, config, n_sims: int, seed: int = 0, *, group=None, l
     """A batch over all ranks of ``group`` (one GPU per rank, NCCL).
 
     Each rank simulates its contiguous shard of [0, n_sims) with global sim indices, the device
-    tallies are all-reduced, and every rank returns the job total.  mode="native": Philox keyed by
-    ``seed``; mode="mt": sim i replays the reference's stream random.Random(derive_seed(seed, "run", i))
+    tallies are all-reduced, and every rank returns the job total.  mode="native64" (FP64 state) /
+    "native" (FP32 state): Philox keyed by ``seed``; mode="mt": sim i replays the reference's stream random.Random(derive_seed(seed, "run", i))
     -- run_batch's seeds (batch.py:117-119), so the total equals the reference's batch tallies.
     """
     import torch
@@ -137,7 +137,8 @@ def simulate_sharded(state, config, n_sims: int, seed: int = 0, *, group=None, l
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     lo, hi = shard_range(int(n_sims), rank, world)
-    launcher = DeviceLauncher(state, config, lanes_per_slot=lanes_per_slot)
+    launcher = DeviceLauncher(state, config, lanes_per_slot=lanes_per_slot,
+                              native_mode=mode if mode in ("native", "native64") else "native")
     layout = TallyLayout.for_n(len(config.competitors))
     assert layout.length == launcher.tally_len
     tally = torch.zeros(layout.length, dtype=torch.int64, device="cuda")

@@ -258,6 +258,35 @@ def import_racemarket():
     return racemarket
 
 
+def to_reference_race(config):
+    """This package's RaceConfig as a ``racemarket.race.RaceConfig`` (same fields; race.py:99-189).
+    A racemarket config is returned unchanged."""
+    rm = import_racemarket()
+    R = rm.race
+    if isinstance(config, R.RaceConfig):
+        return config
+    comps = []
+    for c in config.competitors:
+        s = c.steps
+        steps = (R.LogNormalSteps(s.mu, s.sigma, s.scale) if hasattr(s, "mu") else R.UniformSteps(s.lo, s.hi))
+        r = c.responsiveness
+        comps.append(R.Competitor(c.cid, steps, c.preference, c.pref_sensitivity, c.theta,
+                                  R.Responsiveness(r.early_mult, r.late_mult, r.breakpoint)))
+    bc = config.betting_close
+    return R.RaceConfig(config.track_length, tuple(comps), dt=config.dt, conditions=config.conditions,
+                        betting_close=R.BettingClose(bc.rule, bc.k), tick_limit=config.tick_limit)
+
+
+def c4_session_config(race, *, n_agents: int = 100, d: int = 1000, master_seed: int = 20260818,
+                      opening_period: float = 5.0, strategy: str = "rp"):
+    """``SessionConfig(race, (AgentParams(strategy, count=n_agents, d=d,
+    reevaluate_every=1.0, wake_jitter=1.0),), master_seed, opening_period=5.0)``."""
+    rm = import_racemarket()
+    group = rm.agents.AgentParams(strategy, count=n_agents, d=d, reevaluate_every=1.0, wake_jitter=1.0)
+    return rm.session.SessionConfig(race=to_reference_race(race), agent_groups=(group,), master_seed=master_seed,
+                                    opening_period=opening_period)
+
+
 @dataclass
 class SessionStats:
     launches: int = 0          # batched prediction launches

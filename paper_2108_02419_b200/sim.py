@@ -31,7 +31,7 @@ from .race import (
 _LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
 LIB_PATH = os.environ.get("BBE_LIB") or os.path.join(_LIB_DIR, "libbbe_sim.so")  # BBE_LIB: A/B builds
 
-BBE_OK, BBE_EINVAL, BBE_EDIVERGED, BBE_EDRAWS, BBE_ECUDA, BBE_ENODEV = range(6)
+BBE_OK, BBE_EINVAL, BBE_EDIVERGED, BBE_EDRAWS, BBE_ECUDA, BBE_ENODEV, BBE_ENCCL = range(7)
 MODES = {"native": 0, "inject": 1, "mt": 2, "native64": 3}
 MAX_COMPETITORS = 128
 MAX_PERM_COMPETITORS = 6

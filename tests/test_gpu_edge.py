@@ -197,6 +197,23 @@ def test_multi_part_split_is_invisible(mode):
     assert e.value.sim_index == 40
 
 
+@pytest.mark.parametrize("mode", ["native", "native64", "mt"])
+def test_multi_tally_only_device_path(mode):
+    """bbe_simulate_multi without per-sim outputs: every part adds into one device tally per GPU and
+    the devices are combined by one grouped NCCL all-reduce (one GPU here: the device accumulation,
+    no collective) -- tallies equal one launch's bit for bit, with perms, for any number of parts;
+    MT derives run seeds on the device (seed_master) like run_batch."""
+    cfg = _mixed_field(5)
+    n_sims = 20_011
+    kw = dict(seed_master=4321) if mode == "mt" else {}
+    one = sim.simulate_batch(None, cfg, n_sims, 3, mode=mode, perms=True, **kw)
+    for parts in (1, 2, 7):
+        r = sim.simulate_batch(None, cfg, n_sims, 3, mode=mode, perms=True, parts=parts, **kw)
+        assert (r.wins == one.wins).all() and (r.ranks == one.ranks).all() and (r.perms == one.perms).all()
+        assert r.competitor_steps == one.competitor_steps and r.blocked_steps == one.blocked_steps
+        assert r.kernel_ms > 0
+
+
 @pytest.mark.parametrize("mode", ["native", "mt"])
 def test_group_wins_equal_per_group_winner_counts(mode):
     """req.group_size: per-group winner counts from the kernel equal the host split of the per-sim

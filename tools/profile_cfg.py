@@ -2,7 +2,7 @@
 
 usage: python tools/profile_cfg.py FIELD MODE [sims] [reps]
   FIELD: c1 (5 x U(10,20) from the start), c2 (derby10 mid-race), c3 (20 x U(10,20) from the start),
-         derby20 (derby.json resized to 20, from the start)
+         derby20 (derby.json resized to 20, from the start), c5 (= the c3 field)
   MODE:  native | native64
 """
 import os
@@ -27,7 +27,7 @@ def field(name):
         return state_from_dict(g["state"]), derby10
     if name == "derby20":
         return None, resize_race(resize_race(derby10, 5), 20)
-    n = {"c1": 5, "c3": 20}[name]
+    n = {"c1": 5, "c3": 20, "c5": 20}[name]
     return None, RaceConfig(2000.0, tuple(Competitor(f"c{i + 1}", UniformSteps(10.0, 20.0)) for i in range(n)))
 
 
