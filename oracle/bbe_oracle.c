@@ -215,10 +215,9 @@ void orc_philox4x32_10(const uint32_t* ctr_in, uint64_t key, uint32_t* out) {
     out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
 }
 
-/* CPython's random_random() formula applied to two words: a 53-bit fraction in [0, 1) */
-static double res53(uint32_t w0, uint32_t w1) {
-    uint32_t a = w0 >> 5, b = w1 >> 6;
-    return (a * 67108864.0 + b) * (1.0 / 9007199254740992.0);
+/* NATIVE64's draw of two words (common.cuh unit53): the top 53 bits of w0:w1 times 2^-53 */
+static double unit53(uint32_t w0, uint32_t w1) {
+    return (double)((((uint64_t)w0 << 32) | w1) >> 11) * (1.0 / 9007199254740992.0);
 }
 
 /* Draw source: an MT stream (the reference), a replay of recorded draw values, or the NATIVE64
@@ -237,17 +236,17 @@ typedef struct {
 } orc_draws;
 
 /* NATIVE64 draw (native64_kernel.cuh): counter (rt / 2, c, gs) -- word 0 = 0xFFFFFFFF for the
- * priming draws -- gives (x, y, z, w); a uniform takes lo + (hi - lo) * random53 of (x, y) at even
+ * priming draws -- gives (x, y, z, w); a uniform takes lo + (hi - lo) * unit53 of (x, y) at even
  * rt and (z, w) at odd rt; a lognormal takes scale * exp(mu + z * sigma) with the Box-Muller normal
- * of u1 = 1 - random53(x, y), u2 = random53(z, w): the cosine branch at even rt, the sine at odd. */
+ * of u1 = 1 - unit53(x, y), u2 = unit53(z, w): the cosine branch at even rt, the sine at odd. */
 static double draw_philox(const orc_draws* d, const orc_comp* cp, int c) {
     uint32_t ctr[4] = {d->rt < 0 ? 0xFFFFFFFFu : (uint32_t)(d->rt >> 1), (uint32_t)c, (uint32_t)d->gs,
                        (uint32_t)(d->gs >> 32)};
     uint32_t w[4];
     orc_philox4x32_10(ctr, d->key, w);
     int odd = d->rt >= 0 && (d->rt & 1);
-    if (cp->family == 0) return cp->lo + (cp->hi - cp->lo) * (odd ? res53(w[2], w[3]) : res53(w[0], w[1]));
-    double u1 = 1.0 - res53(w[0], w[1]), u2 = res53(w[2], w[3]);
+    if (cp->family == 0) return cp->lo + (cp->hi - cp->lo) * (odd ? unit53(w[2], w[3]) : unit53(w[0], w[1]));
+    double u1 = 1.0 - unit53(w[0], w[1]), u2 = unit53(w[2], w[3]);
     double r = sqrt(-2.0 * log(u1));
     double t = 3.141592653589793 * (2.0 * u2);
     double z = odd ? r * sin(t) : r * cos(t);

@@ -155,6 +155,16 @@ __device__ __forceinline__ double random53(uint32_t w0, uint32_t w1) {
     return __fma_rn(E, 1.0 / 9007199254740992.0, top);
 }
 
+// NATIVE64 draws: u = m * 2^-53, m = the top 53 bits of the 64-bit word pair (w0:w1) -- uniform on
+// the reference's grid k * 2^-53 (random.random()'s resolution), with fewer operations than
+// random53: H = 0.5 + (m mod 2^52) * 2^-53 is built from bits, and u = H - 0.5 + m_52 / 2 is one
+// exact DADD (Sterbenz when m_52 = 0).  oracle/bbe_oracle.c unit53 is the same formula.
+__device__ __forceinline__ double unit53(uint32_t w0, uint32_t w1) {
+    const uint32_t lo = __funnelshift_r(w1, w0, 11);            // m bits 0..31
+    const uint32_t hi = 0x3FE00000u | ((w0 >> 11) & 0xFFFFFu);  // m bits 32..51 under 2^-1
+    return __dadd_rn(__hiloint2double((int)hi, (int)lo), (w0 >> 31) ? 0.0 : -0.5);
+}
+
 template <typename T>
 __device__ __forceinline__ T shfl(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 

@@ -18,9 +18,9 @@
 // request seed with counter (tick / 2, competitor, global sim index), instead of a per-sim MT19937.
 //
 // Draws.  One Philox call per competitor per two ticks gives words (x, y, z, w).  A uniform step takes
-// random() = ((x >> 5) * 2^26 + (y >> 6)) * 2^-53 for the even tick and (z, w) for the odd one --
-// CPython's random_random() formula on Philox words, 53-bit resolution as the reference's.  A
-// lognormal step takes a Box-Muller normal from u1 = 1 - random(x, y), u2 = random(z, w) (the cosine
+// lo + (hi - lo) * u with u = unit53(x, y) = (the top 53 bits of x:y) * 2^-53 for the even tick and
+// unit53(z, w) for the odd one -- random()'s 53-bit grid, as the reference's.  A lognormal step
+// takes a Box-Muller normal from u1 = 1 - unit53(x, y), u2 = unit53(z, w) (the cosine
 // branch for the even tick, the sine branch for the odd one): the reference's Kinderman-Monahan loop
 // needs a variable number of words, which a counter-based stream replaces by the same N(0, 1) law.
 // Priming draws (run_race) use counter word 0 = 0xFFFFFFFF.
@@ -67,11 +67,17 @@ struct CBool {
 #ifndef BBE_N64_MINBLOCKS_KN
 #define BBE_N64_MINBLOCKS_KN 4
 #endif
+// Tick pairs per iteration of the draw-staging loop: 2 (two Philox chains per slot in flight) for
+// K <= 2, except the wide-row scan layouts, where the registers cost more than the ILP gains (A/B round 2, ms per
+// launch, 1 -> 2: C3/C5 field 58.04 -> 54.91, C2 0.685 -> 0.667, derby20 33.36 -> 34.44).
+#ifndef BBE_N64_DRAW_UNROLL
+#define BBE_N64_DRAW_UNROLL 0  // 0 = the rule above; else forced (A/B builds)
+#endif
 
 // Box-Muller: two independent N(0, 1) from four words; u1 in (0, 1], u2 in [0, 1).
 __device__ __forceinline__ void normal_pair64(const U4& w, double& n0, double& n1) {
-    const double u1 = __dsub_rn(1.0, random53(w.x, w.y));
-    const double u2 = random53(w.z, w.w);
+    const double u1 = __dsub_rn(1.0, unit53(w.x, w.y));
+    const double u2 = unit53(w.z, w.w);
     const double r = sqrt(__dmul_rn(-2.0, log(u1)));
     double s, c;
     sincospi(__dmul_rn(2.0, u2), &s, &c);
@@ -192,8 +198,8 @@ native64_kernel(const LaunchArgs a) {
     // the uniform step draws of slot k for ticks 2h and 2h + 1 of the sim (counter word 0 = h)
     auto draw_pair = [&](int k, uint32_t h, uint64_t gs, double& d0, double& d1) {
         const U4 w = philox_rk(U4{h, (uint32_t)cidx[k], (uint32_t)gs, (uint32_t)(gs >> 32)}, a.rk);
-        d0 = __dadd_rn(lo[k], __dmul_rn(span[k], random53(w.x, w.y)));
-        d1 = __dadd_rn(lo[k], __dmul_rn(span[k], random53(w.z, w.w)));
+        d0 = __dadd_rn(lo[k], __dmul_rn(span[k], unit53(w.x, w.y)));
+        d1 = __dadd_rn(lo[k], __dmul_rn(span[k], unit53(w.z, w.w)));
     };
 
     auto load_sim = [&](bool do_it) {
@@ -320,7 +326,8 @@ native64_kernel(const LaunchArgs a) {
         // ---- the block's draws: NT per slot, into this lane's shared-memory column ----
         {
             const uint64_t gs = (uint64_t)(a.sim_offset + s);
-#pragma unroll 1
+            constexpr int DU = BBE_N64_DRAW_UNROLL ? BBE_N64_DRAW_UNROLL : ((K <= 2 && (!SCAN || CH <= 3)) ? 2 : 1);
+#pragma unroll DU
             for (int h = 0; h < NT / 2; ++h) {
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
