@@ -73,10 +73,12 @@ exact_kernel(const LaunchArgs a) {
     uint32_t* const smem_w = reinterpret_cast<uint32_t*>(s_dyn);
     uint32_t* const seg_mt = smem_w + (warp * S + (lane_on ? seg : 0)) * kSeg;
     uint32_t* const mt = seg_mt + kSide;  // the 624-word MT19937 block
-    // start-of-tick positions, per warp: [parity][slot][segment * WP2 + lane-in-segment], pads -inf
-    const int WP2 = (W + 1) & ~1;
+    // start-of-tick front-runner keys, per warp: [parity][slot] rows of kKRow words, segment at
+    // seg * WPK (4-word chunks, padding words 0), idle lanes write the row's last word
+    const int CHK = (W + 3) >> 2, WPK = 4 * CHK;
     double* const xrows_all = reinterpret_cast<double*>(smem_w + (MODE == MT ? kWarpsPerBlock * S * kSeg : 0));
-    double* const xrows = xrows_all + warp * 2 * K * kXSlot;
+    uint32_t* const krows = reinterpret_cast<uint32_t*>(xrows_all + warp * 2 * K * kXSlot);
+    constexpr int kKRow = 2 * kXSlot;  // words per key row (the double row's footprint; S * WPK <= 36)
     // MT, K = 1: the round's pending lognormal draws publish their speculative word offsets here, by
     // rank in their segment (lane base + rank), for the lanes that evaluate their trials
     int* const ln_off_all = reinterpret_cast<int*>(xrows_all + kWarpsPerBlock * 2 * K * kXSlot);
@@ -85,9 +87,11 @@ exact_kernel(const LaunchArgs a) {
     // in one bin is at most the sims of its launch, which the host keeps below 2^32 (launch_one).
     uint32_t* const s_hist = reinterpret_cast<uint32_t*>(ln_off_all + (MODE == MT ? kWarpsPerBlock * kWarp : 0));
     for (int i = threadIdx.x; i < hist_len; i += blockDim.x) s_hist[i] = 0u;
-    for (int i = lane; i < 2 * K * kXSlot; i += kWarp) xrows[i] = -CUDART_INF;
-    const int xseg = lane_on ? seg * WP2 : 0;
-    double* const xw = xrows + (lane_on ? seg * WP2 + l : kXSlot - 1);
+    for (int i = lane; i < 2 * K * kKRow; i += kWarp) krows[i] = 0u;
+    uint32_t* const kw = krows + (lane_on ? seg * WPK + l : kKRow - 1);
+    const uint32_t* const kr = krows + (lane_on ? seg * WPK : 0);
+    const double C64 = a.key_c64;
+    const uint32_t cl = (uint32_t)l - a.key_sub64;  // v = funnel * 32 + cl = (key << 5) | l
     __syncthreads();
 
     // ---- per-slot constants (the lane->competitor map is fixed for the kernel) ----
@@ -131,7 +135,7 @@ exact_kernel(const LaunchArgs a) {
     int wp = kSeg;                       // MT: start of the unread window seg_mt[wp, kSeg)
     bool running = false, diverged = false, bad = false;
 
-    double pos[K], prev[K], pv[K];
+    double pos[K], prev[K];
     int64_t fin[K];
     bool racing[K];
     uint32_t ct_sim = 0, blk_sim = 0;
@@ -439,11 +443,7 @@ exact_kernel(const LaunchArgs a) {
                 }
             }
         }
-        if (do_it) {
-#pragma unroll
-            for (int k = 0; k < K; ++k) pv[k] = racing[k] ? pos[k] : NEG_INF;
-            if (a.traj_pos && running) record(0);
-        }
+        if (do_it && a.traj_pos && running) record(0);
     };
 
     load_sim(true);
@@ -542,7 +542,7 @@ exact_kernel(const LaunchArgs a) {
         if (!__any_sync(0xffffffffu, running)) break;
 
         // ---------------- 4 synchronous ticks -------------------------------------------------------
-        __syncwarp();  // position rows: the previous block's reads precede this block's writes
+        __syncwarp();  // key rows: the previous block's reads precede this block's writes
         for (int tj = 0; tj < kTicksPerBlock; ++tj) {
             bool any_racing = false;
 #pragma unroll
@@ -555,80 +555,127 @@ exact_kernel(const LaunchArgs a) {
             if (seg_running && rt >= a.limit) {
                 diverged = true;
 #pragma unroll
-                for (int k = 0; k < K; ++k) { racing[k] = false; pv[k] = NEG_INF; }
+                for (int k = 0; k < K; ++k) racing[k] = false;
             }
 
-            // ---- front runner (race.py:244-264): gap = p_i - p_c, strict compares in index order ----
-            // Rounding is monotonic, so the reference's smallest gap min_i fl(p_i - p_c) over rivals
-            // strictly ahead equals fl(p* - p_c), p* = the smallest position strictly ahead: one pass
-            // over the segment's start-of-tick positions (shared memory, finished rivals as -inf) keeps
-            // p* and the lowest index holding it (strict compares in index order).  That index is the
-            // reference's front unless a rival further ahead has a gap that rounds to the same double;
-            // rival positions differ by >= ulp(p*), so that needs ulp(p*) <= ulp(gap), impossible when
-            // p* > 2 gap.  Blocked lanes outside that bound (only near a zero start line) rerun the
-            // reference's own gap arithmetic below.
-            double gap[K], best[K];
-            int bi[K];
+            // ---- front runner (race.py:244-264) ----
+            // Coarse keys, as native64_kernel.cuh: key = mantissa bits 51..26 of pos + C64 (the host's
+            // native64_frame puts every racing position of the race in one binade, so the key is a
+            // monotone function of the position).  Each lane publishes v = (key << 5) | lane and keeps
+            // one wrapped minimum of v_r + nk per rival (VIADDMNMX): the nearest rival after c in
+            // (key, index) order.  With all racing keys of the segment distinct that is exactly the
+            // reference's front (the smallest position strictly ahead, by its lowest index) and
+            // gap = fl(p_front - p_c) is the reference's smallest gap (rounding is monotonic).  Two
+            // racing competitors sharing a key always show up (the lower in (key, index) order finds
+            // the other with an equal key), and so does a blocked lane whose front could be a
+            // gap-rounding tie (distinct positions whose gaps round equal need p_front <= 2 gap); then
+            // the whole warp reruns the reference's own loop over the segment's FP64 positions.
+            double gap[K], pfp[K];
+            bool ahead[K];
+            int fk[K], fj[K];
 #pragma unroll
-            for (int k = 0; k < K; ++k) { gap[k] = CUDART_INF; best[k] = CUDART_INF; bi[k] = 0; }
-            double* const prow = xrows + (tj & 1) * K * kXSlot;
+            for (int k = 0; k < K; ++k) { gap[k] = CUDART_INF; pfp[k] = CUDART_INF; ahead[k] = false; fk[k] = 0; fj[k] = 0; }
+            const int par = (tj & 1) * K * kKRow;
             if (a.scan) {
+                uint32_t v[K];
 #pragma unroll
-                for (int k = 0; k < K; ++k) xw[(tj & 1) * K * kXSlot + k * kXSlot] = pv[k];
-                __syncwarp();
-#pragma unroll
-                for (int kk = 0; kk < K; ++kk) {
-                    const double2* r2 = reinterpret_cast<const double2*>(prow + kk * kXSlot + xseg);
-#pragma unroll 4
-                    for (int j = 0; j < WP2 / 2; ++j) {
-                        const double2 v = r2[j];
-#pragma unroll
-                        for (int k = 0; k < K; ++k) {
-                            if (v.x > pos[k] && v.x < best[k]) { best[k] = v.x; bi[k] = (kk << 5) | (2 * j); }
-                            if (v.y > pos[k] && v.y < best[k]) { best[k] = v.y; bi[k] = (kk << 5) | (2 * j + 1); }
-                        }
-                    }
+                for (int k = 0; k < K; ++k) {
+                    const double y = __dadd_rn(pos[k], C64);
+                    const uint32_t key = __funnelshift_r((uint32_t)__double2loint(y), (uint32_t)__double2hiint(y), 26);
+                    v[k] = key * 32u + cl;
+                    kw[par + k * kKRow] = racing[k] ? v[k] : 0u;
                 }
+                __syncwarp();
+                bool coll = false;
 #pragma unroll
-                for (int k = 0; k < K; ++k) gap[k] = best[k] < CUDART_INF ? __dsub_rn(best[k], pos[k]) : CUDART_INF;
-            }
-
-            // ---- step resolution (race.py:267-274) ----
-            bool fr[K], bl[K];
-            bool any_blocked = false, need_exact = false;
+                for (int k = 0; k < K; ++k) {
+                    uint32_t bestv = 0xffffffffu;
+                    int bestkk = 0;
+                    bool any = false;
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                // race.py:271: free when nobody is strictly ahead (front is None) -- tested explicitly, as
-                // gap = inf > theta fails for theta = inf or NaN -- or when gap > theta
-                fr[k] = racing[k] && (!(best[k] < CUDART_INF) || gap[k] > th[k]);
-                bl[k] = racing[k] && !fr[k];
-                any_blocked |= bl[k];
-                need_exact |= bl[k] && !(best[k] > __dmul_rn(2.0, gap[k]));
-            }
-            double pf[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) pf[k] = 0.0;
-            if (__any_sync(0xffffffffu, any_blocked)) {
-                if (__any_sync(0xffffffffu, need_exact)) {
-                    // the front: lowest index i (slot-major, then lane) with p_i > p_c and
-                    // fl(p_i - p_c) == gap -- race.py:244-264 verbatim, scanned from the top index down
-#pragma unroll
-                    for (int kk = K - 1; kk >= 0; --kk) {
-                        const double* r = prow + kk * kXSlot + xseg;
-                        for (int j = W - 1; j >= 0; --j) {
-                            const double pr = r[j];
-#pragma unroll
-                            for (int k = 0; k < K; ++k)
-                                if (pr > pos[k] && __dsub_rn(pr, pos[k]) == gap[k]) bi[k] = (kk << 5) | j;
+                    for (int kk = 0; kk < K; ++kk) {
+                        // t = v_r + nk is < 2^31 iff rival r follows c in (key, index) order: rows below
+                        // c's slot need a strictly larger key, c's own row a larger (key, lane), rows
+                        // above a key at least as large; finished lanes and padding publish 0
+                        const uint32_t nk = kk < k ? ~(v[k] | 31u) : (kk == k ? ~v[k] : 0u - (v[k] & ~31u));
+                        uint32_t b0 = 0xffffffffu, b1 = 0xffffffffu;
+                        const uint4* r4 = reinterpret_cast<const uint4*>(kr + par + kk * kKRow);
+#pragma unroll 3
+                        for (int c = 0; c < CHK; ++c) {
+                            const uint4 q = r4[c];
+                            b0 = min(b0, q.x + nk);
+                            b1 = min(b1, q.y + nk);
+                            b0 = min(b0, q.z + nk);
+                            b1 = min(b1, q.w + nk);
                         }
+                        const uint32_t t = min(b0, b1);
+                        const uint32_t vf = t - nk;
+                        if (t < 0x80000000u && (!any || (vf >> 5) < (bestv >> 5))) { bestv = vf; bestkk = kk; any = true; }
                     }
+                    ahead[k] = any;
+                    fk[k] = bestkk;
+                    fj[k] = (int)(bestv & 31u);
+                    coll |= racing[k] && any && (bestv >> 5) == (v[k] >> 5);
                 }
 #pragma unroll
                 for (int kk = 0; kk < K; ++kk) {
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
-                        const double v = shfl(prev[kk], base + (bi[k] & 31));
-                        pf[k] = ((bi[k] >> 5) == kk) ? v : pf[k];
+                        const double pr = shfl(pos[kk], base + fj[k]);
+                        pfp[k] = (K == 1 || fk[k] == kk) ? pr : pfp[k];
+                    }
+                }
+                bool need_exact = coll;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    gap[k] = ahead[k] ? __dsub_rn(pfp[k], pos[k]) : CUDART_INF;
+                    need_exact |= racing[k] && ahead[k] && !(gap[k] > th[k]) && !(pfp[k] > __dmul_rn(2.0, gap[k]));
+                }
+                if (__any_sync(0xffffffffu, need_exact)) {
+                    // race.py:244-264 verbatim over the segment's start-of-tick positions, in index order
+                    double bg[K];
+#pragma unroll
+                    for (int k = 0; k < K; ++k) { bg[k] = CUDART_INF; ahead[k] = false; }
+#pragma unroll
+                    for (int kk = 0; kk < K; ++kk) {
+                        for (int j = 0; j < W; ++j) {
+                            const double pr = shfl(pos[kk], base + j);
+                            const bool rr = shfl((int)racing[kk], base + j) != 0;
+#pragma unroll
+                            for (int k = 0; k < K; ++k) {
+                                if (rr && pr > pos[k]) {
+                                    const double g = __dsub_rn(pr, pos[k]);
+                                    if (!ahead[k] || g < bg[k]) { bg[k] = g; ahead[k] = true; fk[k] = kk; fj[k] = j; }
+                                }
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int k = 0; k < K; ++k) gap[k] = bg[k];
+                }
+            }
+
+            // ---- step resolution (race.py:267-274) ----
+            bool fr[K], bl[K];
+            bool any_blocked = false;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                // race.py:271: free when nobody is strictly ahead (front is None) -- tested explicitly, as
+                // gap = inf > theta fails for theta = inf or NaN -- or when gap > theta
+                fr[k] = racing[k] && (!ahead[k] || gap[k] > th[k]);
+                bl[k] = racing[k] && !fr[k];
+                any_blocked |= bl[k];
+            }
+            double pf[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) pf[k] = 0.0;
+            if (__any_sync(0xffffffffu, any_blocked)) {
+#pragma unroll
+                for (int kk = 0; kk < K; ++kk) {
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const double v = shfl(prev[kk], base + fj[k]);
+                        pf[k] = (K == 1 || fk[k] == kk) ? v : pf[k];
                     }
                 }
             }
@@ -673,7 +720,6 @@ exact_kernel(const LaunchArgs a) {
                     blk_sim += bl[k] ? 1 : 0;
                     if (p >= L) { fin[k] = start + rt + 1; racing[k] = false; }
                 }
-                pv[k] = racing[k] ? pos[k] : NEG_INF;
             }
             if (seg_running && !diverged) {
                 rt += 1;

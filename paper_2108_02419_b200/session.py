@@ -20,6 +20,7 @@ jittered wake schedule of session.py:104-121, and one batched prediction launch 
 
 from __future__ import annotations
 
+import ctypes
 import os
 import random
 import sys
@@ -29,7 +30,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .agents import dry_run_seeds, dry_run_seeds_many, rb_bettor_predict, rb_weighted, rp_bettor_predict
+from .agents import (_IDX_OFF, _inplace_ok, dry_run_seeds, dry_run_seeds_many, rb_bettor_predict, rb_weighted,
+                     rp_bettor_predict)
 from .race import RaceState
 from .seeding import derive_seed, spawn_rng
 from .sim import run_race, simulate_batch_begin
@@ -287,6 +289,28 @@ def c4_session_config(race, *, n_agents: int = 100, d: int = 1000, master_seed: 
                                     opening_period=opening_period)
 
 
+_MT_BYTES = 4 + 624 * 4  # RandomObject: int index, then uint32_t state[624] (agents.py layout)
+
+
+def stream_fingerprint(rng):
+    """The exact position of a bettor's MT19937 stream: the 2,500 bytes of index + state inside a
+    CPython random.Random (layout verified once by agents._inplace_ok), else its getstate()."""
+    if type(rng) is random.Random and _inplace_ok():
+        return ctypes.string_at(id(rng) + _IDX_OFF, _MT_BYTES)
+    return rng.getstate()
+
+
+def clone_stream(rng, into: random.Random | None = None) -> random.Random:
+    """A random.Random at the same stream position as ``rng`` (``into``, reused, or a new one): a
+    memmove of the MT19937 fields when the layout is verified, else setstate(getstate())."""
+    v = into if into is not None else random.Random(0)
+    if type(rng) is random.Random and type(v) is random.Random and _inplace_ok():
+        ctypes.memmove(id(v) + _IDX_OFF, id(rng) + _IDX_OFF, _MT_BYTES)
+    else:
+        v.setstate(rng.getstate())
+    return v
+
+
 @dataclass
 class SessionStats:
     launches: int = 0          # batched prediction launches
@@ -330,10 +354,12 @@ def make_gpu_session(config, *, mode: str = "mt", predictor=None):
             self.stats = SessionStats()
             self._plans: dict[int, deque] = {}
             self._batched: dict[int, object] = {}
+            self._virt: dict[int, random.Random] = {}  # per bettor: the planning clone of its stream
             for i, a in enumerate(self.agents):
                 if type(a) in (RPBettor, RBBettor) and type(a.rng) is random.Random:
                     self._batched[i] = a
                     self._plans[i] = deque()
+                    self._virt[i] = random.Random(0)
                     a.predict = self._hook(i, a)  # instance attribute: shadows the class method
 
         def _hook(self, i, agent):
@@ -344,7 +370,7 @@ def make_gpu_session(config, *, mode: str = "mt", predictor=None):
                 q = self._plans[i]
                 if q:
                     expect, probs = q.popleft()
-                    if agent.rng.getstate() == expect:
+                    if stream_fingerprint(agent.rng) == expect:
                         dry_run_seeds(agent.rng, d, want=False)
                         return probs
                     q.clear()  # the stream moved off the plan: later planned wakes are void too
@@ -377,15 +403,11 @@ def make_gpu_session(config, *, mode: str = "mt", predictor=None):
             positions, finish_ticks, history = self._race_view()
             state = RaceState(self.state.tick, list(positions), [h[-1] if h else 0.0 for h in history],
                               list(finish_ticks))
-            virt = {}
-            for i in count:
-                v = random.Random()
-                v.setstate(self._batched[i].rng.getstate())
-                virt[i] = v
             t0 = time.perf_counter()
+            virt = {i: clone_stream(self._batched[i].rng, self._virt[i]) for i in count}
             for r in range(max(count.values())):
                 members = [i for i in count if count[i] > r]
-                expects = [virt[i].getstate() for i in members]
+                expects = [stream_fingerprint(virt[i]) for i in members]
                 reqs = [DryRunRequest(virt[i], self._batched[i].params.d) for i in members]
                 before = (getattr(self.predictor, "launches", 0), getattr(self.predictor, "sims", 0))
                 probs = self.predictor.predict_many(state, reqs)
