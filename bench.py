@@ -508,9 +508,11 @@ def sweep_configs(args, torch, sim):
                 "races_per_s_end_to_end": st.sims / st.seconds, "seconds": st.seconds,
                 "predict_seconds": st.predict_seconds, "exchange_loop_seconds": st.seconds - st.predict_seconds,
                 "sims": st.sims, "predictions": st.predictions, "launches": st.launches, "rounds": st.rounds,
+                "look_ahead_hits": st.ahead_hits, "look_ahead_misses": st.ahead_misses,
                 "fallbacks": st.fallbacks, "events": len(res.events), "race_ticks": res.trajectory.n_ticks
                 if hasattr(res.trajectory, "n_ticks") else None,
-                "note": "reference exchange loop (racemarket.session) with batched GPU predictions"
+                "note": "reference exchange loop (racemarket.session) with batched GPU predictions, the next "
+                        "call's first round launched during this call's exchange"
                         + ("; event log equals the reference's" if mode == "mt" else "")}
     except ImportError as e:
         out["C4_session"] = {"unavailable": f"racemarket not importable ({e})"}

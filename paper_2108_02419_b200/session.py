@@ -313,24 +313,29 @@ def clone_stream(rng, into: random.Random | None = None) -> random.Random:
 
 @dataclass
 class SessionStats:
-    launches: int = 0          # batched prediction launches
+    launches: int = 0          # batched prediction launches (look-ahead launches included)
     sims: int = 0              # dry runs simulated
     predictions: int = 0       # RP/RB predictions served from a batch
     fallbacks: int = 0         # predictions computed on their own (stream not where planned)
     rounds: int = 0            # wake rounds
-    predict_seconds: float = 0.0  # host wall time inside the batched predictions (seeds + GPU + tally)
+    ahead_hits: int = 0        # rounds served by the launch made during the previous call's exchange
+    ahead_misses: int = 0      # look-ahead launches discarded (their inputs did not come true)
+    predict_seconds: float = 0.0  # host wall time inside the prediction planning (seeds + waits + tally)
     seconds: float = 0.0          # wall time of the whole session run
 
 
-def make_gpu_session(config, *, mode: str = "mt", predictor=None):
+def make_gpu_session(config, *, mode: str = "mt", predictor=None, look_ahead: bool = True):
     """A ``racemarket.session._Session`` whose RP/RB bettors' predictions come from batched launches.
 
     ``predictor.predict_many(state, requests)`` serves a round (default: ``DryRunDispatcher(race,
     mode)``).  Everything else -- wake schedule, observations, ``decide``, the exchange, matching,
     close, settlement, the event log -- is the reference's own code (session.py:124-340).
+    ``look_ahead`` (predictors with ``prepare``/``launch``/``finish``): the next call's first round
+    is launched before this call's exchange runs, so the GPU works while the host matches orders.
     """
     rm = import_racemarket()
     from racemarket.agents import RBBettor, RPBettor
+    from racemarket.race import advance_race
 
     class GpuSession(rm.session._Session):
         """session.py:_Session with ``_process_wakes`` (session.py:258-267) prefetching predictions.
@@ -345,6 +350,14 @@ def make_gpu_session(config, *, mode: str = "mt", predictor=None):
         where the plan drew the seeds, and advances it by d ``getrandbits(64)`` as ``rp_predict``
         does (agents.py:164).  A stream found anywhere else is predicted on its own (GPU, same
         mode), so the result never depends on the plan being right.
+
+        Look-ahead (§8f-1): the live race never depends on the market (session.py:282 advances it
+        with ``rng_race`` alone) and a bettor's stream after its decision depends only on its
+        prediction, so once a call's rounds are planned, the next call's first round is fully
+        determined: its race state (one ``advance_race`` of a clone of the state and of
+        ``rng_race``), its due wakes (the schedule) and every member's stream position.  It is
+        launched right away and runs on the GPU while the reference processes this call's wakes; the
+        next call uses it only if its until, members, race state and stream positions all match.
         """
 
         def __init__(self, cfg):
@@ -354,13 +367,19 @@ def make_gpu_session(config, *, mode: str = "mt", predictor=None):
             self.stats = SessionStats()
             self._plans: dict[int, deque] = {}
             self._batched: dict[int, object] = {}
-            self._virt: dict[int, random.Random] = {}  # per bettor: the planning clone of its stream
+            self._virt: dict[int, random.Random] = {}   # per bettor: the planning clone of its stream
+            self._avirt: dict[int, random.Random] = {}  # per bettor: the look-ahead clone
             for i, a in enumerate(self.agents):
                 if type(a) in (RPBettor, RBBettor) and type(a.rng) is random.Random:
                     self._batched[i] = a
                     self._plans[i] = deque()
                     self._virt[i] = random.Random(0)
+                    self._avirt[i] = random.Random(0)
                     a.predict = self._hook(i, a)  # instance attribute: shadows the class method
+            self._look_ahead = look_ahead and all(hasattr(self.predictor, f) for f in ("prepare", "launch", "finish"))
+            self._ahead = None
+            self._race_clone = random.Random(0)
+            self._close_rank = cfg.race.betting_close.close_rank(self.n)
 
         def _hook(self, i, agent):
             rb = isinstance(agent, RBBettor)
@@ -381,38 +400,69 @@ def make_gpu_session(config, *, mode: str = "mt", predictor=None):
 
             return predict
 
-        def _process_wakes(self, until: float) -> None:
-            nw = list(self.next_wake)
+        def _due(self, until: float, nw: list) -> list:
+            """session.py:259-264 on the wake times ``nw`` (advanced in place)."""
             due = []
-            for i, agent in enumerate(self.agents):  # session.py:259-264, on a copy
+            for i, agent in enumerate(self.agents):
                 period = agent.params.reevaluate_every
                 while nw[i] <= until:
                     due.append((nw[i], i))
                     nw[i] += period
             due.sort()
-            self._prefetch(due)
-            super()._process_wakes(until)
+            return due
 
-        def _prefetch(self, due) -> None:
-            count: dict[int, int] = {}
-            for _, i in due:
-                if i in self._batched:
-                    count[i] = count.get(i, 0) + 1
-            if not count:
-                return
+        def _process_wakes(self, until: float) -> None:
+            nw = list(self.next_wake)
+            due = self._due(until, nw)
             positions, finish_ticks, history = self._race_view()
             state = RaceState(self.state.tick, list(positions), [h[-1] if h else 0.0 for h in history],
                               list(finish_ticks))
             t0 = time.perf_counter()
+            count = self._prefetch(due, state, until)
+            if self._look_ahead:
+                self._launch_ahead(nw, count)
+            self.stats.predict_seconds += time.perf_counter() - t0
+            super()._process_wakes(until)
+
+        def _members(self, due, r: int, count: dict) -> list:
+            seen: dict[int, int] = {}
+            out = []
+            for _, i in due:
+                if i in self._batched:
+                    k = seen.get(i, 0)
+                    seen[i] = k + 1
+                    if k == r:
+                        out.append(i)
+            return out
+
+        def _prefetch(self, due, state, until) -> dict:
+            count: dict[int, int] = {}
+            for _, i in due:
+                if i in self._batched:
+                    count[i] = count.get(i, 0) + 1
+            ahead, self._ahead = self._ahead, None
+            if not count:
+                if ahead is not None:
+                    self._drop(ahead)
+                return count
             virt = {i: clone_stream(self._batched[i].rng, self._virt[i]) for i in count}
             for r in range(max(count.values())):
                 members = [i for i in count if count[i] > r]
                 expects = [stream_fingerprint(virt[i]) for i in members]
-                reqs = [DryRunRequest(virt[i], self._batched[i].params.d) for i in members]
-                before = (getattr(self.predictor, "launches", 0), getattr(self.predictor, "sims", 0))
-                probs = self.predictor.predict_many(state, reqs)
-                self.stats.launches += getattr(self.predictor, "launches", 0) - before[0]
-                self.stats.sims += getattr(self.predictor, "sims", 0) - before[1]
+                probs = None
+                if r == 0 and ahead is not None:
+                    if (ahead["until"] == until and ahead["members"] == members and ahead["state"] == _sig(state)
+                            and ahead["expects"] == expects):
+                        probs = self.predictor.finish(ahead["pending"], ahead["prep"])
+                        for i in members:
+                            clone_stream(self._avirt[i], virt[i])  # advanced past its d seeds by prepare
+                        self.stats.ahead_hits += 1
+                    else:
+                        self._drop(ahead)
+                    ahead = None
+                if probs is None:
+                    reqs = [DryRunRequest(virt[i], self._batched[i].params.d) for i in members]
+                    probs = self.predictor.predict_many(state, reqs)
                 self.stats.rounds += 1
                 for i, e, p in zip(members, expects, probs):
                     a = self._batched[i]
@@ -421,23 +471,75 @@ def make_gpu_session(config, *, mode: str = "mt", predictor=None):
                     self._plans[i].append((e, out))
                     decide_draws(virt[i], out, a.params.max_stake if rb else None)
                 self.stats.predictions += len(members)
-            self.stats.predict_seconds += time.perf_counter() - t0
+            if ahead is not None:
+                self._drop(ahead)
+            self._sync_counts()
+            return count
+
+        def _launch_ahead(self, nw: list, count: dict) -> None:
+            """Launch the next call's first round now (see the class docstring)."""
+            if self.state.all_finished() or self.state.tick >= self.race_cfg.tick_limit:
+                return
+            st = self.state.clone()
+            rng = clone_stream(self.rng_race, self._race_clone)
+            racing_before = [t is None for t in st.finish_ticks]
+            advance_race(st, self.race_cfg, rng)
+            if st.finished_count() >= self._close_rank:
+                return  # betting closes on that tick: no wakes (session.py:294-311)
+            until = self.config.opening_period + st.tick * self.race_cfg.dt
+            due = self._due(until, list(nw))
+            members = self._members(due, 0, count)
+            if not members:
+                return
+            hist = self.histories
+            prev = [st.prev_steps[c] if racing_before[c] else (hist[c][-1] if hist[c] else 0.0) for c in range(self.n)]
+            state = RaceState(st.tick, list(st.positions), prev, list(st.finish_ticks))
+            # member streams now: the planned clone for bettors of this call, the real stream otherwise
+            src = {i: (self._virt[i] if i in count else self._batched[i].rng) for i in members}
+            expects = [stream_fingerprint(src[i]) for i in members]
+            la = [clone_stream(src[i], self._avirt[i]) for i in members]
+            prep = self.predictor.prepare([DryRunRequest(v, self._batched[i].params.d) for v, i in zip(la, members)])
+            pending = self.predictor.launch(state, prep)
+            self._ahead = {"until": until, "members": members, "state": _sig(state), "expects": expects,
+                           "prep": prep, "pending": pending}
+
+        def _drop(self, ahead) -> None:
+            self.stats.ahead_misses += 1
+            self.predictor.finish(ahead["pending"], ahead["prep"])  # wait, release its launch context
+
+        def _sync_counts(self) -> None:
+            self.stats.launches = getattr(self.predictor, "launches", 0)
+            self.stats.sims = getattr(self.predictor, "sims", 0)
+
+        def run(self):
+            try:
+                return super().run()
+            finally:
+                if self._ahead is not None:
+                    self._drop(self._ahead)
+                    self._ahead = None
+                self._sync_counts()
 
     return GpuSession(config)
 
 
-def run_session(config, *, mode: str = "mt", predictor=None):
+def _sig(state) -> tuple:
+    """Exact identity of a RaceState as a bettor reconstructs it."""
+    return (state.tick, tuple(state.positions), tuple(state.prev_steps), tuple(state.finish_ticks))
+
+
+def run_session(config, *, mode: str = "mt", predictor=None, look_ahead: bool = True):
     """``racemarket.session.run_session`` (session.py:345-347) with batched GPU predictions.
 
     mode="mt": every prediction, and so the whole event log, settlement and balances, equals the
     reference's; "native64"/"native": Philox dry runs (statistically equal predictions).  Returns
     the reference's ``SessionResult``."""
-    return run_session_with_stats(config, mode=mode, predictor=predictor)[0]
+    return run_session_with_stats(config, mode=mode, predictor=predictor, look_ahead=look_ahead)[0]
 
 
-def run_session_with_stats(config, *, mode: str = "mt", predictor=None):
+def run_session_with_stats(config, *, mode: str = "mt", predictor=None, look_ahead: bool = True):
     """``run_session`` plus the dispatch counters (``SessionStats``) and the wall time of ``run``."""
-    s = make_gpu_session(config, mode=mode, predictor=predictor)
+    s = make_gpu_session(config, mode=mode, predictor=predictor, look_ahead=look_ahead)
     t0 = time.perf_counter()
     res = s.run()
     s.stats.seconds = time.perf_counter() - t0

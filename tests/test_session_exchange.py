@@ -79,12 +79,16 @@ class OraclePredictor:
         self.launches = 0
         self.sims = 0
 
-    def predict_many(self, state, requests):
+    def prepare(self, requests):
+        ds = [r.d for r in requests]
+        return {"ds": ds, "seeds": [r.rng.getrandbits(64) for r, d in zip(requests, ds) for _ in range(d)]}
+
+    def launch(self, state, prep):
+        """Runs the batch at once; the 'pending' handle is the result (the GPU's is asynchronous)."""
         import oracle
 
         n = len(self.race.competitors)
-        ds = [r.d for r in requests]
-        seeds = [r.rng.getrandbits(64) for r, d in zip(requests, ds) for _ in range(d)]
+        ds, seeds = prep["ds"], prep["seeds"]
         total = len(seeds)
         if total == 0:
             return [tuple(1 / (d + n) for _ in range(n)) for d in ds]
@@ -99,6 +103,13 @@ class OraclePredictor:
             at += d
             res.append(tuple((int(x) + 1) / (d + n) for x in wins))
         return res
+
+    def finish(self, pending, prep):
+        return pending
+
+    def predict_many(self, state, requests):
+        prep = self.prepare(requests)
+        return self.finish(self.launch(state, prep), prep)
 
 
 def record_predictions(sess):
@@ -118,9 +129,9 @@ def record_predictions(sess):
     return log
 
 
-def run_and_compare(g, predictor=None, mode="mt"):
+def run_and_compare(g, predictor=None, mode="mt", look_ahead=True):
     cfg = session_config(g)
-    sess = S.make_gpu_session(cfg, mode=mode, predictor=predictor)
+    sess = S.make_gpu_session(cfg, mode=mode, predictor=predictor, look_ahead=look_ahead)
     log = record_predictions(sess)
     res = sess.run()
     assert sess.stats.fallbacks == 0, "every prediction should come from its planned round"
@@ -137,12 +148,20 @@ def run_and_compare(g, predictor=None, mode="mt"):
     return sess
 
 
+@pytest.mark.parametrize("look_ahead", [False, True])
 @pytest.mark.parametrize("case", [0, 1])
-def test_session_rounds_on_oracle_equal_reference_event_log(case):
+def test_session_rounds_on_oracle_equal_reference_event_log(case, look_ahead):
     g = golden()[case]
-    sess = run_and_compare(g, predictor=OraclePredictor(session_config(g).race))
-    # one launch per wake round, far fewer than the reference's one rp_predict per wake
-    assert sess.stats.launches <= sess.stats.rounds < sess.stats.predictions
+    sess = run_and_compare(g, predictor=OraclePredictor(session_config(g).race), look_ahead=look_ahead)
+    st = sess.stats
+    # one launch per wake round (plus discarded look-aheads), far fewer than one rp_predict per wake
+    assert st.launches - st.ahead_misses <= st.rounds < st.predictions
+    if look_ahead:
+        # the first round of every call after the opening one was launched during the previous
+        # call's exchange (later rounds of a call depend on its earlier decisions), none wasted
+        assert st.ahead_hits > 0 and st.ahead_misses == 0
+    else:
+        assert st.ahead_hits == st.ahead_misses == 0
 
 
 def test_decide_draws_match_reference_decide():
@@ -176,7 +195,7 @@ def test_gpu_session_mt_equals_reference_event_log(case):
     loop unchanged -- the event log, predictions, winner and balances equal the reference's."""
     g = golden()[case]
     sess = run_and_compare(g, mode="mt")
-    assert sess.stats.launches <= sess.stats.rounds
+    assert sess.stats.launches - sess.stats.ahead_misses <= sess.stats.rounds and sess.stats.ahead_hits > 0
 
 
 @pytest.mark.gpu
