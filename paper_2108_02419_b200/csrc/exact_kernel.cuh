@@ -541,8 +541,10 @@ exact_kernel(const LaunchArgs a) {
         }
         if (!__any_sync(0xffffffffu, running)) break;
 
-        // ---------------- 4 synchronous ticks -------------------------------------------------------
+        // ---------------- kTicksPerBlock synchronous ticks ---------------------------------------
         __syncwarp();  // key rows: the previous block's reads precede this block's writes
+        // the per-tick limit test runs only in blocks where some segment can reach the limit
+        const bool near_limit = __any_sync(0xffffffffu, running && rt > a.limit - kTicksPerBlock);
         for (int tj = 0; tj < kTicksPerBlock; ++tj) {
             bool any_racing = false;
 #pragma unroll
@@ -552,7 +554,7 @@ exact_kernel(const LaunchArgs a) {
             if (rmask == 0u) break;  // every segment finished inside this block
 
             // tick-limit check before the advance (race.py:381-386, 402-404)
-            if (seg_running && rt >= a.limit) {
+            if (near_limit && seg_running && rt >= a.limit) {
                 diverged = true;
 #pragma unroll
                 for (int k = 0; k < K; ++k) racing[k] = false;

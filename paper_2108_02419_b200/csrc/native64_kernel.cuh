@@ -67,9 +67,10 @@ struct CBool {
 #ifndef BBE_N64_MINBLOCKS_KN
 #define BBE_N64_MINBLOCKS_KN 4
 #endif
-// Tick pairs per iteration of the draw-staging loop: 2 (two Philox chains per slot in flight) for
-// K <= 2, except the wide-row scan layouts, where the registers cost more than the ILP gains (A/B round 2, ms per
-// launch, 1 -> 2: C3/C5 field 58.04 -> 54.91, C2 0.685 -> 0.667, derby20 33.36 -> 34.44).
+// Tick pairs per iteration of the draw-staging loop: 2 (two Philox chains per slot in flight) for the
+// scan-free K <= 2 layouts and the narrow K = 1 scan layouts; 1 elsewhere, where the registers cost
+// more than the ILP gains (A/B round 2, ms per launch, 1 -> 2: C3/C5 field 58.04 -> 54.91, C1 1.564 ->
+// 1.484, C2 0.682 -> 0.665; derby20 (K = 2 with a scan) 33.22 -> 34.33).
 #ifndef BBE_N64_DRAW_UNROLL
 #define BBE_N64_DRAW_UNROLL 0  // 0 = the rule above; else forced (A/B builds)
 #endif
@@ -326,7 +327,7 @@ native64_kernel(const LaunchArgs a) {
         // ---- the block's draws: NT per slot, into this lane's shared-memory column ----
         {
             const uint64_t gs = (uint64_t)(a.sim_offset + s);
-            constexpr int DU = BBE_N64_DRAW_UNROLL ? BBE_N64_DRAW_UNROLL : ((K <= 2 && (!SCAN || CH <= 3)) ? 2 : 1);
+            constexpr int DU = BBE_N64_DRAW_UNROLL ? BBE_N64_DRAW_UNROLL : (((!SCAN && K <= 2) || (K == 1 && CH <= 3)) ? 2 : 1);
 #pragma unroll DU
             for (int h = 0; h < NT / 2; ++h) {
 #pragma unroll
