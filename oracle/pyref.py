@@ -1,9 +1,11 @@
 """Pure-Python restatement of the reference hot path -- TEST INFRASTRUCTURE / CPU BASELINE ONLY.
 
-Same language and same RNG (CPython ``random.Random``, MT19937) as the reference, so it runs at the
-reference's speed and produces the reference's exact outputs; ``bench.py --impl reference`` times it
-on the GPU box's host cores, where ``/root/reference`` does not exist.  Pinned against the reference
-by tests/test_oracle_golden.py.
+Same language and same RNG (CPython ``random.Random``, MT19937) as the reference, so it produces
+the reference's exact outputs; it runs about 1.35x faster than ``racemarket`` itself (measured on C2:
+692 vs 512 races/s on one core -- it hoists the per-step constants the reference recomputes).
+``bench.py`` times the reference itself (``racemarket`` from ``baseline/_ref``) and falls back to
+this restatement, labelled kind "port", only where that install is missing.  Pinned against the
+reference by tests/test_oracle_golden.py.
 
 Follows /root/reference/pkg/src/racemarket/:
   race.py:192-199 preference_factor, :93-96 responsiveness, :233-241 initial_state,
