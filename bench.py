@@ -645,6 +645,11 @@ def main(argv=None):
     if args.impl == "reference":
         return run_reference(args)
     if args.gpus > 1 and "RANK" not in os.environ:
+        import torch
+
+        if args.gpus > torch.cuda.device_count():
+            print(f"--gpus {args.gpus}: only {torch.cuda.device_count()} GPU(s) visible", file=sys.stderr)
+            return 2
         return subprocess.call(spawn_command(args.gpus, argv, free_port()))
     return run_ours(args)
 

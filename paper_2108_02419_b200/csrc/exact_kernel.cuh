@@ -543,8 +543,6 @@ exact_kernel(const LaunchArgs a) {
 
         // ---------------- kTicksPerBlock synchronous ticks ---------------------------------------
         __syncwarp();  // key rows: the previous block's reads precede this block's writes
-        // the per-tick limit test runs only in blocks where some segment can reach the limit
-        const bool near_limit = __any_sync(0xffffffffu, running && rt > a.limit - kTicksPerBlock);
         for (int tj = 0; tj < kTicksPerBlock; ++tj) {
             bool any_racing = false;
 #pragma unroll
@@ -554,7 +552,7 @@ exact_kernel(const LaunchArgs a) {
             if (rmask == 0u) break;  // every segment finished inside this block
 
             // tick-limit check before the advance (race.py:381-386, 402-404)
-            if (near_limit && seg_running && rt >= a.limit) {
+            if (seg_running && rt >= a.limit) {
                 diverged = true;
 #pragma unroll
                 for (int k = 0; k < K; ++k) racing[k] = false;
