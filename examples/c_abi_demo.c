@@ -57,9 +57,9 @@ int main(void) {
     uint64_t* seeds = (uint64_t*)malloc(sizeof(uint64_t) * d);
     if (!seeds) return 1;
     bbe_derive_seeds(11, 0, d, seeds);
-    const int modes[2] = {BBE_MODE_NATIVE, BBE_MODE_MT};
-    const char* names[2] = {"native", "mt"};
-    for (int m = 0; m < 2; ++m) {
+    const int modes[4] = {BBE_MODE_NATIVE, BBE_MODE_NATIVE64, BBE_MODE_MT, BBE_MODE_NATIVE64};
+    const char* names[4] = {"native", "native64", "mt", "multi64"};
+    for (int m = 0; m < 4; ++m) {
         bbe_request rq;
         memset(&rq, 0, sizeof rq);
         rq.n_sims = d;
@@ -70,7 +70,10 @@ int main(void) {
         bbe_result out;
         memset(&out, 0, sizeof out);
         out.wins = wins;
-        const int rc = bbe_simulate(&race, comps, &st, &rq, &out);
+        /* multi64: the same NATIVE64 request over every visible GPU (one part per device; the
+         * device tallies are combined by one NCCL all-reduce when there is more than one) */
+        const int rc = m == 3 ? bbe_simulate_multi(0, &race, comps, &st, &rq, &out)
+                              : bbe_simulate(&race, comps, &st, &rq, &out);
         if (rc != BBE_OK) {
             fprintf(stderr, "bbe_simulate(%s) failed (%d): %s\n", names[m], rc, bbe_last_error());
             return 2;

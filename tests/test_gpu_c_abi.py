@@ -24,7 +24,7 @@ def test_c_program_drives_the_library(tmp_path):
                     f"-Wl,-rpath,{lib_dir}", "-o", exe], check=True)
     out = subprocess.run([exe], check=True, capture_output=True, text=True).stdout.splitlines()
     rows = {line.split()[0]: [float(x) for x in line.split("probs")[1].split()] for line in out}
-    assert set(rows) == {"native", "mt", "rp_mt"}
+    assert set(rows) == {"native", "native64", "mt", "multi64", "rp_mt"}
     n, d = 10, 20000
     comps = tuple(Competitor(f"c{c}", UniformSteps(10.0 + c % 3, 20.0 + c % 4), theta=8.0 if c % 2 else 0.0)
                   for c in range(n))
@@ -33,6 +33,11 @@ def test_c_program_drives_the_library(tmp_path):
     ref = oracle.batch(cfg, d, state=st, master=11, threads=8)
     assert rows["mt"] == [(int(w) + 1) / (d + n) for w in ref["wins"]]
     assert abs(sum(rows["native"]) - 1.0) < 1e-9
+    # NATIVE64 (seed 7): the oracle's restatement of the same Philox stream, and bbe_simulate_multi
+    # gives the single-call tallies
+    ref64 = oracle.batch_px(cfg, d, 7, state=st, threads=8)
+    assert rows["native64"] == [(int(w) + 1) / (d + n) for w in ref64["wins"]]
+    assert rows["multi64"] == rows["native64"]
     # bbe_rp_predict with random.Random(5) as the bettor: the reference's rp_predict over its seeds
     import random
 
