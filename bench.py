@@ -469,6 +469,17 @@ def sweep_configs(args, torch, sim):
                          "ct_per_s": ct / (ms / 1e3), "ops_per_ct": ops,
                          "issue_roofline_frac": ct * ops / (ms / 1e3) / (peak * 1e9)}
         out[name] = row
+    # the C5 field in MT mode: run_batch's own seeds derive_seed(M, "run", i) derived on the device, so
+    # the tallies are the reference's run_batch(BatchConfig(race, R, M)) tallies bit for bit
+    c5f = uniform_field(20)
+    for r in range(2):
+        t0 = time.perf_counter()
+        res = sim.simulate_batch(None, c5f, 1_000_000, mode="mt", seed_master=MASTER + r)
+        wall = time.perf_counter() - t0
+    out["C5_field_mt_run_batch_seeds_1e6"] = {
+        "dtype": "f64", "device_ms": res.kernel_ms, "races_per_s_device": 1e6 / (res.kernel_ms / 1e3),
+        "e2e_ms": wall * 1e3, "races_per_s_e2e": 1e6 / wall, "ct_per_s": res.competitor_steps / (res.kernel_ms / 1e3),
+        "note": "simulate_batch(None, race, 1e6, mode='mt', seed_master=M): bit-identical to the reference's run_batch"}
     ms, ct, blk = device_launch_ms(torch, sim, None, uniform_field(20), args.c5_sims, "native", reps=1)
     out["C5_fp32_state_1e9"] = {"dtype": "f32", "ms": ms, "races_per_s": args.c5_sims / (ms / 1e3), "ct_per_s": ct / (ms / 1e3),
                                 "issue_roofline_frac": ct * ops_per_ct(20, 1.0, scan=False, native64=False) / (ms / 1e3) / (peak * 1e9)}
@@ -499,7 +510,7 @@ def sweep_configs(args, torch, sim):
     try:
         from paper_2108_02419_b200.session import c4_session_config, run_session_with_stats
 
-        for mode, d in (("mt", 1000), ("native64", 1000), ("native64", 10_000), ("native64", 100_000)):
+        for mode, d in (("mt", 1000), ("mt", 10_000), ("native64", 1000), ("native64", 10_000), ("native64", 100_000)):
             if d > args.c4_max_d:
                 continue
             cfg = c4_session_config(derby10, n_agents=100, d=d)
