@@ -61,6 +61,9 @@ struct CBool {
     static constexpr bool value = B;
 };
 
+#ifndef BBE_N64_TICK_ROLL
+#define BBE_N64_TICK_ROLL 1
+#endif
 #ifndef BBE_N64_MINBLOCKS_K1
 #define BBE_N64_MINBLOCKS_K1 5
 #endif
@@ -522,10 +525,19 @@ native64_kernel(const LaunchArgs a) {
 
         // the block's NT ticks, in pairs (the key rows alternate by tick parity), under the host flags
         auto run_block = [&](auto resp_var, auto guard) {
+            if constexpr (SCAN && K >= 2 && BBE_N64_TICK_ROLL) {
+                // one tick body (the row parity a runtime value): the multi-slot scan layouts' tick is
+                // large, and two unrolled copies overflow the instruction cache (derby20, K = 2: 27 %
+                // no_instructions stalls; 33.4 -> 29.3 ms).  K = 1 keeps both: rolled it is 1.5-2 %
+                // slower (C2, derby12/16/24/32).
 #pragma unroll 1
-            for (int tp = 0; tp < NT; tp += 2) {
-                tick(tp, 0, resp_var, guard);
-                tick(tp + 1, 1, resp_var, guard);
+                for (int t = 0; t < NT; ++t) tick(t, t & 1, resp_var, guard);
+            } else {
+#pragma unroll 1
+                for (int tp = 0; tp < NT; tp += 2) {
+                    tick(tp, 0, resp_var, guard);
+                    tick(tp + 1, 1, resp_var, guard);
+                }
             }
         };
         if (SCAN) __syncwarp();  // key rows: the previous block's reads precede this block's writes

@@ -27,6 +27,8 @@ def field(name):
         return state_from_dict(g["state"]), derby10
     if name == "derby20":
         return None, resize_race(resize_race(derby10, 5), 20)
+    if name.startswith("derby"):  # derbyN: derby.json resized to N, from the start line
+        return None, resize_race(resize_race(derby10, 5), int(name[5:]))
     n = {"c1": 5, "c3": 20, "c5": 20}[name]
     return None, RaceConfig(2000.0, tuple(Competitor(f"c{i + 1}", UniformSteps(10.0, 20.0)) for i in range(n)))
 
