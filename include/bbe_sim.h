@@ -10,8 +10,9 @@
  *                         agents.py:153-166 rp_predict(state, config, d, rng)      (wins -> (w+1)/(d+n))
  *                         batch.py:110-124 run_batch(BatchConfig)                  (per-sim outputs)
  *                         batch.py:149-170 estimate_pmf / pmf_from_results         (perms tally, n <= 6)
- *   bbe_simulate_multi    the same over several GPUs (one host thread per device, host-merged
- *                         tallies): run_batch(BatchConfig(workers=N)), batch.py:120-124.
+ *   bbe_simulate_multi    the same over several GPUs (one host thread per device; tally-only requests
+ *                         combined by one grouped NCCL all-reduce, per-sim outputs host-merged):
+ *                         run_batch(BatchConfig(workers=N)), batch.py:120-124.
  *   bbe_simulate_async    the same, device-resident: tallies accumulate into a device buffer on a
  *                         caller stream (used by the multi-GPU path before one NCCL all-reduce).
  *   bbe_rp_predict        agents.py:153-166 rp_predict(state, config, d, rng) in one call: the d

@@ -424,7 +424,8 @@ def make_gpu_session(config, *, mode: str = "mt", predictor=None, look_ahead: bo
             self.stats.predict_seconds += time.perf_counter() - t0
             super()._process_wakes(until)
 
-        def _members(self, due, r: int, count: dict) -> list:
+        def _members(self, due, r: int) -> list:
+            """The batched bettors of round r of a due list (their r-th wake), in due order."""
             seen: dict[int, int] = {}
             out = []
             for _, i in due:
@@ -488,7 +489,7 @@ def make_gpu_session(config, *, mode: str = "mt", predictor=None, look_ahead: bo
                 return  # betting closes on that tick: no wakes (session.py:294-311)
             until = self.config.opening_period + st.tick * self.race_cfg.dt
             due = self._due(until, list(nw))
-            members = self._members(due, 0, count)
+            members = self._members(due, 0)
             if not members:
                 return
             hist = self.histories
