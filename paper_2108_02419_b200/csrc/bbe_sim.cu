@@ -545,7 +545,7 @@ int pick_ticks64(bool scan, double T) {
         const char* e = std::getenv("BBE_TICKS64");
         return e ? std::atoi(e) : 0;
     }();
-    if (scan) return 8;
+    if (scan) return BBE_N64_SCAN_NT;
     if (env == 8 || env == 16) return env;
     return T >= 43.0 ? 16 : 8;
 }

@@ -14,6 +14,10 @@ constexpr int kWarpsPerBlock = kBlockThreads / kWarp;
 #ifndef BBE_EXACT_TICKS
 #define BBE_EXACT_TICKS 8  // C2 MT: 4 -> 2.54 ms, 8 -> 2.43, 16 -> 2.42 (bit-identical; 8 idles less on short races)
 #endif
+#ifndef BBE_N64_SCAN_NT
+#define BBE_N64_SCAN_NT 16  // NATIVE64 layouts with a front-runner scan: ticks per block (A/B, ms:
+                            // 8 -> 16: C2 0.667 -> 0.653, derby20 29.25 -> 28.12, derby12 17.85 -> 15.25)
+#endif
 constexpr int kTicksPerBlock = BBE_EXACT_TICKS;  // exact kernels: ticks between finalize/refill boundaries
 
 // Parameter block fields (SoA, stride n), host-packed in double (see bbe_sim.cu: pack_params).

@@ -23,7 +23,7 @@ KernelFn pick_native_k1_nt8(int ch, bool scan, int vec);
 KernelFn pick_native_k1_nt16(int ch, bool scan, int vec);
 KernelFn pick_native_kn_nt4(int k, int ch, bool scan);
 KernelFn pick_native_kn_nt16(int k, int ch, bool scan);
-// NATIVE64 (FP64 state): with a front-runner scan (8-tick blocks), or scan-free (NT = 8 or 16);
+// NATIVE64 (FP64 state): with a front-runner scan (BBE_N64_SCAN_NT = 16-tick blocks), or scan-free (NT = 8 or 16);
 // LN = some lognormal competitor
 KernelFn pick_native64_scan(int k, int ch, bool ln);  // bbe_sim.cu: dispatches to the four parts
 KernelFn pick_native64_scan_k1_ln0(int k, int ch);

@@ -2,7 +2,7 @@
 // selectors.  Compiled once per part so the objects build in parallel:
 //   BBE_N64_SCAN = 0: the scan-free layouts (theta = 0 everywhere): K = 1-4, 8- and 16-tick blocks,
 //                     with and without a lognormal competitor;
-//   BBE_N64_SCAN = 1: layouts with a front-runner scan, 8-tick blocks, CH = 1-8 key chunks, one part
+//   BBE_N64_SCAN = 1: layouts with a front-runner scan, BBE_N64_SCAN_NT-tick blocks, CH = 1-8 key chunks, one part
 //                     per (BBE_N64_K1: K = 1 or K = 2-4) x (BBE_N64_LN: lognormal competitor or not).
 #include "kernels.h"
 #include "native64_kernel.cuh"
@@ -27,14 +27,14 @@ constexpr bool LN = BBE_N64_LN != 0;
 template <int K>
 KernelFn n64_scan_for_ch(int ch) {
     switch (ch) {
-        case 1: return native64_kernel<K, 1, true, LN, 8>;
-        case 2: return native64_kernel<K, 2, true, LN, 8>;
-        case 3: return native64_kernel<K, 3, true, LN, 8>;
-        case 4: return native64_kernel<K, 4, true, LN, 8>;
-        case 5: return native64_kernel<K, 5, true, LN, 8>;
-        case 6: return native64_kernel<K, 6, true, LN, 8>;
-        case 7: return native64_kernel<K, 7, true, LN, 8>;
-        case 8: return native64_kernel<K, 8, true, LN, 8>;
+        case 1: return native64_kernel<K, 1, true, LN, BBE_N64_SCAN_NT>;
+        case 2: return native64_kernel<K, 2, true, LN, BBE_N64_SCAN_NT>;
+        case 3: return native64_kernel<K, 3, true, LN, BBE_N64_SCAN_NT>;
+        case 4: return native64_kernel<K, 4, true, LN, BBE_N64_SCAN_NT>;
+        case 5: return native64_kernel<K, 5, true, LN, BBE_N64_SCAN_NT>;
+        case 6: return native64_kernel<K, 6, true, LN, BBE_N64_SCAN_NT>;
+        case 7: return native64_kernel<K, 7, true, LN, BBE_N64_SCAN_NT>;
+        case 8: return native64_kernel<K, 8, true, LN, BBE_N64_SCAN_NT>;
     }
     return nullptr;
 }
