@@ -6,7 +6,30 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+// BBE_CHECKS builds (tools/ab_build.sh checks "-DBBE_CHECKS"): device-side bounds asserts on every
+// shared-memory index the kernels compute (MT stream window, key rows, staged draws, histograms) --
+// the bounds evidence on a pool where compute-sanitizer is closed.  Off in the product build.
+#ifdef BBE_CHECKS
+#include <cassert>
+#define BBE_CHECK(cond) assert(cond)
+#else
+#define BBE_CHECK(cond) ((void)0)
+#endif
+
 namespace bbe {
+
+// the block's dynamic shared memory size in bytes (%dynamic_smem_size), for BBE_CHECK
+__device__ __forceinline__ uint32_t dyn_smem_bytes() {
+    uint32_t v;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(v));
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ bool in_dyn_smem(const T* p, const void* base) {
+    const char* c = reinterpret_cast<const char*>(p);
+    const char* b = reinterpret_cast<const char*>(base);
+    return c >= b && c + sizeof(T) <= b + dyn_smem_bytes();
+}
 
 constexpr int kWarp = 32;
 constexpr int kBlockThreads = 128;

@@ -191,7 +191,10 @@ exact_kernel(const LaunchArgs a) {
     // window offset k -> raw word.  No clamp: after mt_window_fill the window holds >= fill_need words
     // and a round reads below offset fill_need + 4, so an idle lane's read lands at most 3 words past
     // the segment, inside the block's dynamic shared memory (the next segment or the position rows).
-    auto mt_word = [&](int k) -> uint32_t { return seg_mt[wp + k]; };
+    auto mt_word = [&](int k) -> uint32_t {
+        BBE_CHECK(in_dyn_smem(seg_mt + wp + k, s_dyn));
+        return seg_mt[wp + k];
+    };
     auto mt_consume = [&](int c) { wp += c; };
     // One step draw per (slot, lane) with want[k], in competitor-index order within each segment
     // (slot-major, then lane): uniform(lo, hi) = lo + (hi - lo) * random(); scale *
@@ -512,11 +515,13 @@ exact_kernel(const LaunchArgs a) {
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
                         if (!has[k]) continue;
+                        BBE_CHECK(cidx[k] < n && rank[k] >= 0 && rank[k] < n);
                         if (rank[k] == 0) atomicAdd(&s_hist[TL.wins() + cidx[k]], 1u);
                         atomicAdd(&s_hist[TL.ranks() + cidx[k] * n + rank[k]], 1u);
                         if (a.group_wins && rank[k] == 0)
                             atomicAdd(&a.group_wins[((a.group_base + s) / a.group_size) * n + cidx[k]], 1ull);
                     }
+                    BBE_CHECK(!a.perms || (lehmer >= 0 && lehmer < a.perms));
                     if (a.perms && l == 0) atomicAdd(&s_hist[TL.perms() + lehmer], 1u);
                 }
 #pragma unroll
@@ -583,6 +588,7 @@ exact_kernel(const LaunchArgs a) {
                     const double y = __dadd_rn(pos[k], C64);
                     const uint32_t key = __funnelshift_r((uint32_t)__double2loint(y), (uint32_t)__double2hiint(y), 26);
                     v[k] = key * 32u + cl;
+                    BBE_CHECK(in_dyn_smem(kw + par + k * kKRow, s_dyn) && (!lane_on || seg * WPK + l < kKRow - 1));
                     kw[par + k * kKRow] = racing[k] ? v[k] : 0u;
                 }
                 __syncwarp();
@@ -600,6 +606,7 @@ exact_kernel(const LaunchArgs a) {
                         const uint32_t nk = kk < k ? ~(v[k] | 31u) : (kk == k ? ~v[k] : 0u - (v[k] & ~31u));
                         uint32_t b0 = 0xffffffffu, b1 = 0xffffffffu;
                         const uint4* r4 = reinterpret_cast<const uint4*>(kr + par + kk * kKRow);
+                        BBE_CHECK(in_dyn_smem(r4 + CHK - 1, s_dyn));
 #pragma unroll 3
                         for (int c = 0; c < CHK; ++c) {
                             const uint4 q = r4[c];

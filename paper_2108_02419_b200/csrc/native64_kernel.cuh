@@ -297,11 +297,13 @@ native64_kernel(const LaunchArgs a) {
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
                         if (!has[k]) continue;
+                        BBE_CHECK(cidx[k] < n && rank[k] >= 0 && rank[k] < n);
                         if (rank[k] == 0) atomicAdd(&s_hist[TL.wins() + cidx[k]], 1u);
                         atomicAdd(&s_hist[TL.ranks() + cidx[k] * n + rank[k]], 1u);
                         if (a.group_wins && rank[k] == 0)
                             atomicAdd(&a.group_wins[((a.group_base + s) / a.group_size) * n + cidx[k]], 1ull);
                     }
+                    BBE_CHECK(!a.perms || (lehmer >= 0 && lehmer < a.perms));
                     if (a.perms && l == 0) atomicAdd(&s_hist[TL.perms() + lehmer], 1u);
                 }
 #pragma unroll
@@ -337,6 +339,7 @@ native64_kernel(const LaunchArgs a) {
                 for (int k = 0; k < K; ++k) {
                     double d0, d1;
                     draw_pair(k, ((uint32_t)rt >> 1) + (uint32_t)h, gs, d0, d1);
+                    BBE_CHECK(in_dyn_smem(s_draw + (k * NT + 2 * h + 1) * kWarp, s_dyn));
                     s_draw[(k * NT + 2 * h) * kWarp] = d0;
                     s_draw[(k * NT + 2 * h + 1) * kWarp] = d1;
                 }
@@ -363,6 +366,8 @@ native64_kernel(const LaunchArgs a) {
                         const double2 d = ln_pair(P, n, c, ((uint32_t)rt_item >> 1) + (uint32_t)h,
                                                   (uint64_t)(a.sim_offset + s_item), a.rk[0], a.rk[1]);
                         double* col = s_draw - lane + owner;
+                        BBE_CHECK(owner >= 0 && owner < kWarp && kk < K && h < NT / 2 &&
+                                  in_dyn_smem(col + (kk * NT + 2 * h + 1) * kWarp, s_dyn));
                         col[(kk * NT + 2 * h) * kWarp] = d.x;
                         col[(kk * NT + 2 * h + 1) * kWarp] = d.y;
                     }
@@ -389,6 +394,7 @@ native64_kernel(const LaunchArgs a) {
                     const double y = __dadd_rn(pos[k], C64);
                     const uint32_t key = __funnelshift_r((uint32_t)__double2loint(y), (uint32_t)__double2hiint(y), 26);
                     v[k] = key * 32u + cl;
+                    BBE_CHECK(in_dyn_smem(wr + par * PAR + k * SLOT, s_dyn));
                     wr[par * PAR + k * SLOT] = racing[k] ? v[k] : 0u;
                 }
                 __syncwarp();

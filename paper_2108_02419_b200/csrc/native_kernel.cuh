@@ -267,6 +267,7 @@ native_kernel(const LaunchArgs a) {
                         if (a.group_wins && rank[k] == 0)
                             atomicAdd(&a.group_wins[((a.group_base + s) / a.group_size) * n + cidx[k]], 1ull);
                     }
+                    BBE_CHECK(!a.perms || (lehmer >= 0 && lehmer < a.perms));
                     if (a.perms && l == 0) atomicAdd(&s_hist[TL.perms() + lehmer], 1u);
                 }
 #pragma unroll
