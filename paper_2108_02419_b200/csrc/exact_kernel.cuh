@@ -48,8 +48,15 @@ namespace bbe {
 
 // LN = false (MT): the field has no lognormal competitor, so every draw takes exactly two words and a
 // tick's offsets follow from one ballot per slot -- no speculative rounds.
+// MT, K > 1 (fields of 33..128 competitors): 4 blocks/SM for K = 2 (126 registers, no spills; the C5
+// field forced to K = 2: 90.8 -> 72.9 ms per 10^6 races, derby20: 116.8 -> 86.3 ms), 2 for K >= 3
+// (4 is slower there: more spills)
+#ifndef BBE_MT_MINBLOCKS_K2
+#define BBE_MT_MINBLOCKS_K2 4
+#endif
 template <int K, int MODE, bool LN = true>
-__global__ void __launch_bounds__(kBlockThreads, MODE == MT ? (K == 1 ? BBE_MT_MINBLOCKS : 2) : 1)
+__global__ void __launch_bounds__(kBlockThreads,
+                                  MODE == MT ? (K == 1 ? BBE_MT_MINBLOCKS : (K == 2 ? BBE_MT_MINBLOCKS_K2 : 2)) : 1)
 exact_kernel(const LaunchArgs a) {
     static_assert(MODE == INJECT || MODE == MT, "exact kernel modes");
     constexpr int kSeg = mt_seg_words(K);  // MT: words per segment (block + side buffer)

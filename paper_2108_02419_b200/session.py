@@ -505,8 +505,14 @@ def make_gpu_session(config, *, mode: str = "mt", predictor=None, look_ahead: bo
                            "prep": prep, "pending": pending}
 
         def _drop(self, ahead) -> None:
+            """Discard a look-ahead launch whose inputs did not come true: wait for it (releasing its
+            launch context) and ignore its outcome -- the reference never runs that prediction, so
+            not even its failure (e.g. a diverged dry run) may surface."""
             self.stats.ahead_misses += 1
-            self.predictor.finish(ahead["pending"], ahead["prep"])  # wait, release its launch context
+            try:
+                self.predictor.finish(ahead["pending"], ahead["prep"])
+            except Exception:  # noqa: BLE001 -- an unused prediction's error is not the session's
+                pass
 
         def _sync_counts(self) -> None:
             self.stats.launches = getattr(self.predictor, "launches", 0)
