@@ -17,12 +17,22 @@ DEFAULT_TICK_LIMIT = 1_000_000  # race.py:21
 MIN_PREFERENCE_FACTOR = 0.01  # race.py:24
 
 
-class RaceConfigError(ValueError):
-    """Invalid race configuration (race.py:27-28)."""
+# When the reference package is installed, the errors here also subclass its own, so reference code
+# (and callers) catching ``racemarket.race.RaceConfigError`` / ``RaceDivergedError`` catch ours too.
+try:  # pragma: no cover - depends on the environment
+    from racemarket.race import RaceConfigError as _RefConfigError
+    from racemarket.race import RaceDivergedError as _RefDivergedError
+except ImportError:
+    _RefConfigError, _RefDivergedError = ValueError, RuntimeError
 
 
-class RaceDivergedError(RuntimeError):
-    """A simulated race exceeded its tick limit (race.py:31-32)."""
+class RaceConfigError(_RefConfigError):
+    """Invalid race configuration (race.py:27-28); a ValueError, and racemarket's when installed."""
+
+
+class RaceDivergedError(_RefDivergedError):
+    """A simulated race exceeded its tick limit (race.py:31-32); a RuntimeError, and racemarket's when
+    installed."""
 
 
 @dataclass(frozen=True)

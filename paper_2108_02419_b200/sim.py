@@ -77,11 +77,20 @@ class DrawStreamError(RuntimeError):
         super().__init__(message)
         self.sim_index = sim_index
 
+    def __reduce__(self):  # picklable across process pools, like batch.BatchRunError
+        return (type(self), (self.sim_index, self.args[0] if self.args else ""))
+
 
 class SimDivergedError(RaceDivergedError):
+    """A dry run exceeded tick_limit; ``sim_index`` is the first failing sim (the reference raises
+    RaceDivergedError from that sim's simulate_from, race.py:402-404)."""
+
     def __init__(self, sim_index: int, message: str):
         super().__init__(message)
         self.sim_index = sim_index
+
+    def __reduce__(self):
+        return (type(self), (self.sim_index, self.args[0] if self.args else ""))
 
 
 # -- ctypes mirrors of the header structs -------------------------------------------------------

@@ -109,3 +109,15 @@ def test_race_section_parser_matches_reference_defaults():
         parse_race({"competitors": [{"id": "a", "steps": {"family": "gamma"}}]})
     with pytest.raises(ConfigError):
         parse_race({"competitors": [], "track_length": 10})
+
+
+def test_sim_errors_pickle_and_keep_the_sim_index():
+    import pickle
+
+    from paper_2108_02419_b200.race import RaceDivergedError
+    from paper_2108_02419_b200.sim import DrawStreamError, SimDivergedError
+
+    for cls in (SimDivergedError, DrawStreamError):
+        e = pickle.loads(pickle.dumps(cls(7, "sim 7 failed")))
+        assert type(e) is cls and e.sim_index == 7 and str(e) == "sim 7 failed"
+    assert issubclass(SimDivergedError, RaceDivergedError) and issubclass(RaceDivergedError, RuntimeError)
