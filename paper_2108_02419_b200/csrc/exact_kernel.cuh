@@ -51,6 +51,9 @@ namespace bbe {
 // MT, K > 1 (fields of 33..128 competitors): 4 blocks/SM for K = 2 (126 registers, no spills; the C5
 // field forced to K = 2: 90.8 -> 72.9 ms per 10^6 races, derby20: 116.8 -> 86.3 ms), 2 for K >= 3
 // (4 is slower there: more spills)
+#ifndef BBE_MT_TWIST_SHFL
+#define BBE_MT_TWIST_SHFL 1  // MT19937 twist with one warp sync per 32-word chunk (shuffled neighbours)
+#endif
 #ifndef BBE_MT_MINBLOCKS_K2
 #define BBE_MT_MINBLOCKS_K2 4
 #endif
@@ -161,6 +164,23 @@ exact_kernel(const LaunchArgs a) {
             const int leader = __ffs(todo) - 1;
             todo &= todo - 1u;
             uint32_t* const t = warp_mt + (leader / W) * kSeg + kSide;
+#if BBE_MT_TWIST_SHFL
+            // one sync per chunk: y = the next word comes from lane + 1's x by shuffle (read before any
+            // write of the chunk), lane 31 reads the next chunk's first word (old until the next chunk
+            // writes it, after this chunk's sync); the last word wraps to the already-new t[0]
+#pragma unroll
+            for (int c0 = 0; c0 < kMtWords; c0 += kWarp) {
+                const int i = c0 + lane;
+                const bool act = i < kMtWords;
+                const uint32_t x = act ? t[i] : 0u;
+                const uint32_t nx = t[c0 + kWarp < kMtWords ? c0 + kWarp : 0];
+                uint32_t y = __shfl_down_sync(0xffffffffu, x, 1);
+                if (i + 1 == c0 + kWarp || i + 1 == kMtWords) y = nx;
+                const uint32_t m = act ? t[i < kMtWords - kMtM ? i + kMtM : i + kMtM - kMtWords] : 0u;
+                if (act) t[i] = mt_mix(x, y, m);
+                __syncwarp();
+            }
+#else
             for (int c0 = 0; c0 < kMtWords; c0 += kWarp) {
                 const int i = c0 + lane;
                 const bool act = i < kMtWords;
@@ -174,6 +194,7 @@ exact_kernel(const LaunchArgs a) {
                 if (act) t[i] = mt_mix(x, y, m);
                 __syncwarp();
             }
+#endif
         }
     };
     // The segment's unread stream is the window seg_mt[wp, kSeg): words saved from earlier blocks
