@@ -601,7 +601,7 @@ int make_plan(DevCtx* ctx, const bbe_race* race, const bbe_competitor* comps, co
     } else {
         pl->NT = rq->mode == BBE_MODE_NATIVE ? pick_ticks(pl->K, scan, expected_ticks(race, comps, st)) : 4;
         pl->fn = rq->mode == BBE_MODE_NATIVE ? pick_native(pl->K, pl->CH, scan, vec2 ? 2 : 4, pl->NT)
-                                             : pick_exact(rq->mode == BBE_MODE_MT ? MT : INJECT, pl->K, ln);
+                                             : pick_exact(rq->mode == BBE_MODE_MT ? MT : INJECT, pl->K, ln, pl->S <= 2);
     }
     if (!pl->fn && rq->mode == BBE_MODE_NATIVE && pl->NT != 4) {
         pl->NT = 4;  // that block length is not built for this layout

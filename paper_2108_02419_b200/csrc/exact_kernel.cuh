@@ -57,9 +57,22 @@ namespace bbe {
 #ifndef BBE_MT_MINBLOCKS_K2
 #define BBE_MT_MINBLOCKS_K2 4
 #endif
-template <int K, int MODE, bool LN = true>
+// MT, K = 1 with at most 2 segments per warp (W >= 11): the block's MT states take little shared
+// memory, so residency is set by registers -- LEAN kernels are built for more blocks per SM (A/B, C5
+// field W = 20, 10^6 races: 5 -> 7 blocks/SM 33.3 -> 29.2 ms; with 4 segments per warp (W = 8, C1) the
+// shared memory caps residency at 4 blocks and fewer registers only cost: 11.9 -> 12.4 ms)
+#ifndef BBE_MT_MINBLOCKS_LEAN
+#define BBE_MT_MINBLOCKS_LEAN 7
+#endif
+#ifndef BBE_MT_MINBLOCKS_LEAN_LN
+#define BBE_MT_MINBLOCKS_LEAN_LN 5  // with lognormal competitors 6 or 7 spill and lose (derby20 24.9 -> 25.8 / 25.1 ms)
+#endif
+template <int K, int MODE, bool LN = true, bool LEAN = false>
 __global__ void __launch_bounds__(kBlockThreads,
-                                  MODE == MT ? (K == 1 ? BBE_MT_MINBLOCKS : (K == 2 ? BBE_MT_MINBLOCKS_K2 : 2)) : 1)
+                                  MODE == MT ? (K == 1 ? (LEAN ? (LN ? BBE_MT_MINBLOCKS_LEAN_LN : BBE_MT_MINBLOCKS_LEAN)
+                                                               : BBE_MT_MINBLOCKS)
+                                                       : (K == 2 ? BBE_MT_MINBLOCKS_K2 : 2))
+                                             : 1)
 exact_kernel(const LaunchArgs a) {
     static_assert(MODE == INJECT || MODE == MT, "exact kernel modes");
     constexpr int kSeg = mt_seg_words(K);  // MT: words per segment (block + side buffer)

@@ -32,7 +32,7 @@ KernelFn pick_native64_scan_kn_ln0(int k, int ch);
 KernelFn pick_native64_scan_kn_ln1(int k, int ch);
 KernelFn pick_native64_free(int k, bool ln, int nt);
 // INJECT / MT (mode: INJECT or MT), K competitors per lane, LN = some lognormal competitor (MT)
-KernelFn pick_exact(int mode, int k, bool ln);
+KernelFn pick_exact(int mode, int k, bool ln, bool lean);  // lean: MT, K = 1, <= 2 segments per warp
 // c_mt_init (init_genrand(19650218)), and the host libm's exp table for MT lognormal steps
 cudaError_t upload_mt_tables(const uint32_t* init624, int exp_ok, const uint64_t* exp_tab256, const double* exp_c8);
 // random.Random(seed) for n sims (per-sim seeds, or derive_seed(master, "run", offset + i) via h_run)

@@ -5,10 +5,12 @@
 
 namespace bbe {
 
-KernelFn pick_exact(int mode, int k, bool ln) {
+KernelFn pick_exact(int mode, int k, bool ln, bool lean) {
     if (mode == MT) {
         switch (k) {
-            case 1: return ln ? exact_kernel<1, MT, true> : exact_kernel<1, MT, false>;
+            case 1:
+                if (lean) return ln ? exact_kernel<1, MT, true, true> : exact_kernel<1, MT, false, true>;
+                return ln ? exact_kernel<1, MT, true> : exact_kernel<1, MT, false>;
             case 2: return ln ? exact_kernel<2, MT, true> : exact_kernel<2, MT, false>;
             case 3: return ln ? exact_kernel<3, MT, true> : exact_kernel<3, MT, false>;
             case 4: return ln ? exact_kernel<4, MT, true> : exact_kernel<4, MT, false>;
