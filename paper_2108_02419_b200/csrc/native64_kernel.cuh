@@ -61,6 +61,9 @@ struct CBool {
     static constexpr bool value = B;
 };
 
+#ifndef BBE_N64_LN_WORDS
+#define BBE_N64_LN_WORDS 1  // lognormal items read their owner's parked Philox words (no second Philox)
+#endif
 #ifndef BBE_N64_TICK_ROLL
 #define BBE_N64_TICK_ROLL 1
 #endif
@@ -93,6 +96,15 @@ __device__ __forceinline__ void normal_pair64(const U4& w, double& n0, double& n
 // h): scale * exp(mu + z * sigma) (random.py lognormvariate / normalvariate) with the Box-Muller pair
 // of the same Philox words a uniform competitor would use.  Parameters are read from the parameter
 // block (L1-resident), not held in registers.
+static __device__ __noinline__ double2 ln_pair_w(const double* P, int n, int c, U4 x) {
+    double z0, z1;
+    normal_pair64(x, z0, z1);
+    const double mu = P[F_MU * n + c], sigma = P[F_SIGMA * n + c], scale = P[F_SCALE * n + c];
+    return make_double2(__dmul_rn(scale, exp(__dadd_rn(mu, __dmul_rn(z0, sigma)))),
+                        __dmul_rn(scale, exp(__dadd_rn(mu, __dmul_rn(z1, sigma)))));
+}
+
+// the same from the counter: Philox words of (h, c, gs) first (the priming draws of run_race)
 static __device__ __noinline__ double2 ln_pair(const double* P, int n, int c, uint32_t h, uint64_t gs, uint32_t k0, uint32_t k1) {
     U4 x{h, (uint32_t)c, (uint32_t)gs, (uint32_t)(gs >> 32)};
 #pragma unroll
@@ -103,11 +115,7 @@ static __device__ __noinline__ double2 ln_pair(const double* P, int n, int c, ui
         k0 += 0x9E3779B9u;
         k1 += 0xBB67AE85u;
     }
-    double z0, z1;
-    normal_pair64(x, z0, z1);
-    const double mu = P[F_MU * n + c], sigma = P[F_SIGMA * n + c], scale = P[F_SCALE * n + c];
-    return make_double2(__dmul_rn(scale, exp(__dadd_rn(mu, __dmul_rn(z0, sigma)))),
-                        __dmul_rn(scale, exp(__dadd_rn(mu, __dmul_rn(z1, sigma)))));
+    return ln_pair_w(P, n, c, x);
 }
 
 // K: competitors per lane; CH: key-row chunks of 4 words (SCAN only); SCAN: some theta > 0 (else
@@ -338,7 +346,18 @@ native64_kernel(const LaunchArgs a) {
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     double d0, d1;
-                    draw_pair(k, ((uint32_t)rt >> 1) + (uint32_t)h, gs, d0, d1);
+                    if constexpr (LN && BBE_N64_LN_WORDS) {
+                        // a lognormal slot parks its raw words (x, y | z, w) in its two draw cells;
+                        // the lane-compacted pass below turns them into the Box-Muller draws
+                        const U4 w = philox_rk(U4{((uint32_t)rt >> 1) + (uint32_t)h, (uint32_t)cidx[k], (uint32_t)gs,
+                                                  (uint32_t)(gs >> 32)}, a.rk);
+                        const double u0 = __dadd_rn(lo[k], __dmul_rn(span[k], unit53(w.x, w.y)));
+                        const double u1 = __dadd_rn(lo[k], __dmul_rn(span[k], unit53(w.z, w.w)));
+                        d0 = lognorm[k] ? __hiloint2double((int)w.y, (int)w.x) : u0;
+                        d1 = lognorm[k] ? __hiloint2double((int)w.w, (int)w.z) : u1;
+                    } else {
+                        draw_pair(k, ((uint32_t)rt >> 1) + (uint32_t)h, gs, d0, d1);
+                    }
                     BBE_CHECK(in_dyn_smem(s_draw + (k * NT + 2 * h + 1) * kWarp, s_dyn));
                     s_draw[(k * NT + 2 * h) * kWarp] = d0;
                     s_draw[(k * NT + 2 * h + 1) * kWarp] = d1;
@@ -363,9 +382,16 @@ native64_kernel(const LaunchArgs a) {
                     if (j < items && s_item < a.n_sims) {
                         const int c = s_lnc[i];
                         const int kk = c / W, owner = sg * W + (c - kk * W);
+                        double* col = s_draw - lane + owner;
+#if BBE_N64_LN_WORDS
+                        const double q0 = col[(kk * NT + 2 * h) * kWarp], q1 = col[(kk * NT + 2 * h + 1) * kWarp];
+                        const U4 wq{(uint32_t)__double2loint(q0), (uint32_t)__double2hiint(q0),
+                                    (uint32_t)__double2loint(q1), (uint32_t)__double2hiint(q1)};
+                        const double2 d = ln_pair_w(P, n, c, wq);
+#else
                         const double2 d = ln_pair(P, n, c, ((uint32_t)rt_item >> 1) + (uint32_t)h,
                                                   (uint64_t)(a.sim_offset + s_item), a.rk[0], a.rk[1]);
-                        double* col = s_draw - lane + owner;
+#endif
                         BBE_CHECK(owner >= 0 && owner < kWarp && kk < K && h < NT / 2 &&
                                   in_dyn_smem(col + (kk * NT + 2 * h + 1) * kWarp, s_dyn));
                         col[(kk * NT + 2 * h) * kWarp] = d.x;
