@@ -378,6 +378,22 @@ int native64_flags(const bbe_race* race, const bbe_competitor* comps, const bbe_
     double step_min = min_free;
     if (scan) step_min = small_mult ? 0.0 : std::min(min_free, min_prev);
     if (!(step_min > std::ldexp(B, -52))) fl |= kN64Guard;
+    // kN64NoTie: a blocked lane has gap <= theta_max and its front ahead at a position >= the smallest
+    // racing start position (positions never decrease); when that exceeds 2 theta_max, p_front > 2 gap
+    // always holds, so distinct positions can never round to the same gap (native64_kernel.cuh)
+#ifndef BBE_N64_TIE_FLAG
+#define BBE_N64_TIE_FLAG 1
+#endif
+    if (BBE_N64_TIE_FLAG && !st->from_start) {
+        double theta_max = 0.0, min_pos = INFINITY;
+        bool finite = true;
+        for (int c = 0; c < n; ++c) {
+            finite = finite && std::isfinite(comps[c].theta);
+            theta_max = std::max(theta_max, comps[c].theta);
+            if (st->finish_ticks[c] < 0) min_pos = std::min(min_pos, st->positions[c]);
+        }
+        if (finite && min_pos > 2.0 * theta_max) fl |= kN64NoTie;
+    }
     return fl;
 }
 

@@ -143,6 +143,7 @@ constexpr int kXSlot = 66;         // exact modes: doubles per position row (S*r
 // NATIVE64 host flags
 constexpr int kN64RespVar = 1;  // some competitor's early and late multipliers differ
 constexpr int kN64Guard = 2;    // fl(pos + step) == pos is possible: keep the nextafter guard
+constexpr int kN64NoTie = 4;    // no blocked lane can face a gap-rounding tie (every racing position > 2 max theta)
 __host__ __device__ inline size_t smem_bytes(int mode, int hist_len_even, int K, int S, int WP, int nt64 = 0) {
     size_t b = (size_t)hist_len_even * 8;
     if (mode == NATIVE || (mode == NATIVE64 && WP > 0)) {  // NATIVE64 scan-free kernels: no key rows (WP 0)

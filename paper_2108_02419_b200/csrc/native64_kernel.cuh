@@ -42,7 +42,9 @@
 // Philox rounds thus appear once in the binary instead of once per unrolled tick (ncu round 2: with
 // them inlined per tick the derby20 kernel spent 76 % of its stall samples on instruction fetch).
 //
-// Host flags (bbe_sim.cu native64_flags): kN64RespVar -- some competitor's early and late multipliers
+// Host flags (bbe_sim.cu native64_flags): kN64NoTie -- every racing start position exceeds twice the
+// largest theta, so no blocked lane can face a gap-rounding tie and that test is skipped (C2: -0.5 %).
+// kN64RespVar -- some competitor's early and late multipliers
 // differ, so the responsiveness test `pos < breakpoint*L` (race.py:93-96) runs per tick; without it the
 // early value is used (bit-identical, the two are equal).  kN64Guard -- the `p == pos -> nextafter`
 // guard (race.py:310-313) can fire: off when every possible step exceeds 2^-52 of the largest
@@ -191,6 +193,8 @@ native64_kernel(const LaunchArgs a) {
     }
     const double L = a.L;
     const double C64 = a.key_c64;
+    // the gap-rounding tie test (below) is needed only when some racing position can be <= 2 theta
+    const bool tie_chk = !(a.n64_flags & kN64NoTie);
     const uint32_t cl = (uint32_t)l - a.key_sub64;  // v = funnel * 32 + cl = (key << 5) | l
 
     // ---- segment bookkeeping ----
@@ -467,10 +471,11 @@ native64_kernel(const LaunchArgs a) {
                 }
                 bool need_exact = coll;
 #pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    gap[k] = ahead[k] ? __dsub_rn(pfpos[k], pos[k]) : CUDART_INF;
-                    // a blocked lane whose front could be a gap-rounding tie (exact_kernel.cuh)
-                    need_exact |= racing[k] && ahead[k] && !(gap[k] > th[k]) && !(pfpos[k] > __dmul_rn(2.0, gap[k]));
+                for (int k = 0; k < K; ++k) gap[k] = ahead[k] ? __dsub_rn(pfpos[k], pos[k]) : CUDART_INF;
+                if (tie_chk) {
+#pragma unroll
+                    for (int k = 0; k < K; ++k)  // a blocked lane whose front could be a gap-rounding tie
+                        need_exact |= racing[k] && ahead[k] && !(gap[k] > th[k]) && !(pfpos[k] > __dmul_rn(2.0, gap[k]));
                 }
                 if (__any_sync(0xffffffffu, need_exact)) {
                     // the reference's loop (race.py:244-264) over the segment's start-of-tick positions
@@ -573,7 +578,7 @@ native64_kernel(const LaunchArgs a) {
             }
         };
         if (SCAN) __syncwarp();  // key rows: the previous block's reads precede this block's writes
-        const int fl = a.n64_flags;
+        const int fl = a.n64_flags & (kN64RespVar | kN64Guard);
         if (fl == (kN64RespVar | kN64Guard)) run_block(CBool<true>{}, CBool<true>{});
         else if (fl == kN64RespVar) run_block(CBool<true>{}, CBool<false>{});
         else if (fl == kN64Guard) run_block(CBool<false>{}, CBool<true>{});
