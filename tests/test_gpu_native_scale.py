@@ -9,12 +9,14 @@ fields:
   C3  20 x U(10,20), L = 2000, from the start line (configs[2] and the C5 field of configs[4])
   derby20  derby.json resized to 20 (blocking, lognormal, closers), from the start line
   C2  derby10 mid-race (tick 65) continuation (configs[1])
+  lognormal8  every runner lognormal (Box-Muller vs the reference's Kinderman-Monahan), from the start
+  blocking12  every runner blocking (theta = 6), from the start
 Tests: two-sample binomial z on every win probability and every rank-marginal cell, Bonferroni over
 all cells of the file at alpha = 0.01 (tests/test_acceptance.py:394-424 calibrates the same way), and
 a z test on the mean race length in competitor-timesteps (variance from a recorded MT subsample).
 
 Scale probe (C5 field, 10^9 vs 10^9): NATIVE (FP32 state, 23-bit draws) against NATIVE64 -- the
-binomial standard error of a difference is ~2e-5 there, the tightest bound any BASELINE config sets;
+binomial standard error of a difference is ~1e-5 there, the tightest bound any BASELINE config sets;
 FP32 bias (position rounding near L = 2000, the overshoot tie-break, 23-bit uniforms) must stay below it.
 Set BBE_REPORT=path to write the measured differences as JSON (DESIGN.md §2 quotes them).
 """
@@ -45,12 +47,30 @@ def uniform_field(n):
     return RaceConfig(2000.0, tuple(Competitor(f"c{i + 1}", UniformSteps(10.0, 20.0)) for i in range(n)))
 
 
+def lognormal_field(n=8):
+    """Every runner lognormal (the Box-Muller law of the Philox modes against the reference's
+    Kinderman-Monahan normalvariate), mixed mu / sigma / scale, a few blockers."""
+    from paper_2108_02419_b200.race import LogNormalSteps
+
+    comps = tuple(Competitor(f"l{i}", LogNormalSteps(2.3 + 0.05 * i, 0.15 + 0.04 * (i % 4), 1.0 + 0.1 * (i % 3)),
+                             theta=6.0 if i % 3 == 0 else 0.0) for i in range(n))
+    return RaceConfig(1500.0, comps)
+
+
+def blocking_field(n=12):
+    """Every runner blocks (theta = 6): the front-runner scan and blocked steps on every tick."""
+    return RaceConfig(1200.0, tuple(Competitor(f"b{i}", UniformSteps(9.0 + 0.3 * i, 16.0), theta=6.0,
+                                               preference=0.1 * (i % 10), pref_sensitivity=0.3)
+                                    for i in range(n)), conditions=0.4)
+
+
 def fields():
     g = c2()
     derby10 = config_from_dict(g["config"])
     return {"C1": (None, uniform_field(5)), "C3": (None, uniform_field(20)),
             "derby20": (None, resize_race(resize_race(derby10, 5), 20)),
-            "C2": (state_from_dict(g["state"]), derby10)}
+            "C2": (state_from_dict(g["state"]), derby10),
+            "lognormal8": (None, lognormal_field()), "blocking12": (None, blocking_field())}
 
 
 # every cell tested in this file: per field and mode, n wins + n^2 rank cells + 1 mean-ct test; plus
@@ -87,7 +107,7 @@ def mt_runs():
 
 
 @pytest.mark.parametrize("mode", ["native64", "native"])
-@pytest.mark.parametrize("name", ["C1", "C3", "derby20", "C2"])
+@pytest.mark.parametrize("name", ["C1", "C3", "derby20", "C2", "lognormal8", "blocking12"])
 def test_native_modes_match_reference_stream_at_scale(mt_runs, name, mode):
     state, cfg = fields()[name]
     n = cfg.n_competitors
