@@ -1415,7 +1415,9 @@ static const NcclApi& nccl_api() {
     return api;
 }
 
-// One communicator clique per device count (devices 0..k-1), created once and kept for the process.
+// One communicator clique per device count (devices 0..k-1), created once and kept for the process
+// (not destroyed at exit: ncclCommDestroy from a static destructor would race the CUDA runtime's own
+// teardown; the driver reclaims the resources with the process).
 static std::mutex g_nccl_mu;
 static std::map<int, std::vector<ncclComm_t>> g_nccl_comms;
 
