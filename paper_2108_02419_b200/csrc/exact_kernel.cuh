@@ -98,7 +98,11 @@ exact_kernel(const LaunchArgs a) {
     uint32_t* const mt = seg_mt + kSide;  // the 624-word MT19937 block
     // start-of-tick front-runner keys, per warp: [parity][slot] rows of kKRow words, segment at
     // seg * WPK (4-word chunks, padding words 0), idle lanes write the row's last word
-    const int CHK = (W + 3) >> 2, WPK = 4 * CHK;
+    // segments of 8 <= W <= 12 lanes (at most 4 per warp) get 12-word rows (3 chunks, zero padding past
+    // W), so their scan is a fixed 3-chunk loop; other widths use ceil(W / 4) chunks (INJECT runs W < 8,
+    // up to 32 segments per warp, whose 12-word rows would overrun the key row)
+    const bool kNarrow = W >= 8 && W <= 12;
+    const int CHK = kNarrow ? 3 : (W + 3) >> 2, WPK = 4 * CHK;
     double* const xrows_all = reinterpret_cast<double*>(smem_w + (MODE == MT ? kWarpsPerBlock * S * kSeg : 0));
     uint32_t* const krows = reinterpret_cast<uint32_t*>(xrows_all + warp * 2 * K * kXSlot);
     constexpr int kKRow = 2 * kXSlot;  // words per key row (the double row's footprint; S * WPK <= 36)
@@ -648,13 +652,18 @@ exact_kernel(const LaunchArgs a) {
                         uint32_t b0 = 0xffffffffu, b1 = 0xffffffffu;
                         const uint4* r4 = reinterpret_cast<const uint4*>(kr + par + kk * kKRow);
                         BBE_CHECK(in_dyn_smem(r4 + CHK - 1, s_dyn));
-#pragma unroll 3
-                        for (int c = 0; c < CHK; ++c) {
-                            const uint4 q = r4[c];
+                        auto chunk = [&](const uint4 q) {
                             b0 = min(b0, q.x + nk);
                             b1 = min(b1, q.y + nk);
                             b0 = min(b0, q.z + nk);
                             b1 = min(b1, q.w + nk);
+                        };
+                        if (kNarrow) {
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) chunk(r4[c]);
+                        } else {
+#pragma unroll 2
+                            for (int c = 0; c < CHK; ++c) chunk(r4[c]);
                         }
                         const uint32_t t = min(b0, b1);
                         const uint32_t vf = t - nk;
