@@ -51,6 +51,12 @@ namespace bbe {
 // MT, K > 1 (fields of 33..128 competitors): 4 blocks/SM for K = 2 (126 registers, no spills; the C5
 // field forced to K = 2: 90.8 -> 72.9 ms per 10^6 races, derby20: 116.8 -> 86.3 ms), 2 for K >= 3
 // (4 is slower there: more spills)
+#ifndef BBE_MT_LIMIT_PRED
+#define BBE_MT_LIMIT_PRED 1  // the per-tick limit test without a branch (C2 MT 2.160 -> 2.131 ms)
+#endif
+#ifndef BBE_MT_LT_TABLE
+#define BBE_MT_LT_TABLE 1  // log2 T from a per-launch 2-bit table (C2 MT 2.160 -> 2.125 ms; both: 2.090)
+#endif
 #ifndef BBE_MT_TWIST_SHFL
 #define BBE_MT_TWIST_SHFL 1  // MT19937 twist with one warp sync per 32-word chunk (shuffled neighbours)
 #endif
@@ -119,6 +125,14 @@ exact_kernel(const LaunchArgs a) {
     const uint32_t* const kr = krows + (lane_on ? seg * WPK : 0);
     const double C64 = a.key_c64;
     const uint32_t cl = (uint32_t)l - a.key_sub64;  // v = funnel * 32 + cl = (key << 5) | l
+#if BBE_MT_LT_TABLE
+    // the K = 1 trial pass's log2 T for m pending lognormal draws (m < 32), two bits per m
+    uint64_t lt_tab = 0;
+    for (int mm = 1; mm < 32; ++mm) {
+        const int v = (8 * mm <= W) ? 3 : (4 * mm <= W) ? 2 : (2 * mm <= W) ? 1 : 0;
+        lt_tab |= (uint64_t)v << (2 * mm);
+    }
+#endif
     __syncthreads();
 
     // ---- per-slot constants (the lane->competitor map is fixed for the kernel) ----
@@ -282,7 +296,11 @@ exact_kernel(const LaunchArgs a) {
                 const int used_all = 2 * (__popc(pm) + __popc(lm));
                 const int m = __popc(lm);
                 // T: the largest power of two <= kMtMaxTrials with m*T <= W (shifts, no division)
+#if BBE_MT_LT_TABLE
+                const int lt = (int)((lt_tab >> (2 * m)) & 3ull);  // lt_tab: the expression below per m
+#else
                 const int lt = (8 * m <= W) ? 3 : (4 * m <= W) ? 2 : (2 * m <= W) ? 1 : 0;
+#endif
                 const int T = 1 << lt;
                 const int ti = l >> lt, tj = l & (T - 1);
                 if (pend && lognorm[0]) ln_off[base + __popc(lm & lt_mask)] = off;
@@ -602,11 +620,20 @@ exact_kernel(const LaunchArgs a) {
             if (rmask == 0u) break;  // every segment finished inside this block
 
             // tick-limit check before the advance (race.py:381-386, 402-404)
+#if BBE_MT_LIMIT_PRED
+            {  // predicated, no branch
+                const bool lim = seg_running && rt >= a.limit;
+                diverged |= lim;
+#pragma unroll
+                for (int k = 0; k < K; ++k) racing[k] = racing[k] && !lim;
+            }
+#else
             if (seg_running && rt >= a.limit) {
                 diverged = true;
 #pragma unroll
                 for (int k = 0; k < K; ++k) racing[k] = false;
             }
+#endif
 
             // ---- front runner (race.py:244-264) ----
             // Coarse keys, as native64_kernel.cuh: key = mantissa bits 51..26 of pos + C64 (the host's
