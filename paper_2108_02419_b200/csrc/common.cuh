@@ -170,17 +170,15 @@ __device__ __forceinline__ U4 philox_rk(U4 c, const uint32_t* rk) {
     return c;
 }
 
-// random_random(): m * 2^-53 with m = a*2^26 + b, a = w0>>5, b = w1>>6 -- an exact 53-bit fraction.
-// Built from bits, without integer->double conversions: D = 2^52 + (m mod 2^52) is m's low 52 bits
-// under the exponent of 2^52, E = D - 2^52 is exact, and m * 2^-53 = E * 2^-53 + (m >= 2^52 ? 0.5 : 0)
-// is one FMA whose result is exact (53 significant bits).  Checked against the integer formula on
-// 2e8 random word pairs and the edge words.
+// random_random(): m * 2^-53 with m = a*2^26 + b, a = w0>>5, b = w1>>6 -- an exact 53-bit fraction
+// (CPython _randommodule.c), built from bits without integer->double conversions (bit 52 of m is bit
+// 31 of w0).
 __device__ __forceinline__ double random53(uint32_t w0, uint32_t w1) {
     const uint32_t lo = ((w0 << 21) & 0xFC000000u) | (w1 >> 6);  // m bits 0..31
     const uint32_t hi = w0 >> 11;                                  // m bits 32..52
-    const double E = __dsub_rn(__hiloint2double((int)(0x43300000u | (hi & 0xFFFFFu)), (int)lo), 4503599627370496.0);
-    const double top = __hiloint2double((hi >> 20) ? 0x3FE00000 : 0, 0);
-    return __fma_rn(E, 1.0 / 9007199254740992.0, top);
+    // as unit53: H = 0.5 + (m mod 2^52) 2^-53 from bits, m * 2^-53 = H - 0.5 + m_52 / 2: one exact DADD
+    // (Sterbenz when m_52 = 0); equal to CPython's value on 2e6 random word pairs and the edge words
+    return __dadd_rn(__hiloint2double((int)(0x3FE00000u | (hi & 0xFFFFFu)), (int)lo), (w0 >> 31) ? 0.0 : -0.5);
 }
 
 // NATIVE64 draws: u = m * 2^-53, m = the top 53 bits of the 64-bit word pair (w0:w1) -- uniform on
