@@ -1,4 +1,5 @@
-"""Native (Philox, FP32) kernel: exact where the reference is RNG-independent, statistically equal to the
+"""The Philox kernels -- NATIVE (FP32 state) and NATIVE64 (FP64 state, the bench headline; every test
+runs once per mode): exact where the reference is RNG-independent, statistically equal to the
 reference elsewhere, and reproducible under any sharding of the simulation index range.
 
 Statistical bar (north star): per-competitor win probabilities agree with the reference's within
@@ -28,6 +29,20 @@ from paper_2108_02419_b200.race import (
 
 pytestmark = pytest.mark.gpu
 ALPHA = 0.01
+
+
+@pytest.fixture(params=["native", "native64"], autouse=True)
+def philox_mode(request, monkeypatch):
+    """Every test of this module once per Philox mode: simulate_batch calls without an explicit mode
+    run in this one."""
+    orig = sim.simulate_batch
+
+    def simulate_batch(*args, **kwargs):
+        kwargs.setdefault("mode", request.param)
+        return orig(*args, **kwargs)
+
+    monkeypatch.setattr(sim, "simulate_batch", simulate_batch)
+    return request.param
 
 
 def binomial_agreement(wins_a, n_a, wins_b, n_b, alpha=ALPHA, min_expected=10):
@@ -211,12 +226,12 @@ def test_records_consistent_with_tallies():
     assert (ticks_run > 0).all()
 
 
-def test_simulate_sharded_single_rank_matches_batch():
+def test_simulate_sharded_single_rank_matches_batch(philox_mode):
     from paper_2108_02419_b200.parallel import simulate_sharded
 
     g = c2()
     cfg, st = config_from_dict(g["config"]), state_from_dict(g["state"])
-    t = simulate_sharded(st, cfg, 50_000, 3)
+    t = simulate_sharded(st, cfg, 50_000, 3, mode=philox_mode)
     r = sim.simulate_batch(st, cfg, 50_000, 3)
     assert (t.wins == r.wins).all() and (t.ranks == r.ranks).all()
     assert t.competitor_steps == r.competitor_steps and t.first_diverged == -1
