@@ -1,4 +1,4 @@
-"""Native mode against MT mode on random configs at GPU scale.
+"""The Philox modes (NATIVE, NATIVE64) against MT mode on random configs at GPU scale.
 
 MT mode is bit-identical to the reference (tests/test_gpu_mt.py, test_gpu_fuzz.py), so it stands in
 for the reference at sample sizes the CPU cannot reach.  For each random field (mixed step families,
@@ -18,6 +18,19 @@ from paper_2108_02419_b200 import sim
 from paper_2108_02419_b200.race import Competitor, LogNormalSteps, RaceConfig, Responsiveness, UniformSteps
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(params=["native", "native64"], autouse=True)
+def philox_mode(request, monkeypatch):
+    """Both Philox modes (FP32 and FP64 state): simulate_batch calls without an explicit mode run in it."""
+    orig = sim.simulate_batch
+
+    def simulate_batch(*args, **kwargs):
+        kwargs.setdefault("mode", request.param)
+        return orig(*args, **kwargs)
+
+    monkeypatch.setattr(sim, "simulate_batch", simulate_batch)
+    return request.param
 
 
 def random_field(rng: random.Random) -> RaceConfig:
