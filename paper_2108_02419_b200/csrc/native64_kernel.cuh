@@ -63,6 +63,13 @@ struct CBool {
     static constexpr bool value = B;
 };
 
+// BBE_N64_F32_PROBE builds (tools/f32_probe.py, never the product): every draw, step and position
+// rounded to FP32 after each FP64 operation -- the FP32-state arithmetic on the very same Philox
+// draws, to count the finish orders the state precision alone changes.
+#ifndef BBE_N64_F32_PROBE
+#define BBE_N64_F32_PROBE 0
+#endif
+#define BBE_P32(x) (BBE_N64_F32_PROBE ? (double)__double2float_rn(x) : (x))
 #ifndef BBE_N64_LN_WORDS
 #define BBE_N64_LN_WORDS 1  // lognormal items read their owner's parked Philox words (no second Philox)
 #endif
@@ -214,8 +221,8 @@ native64_kernel(const LaunchArgs a) {
     // the uniform step draws of slot k for ticks 2h and 2h + 1 of the sim (counter word 0 = h)
     auto draw_pair = [&](int k, uint32_t h, uint64_t gs, double& d0, double& d1) {
         const U4 w = philox_rk(U4{h, (uint32_t)cidx[k], (uint32_t)gs, (uint32_t)(gs >> 32)}, a.rk);
-        d0 = __dadd_rn(lo[k], __dmul_rn(span[k], unit53(w.x, w.y)));
-        d1 = __dadd_rn(lo[k], __dmul_rn(span[k], unit53(w.z, w.w)));
+        d0 = BBE_P32(__dadd_rn(lo[k], __dmul_rn(span[k], unit53(w.x, w.y))));
+        d1 = BBE_P32(__dadd_rn(lo[k], __dmul_rn(span[k], unit53(w.z, w.w))));
     };
 
     auto load_sim = [&](bool do_it) {
@@ -237,7 +244,7 @@ native64_kernel(const LaunchArgs a) {
                 double d, d1;
                 if (LN && lognorm[k]) d = ln_pair(P, n, cidx[k], 0xFFFFFFFFu, gs, a.rk[0], a.rk[1]).x;
                 else draw_pair(k, 0xFFFFFFFFu, gs, d, d1);
-                prev[k] = __dmul_rn((0.0 < bp[k]) ? rpE[k] : rpL[k], d);
+                prev[k] = BBE_P32(__dmul_rn((0.0 < bp[k]) ? rpE[k] : rpL[k], d));
             }
         }
     };
@@ -534,12 +541,12 @@ native64_kernel(const LaunchArgs a) {
                 double step;
                 const double dk = s_draw[(k * NT + tj) * kWarp];
                 if (!SCAN || fr[k]) {
-                    step = __dmul_rn(early ? rpE[k] : rpL[k], dk);
+                    step = BBE_P32(__dmul_rn(early ? rpE[k] : rpL[k], dk));
                 } else {
                     const double m = (pf[k] < prev[k]) ? pf[k] : prev[k];  // Python min(prev_c, prev_front)
-                    step = __dmul_rn(early ? eE[k] : eL[k], m);
+                    step = BBE_P32(__dmul_rn(early ? eE[k] : eL[k], m));
                 }
-                pnew[k] = __dadd_rn(pos[k], step);
+                pnew[k] = BBE_P32(__dadd_rn(pos[k], step));
                 if constexpr (decltype(guard)::value) eq_any |= racing[k] && pnew[k] == pos[k];
                 prev[k] = step;  // a finished competitor's previous step is never read again
             }
